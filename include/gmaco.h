@@ -1,0 +1,264 @@
+/*
+ * gmaco.h — C ABI of the B200-native GMACO-P engine.
+ *
+ * This is the drop-in boundary for the reference simulator's hot path
+ * (reference = /root/reference/proj, "macosim", C++20, CPU-only).  Every entry
+ * point below names the reference interface it replaces.  The ABI is plain C:
+ * opaque handle, POD parameter blocks, raw pointers + sizes, int status codes,
+ * no exceptions, no torch types.
+ *
+ *   status 0 = ok, 1 = validation error (reference ValidationError,
+ *   net.hpp:24-27), 2 = runtime / CUDA error.  These mirror the CLI exit codes
+ *   of the reference (tools/main.cpp:149-158).  gmaco_last_error() returns the
+ *   message of the last failing call on a handle (or the last failing create).
+ *
+ * Units are the reference's: lengths int64 millimetres (net.hpp:17), pheromone
+ * int64 micro-units (pheromone.hpp:13-21), time in whole steps of dt seconds.
+ */
+#ifndef GMACO_H_
+#define GMACO_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMACO_ABI_VERSION 1
+
+enum gmaco_status { GMACO_OK = 0, GMACO_EVALIDATION = 1, GMACO_ERUNTIME = 2 };
+
+/* Algorithm (engine.hpp:17) plus the colony extension of the north star. */
+enum gmaco_algorithm {
+  GMACO_DIJKSTRA = 0,
+  GMACO_ACO = 1,
+  GMACO_MACO = 2,
+  GMACO_MACO_P = 3,
+  GMACO_COLONY = 4 /* K-ant ACO colonies per vehicle, best-tour argmin */
+};
+enum gmaco_controller { GMACO_FIXED = 0, GMACO_ADAPTIVE = 1, GMACO_PREEMPTIVE = 2 }; /* engine.hpp:18 */
+enum gmaco_spawn { GMACO_ALL_AT_START = 0, GMACO_UNIFORM_WINDOW = 1 };               /* engine.hpp:19 */
+enum gmaco_od { GMACO_OD_UNIFORM = 0, GMACO_OD_BLOCKS = 1 };                          /* engine.hpp:20 */
+enum gmaco_deviation { GMACO_DEV_GLOBAL = 0, GMACO_DEV_EDGE_OCCUPANCY = 1 };          /* routing.hpp:12 */
+enum gmaco_rng { GMACO_RNG_PHILOX = 0, GMACO_RNG_REFERENCE = 1 };
+enum gmaco_deposit { GMACO_DEPOSIT_COMPLETION = 0, GMACO_DEPOSIT_BEST_TOUR = 1, GMACO_DEPOSIT_NONE = 2 };
+enum gmaco_vehicle_state {                                                           /* engine.hpp:52-59 */
+  GMACO_PENDING = 0, GMACO_AT_NODE = 1, GMACO_ON_EDGE = 2,
+  GMACO_QUEUED = 3, GMACO_ARRIVED = 4, GMACO_RETIRED = 5
+};
+enum gmaco_distance_kind {
+  GMACO_DIST_DENSE = 0, /* reference DistanceTable layout, row u, column v (net.hpp:84-102) */
+  GMACO_DIST_GRID = 1,  /* closed-form Manhattan distance of a generate_grid network (net.cpp:208-244) */
+  GMACO_DIST_TARGETS = 2 /* exact distances to a bounded destination set, computed by the engine */
+};
+
+#define GMACO_PHASES 8 /* kPhaseCount, signals.hpp:12 */
+
+/* PheromoneParams, pheromone.hpp:23-42. */
+typedef struct {
+  double tau_init_lo, tau_init_hi;
+  double delta_inc, delta_dec;
+  double rho;
+  double tau_min, tau_max;
+  double aco_deposit_q;
+  int32_t decrement_siblings_only;
+  int32_t _pad;
+} gmaco_pheromone_params;
+
+/* SignalParams, signals.hpp:14-22. */
+typedef struct {
+  int32_t th_max;
+  int32_t fixed_cycle_order[GMACO_PHASES];
+  int32_t _pad;
+  double t_max;
+  double green_duration_s;
+  double saturation_flow;
+} gmaco_signal_params;
+
+/* RoutingParams, routing.hpp:14-23. */
+typedef struct {
+  int64_t deviation_threshold;
+  int32_t deviation_mode; /* gmaco_deviation */
+  int32_t progress_filter;
+  double aco_alpha, aco_beta;
+} gmaco_routing_params;
+
+/* Colony extension (north star; not in the reference).
+ * With ants=1, hop_limit=1, rng=GMACO_RNG_REFERENCE, congestion=0,
+ * deposit=GMACO_DEPOSIT_COMPLETION, congestion_evaporation=0 the colony run is
+ * bit-identical to the reference Algorithm::Aco run (routing.cpp:77-115). */
+typedef struct {
+  int32_t ants;                   /* K ants per vehicle per iteration, >= 1 */
+  int32_t hop_limit;              /* 0 = walk to the destination, h > 0 = stop after h hops */
+  int32_t max_hops;               /* tour cap (0 = node_count - 1); longer tours fail */
+  int32_t rng;                    /* gmaco_rng */
+  int32_t congestion;             /* 1: roulette weight x 1/(1+load), tour cost len x (1+load) */
+  int32_t deposit;                /* gmaco_deposit */
+  int32_t congestion_evaporation; /* 1: tau <- max(tau_min, evap(tau) - dec * occupancy) */
+  int32_t replan_all;             /* 1: every active vehicle's colony runs every iteration */
+} gmaco_colony_params;
+
+/* SimConfig, engine.hpp:29-50 (network / distance passed separately). */
+typedef struct {
+  int32_t algorithm;  /* gmaco_algorithm */
+  int32_t controller; /* gmaco_controller */
+  int32_t vehicle_count;
+  int32_t spawn; /* gmaco_spawn */
+  int32_t spawn_window_steps;
+  int32_t od_pattern; /* gmaco_od */
+  double dt_s;
+  int64_t max_steps;
+  uint64_t seed;
+  double decision_latency_s;
+  double od_bias;
+  const int32_t* od_block_a;
+  const int32_t* od_block_b;
+  int32_t od_block_a_len, od_block_b_len;
+  double speed_min_mps, speed_max_mps;
+  gmaco_pheromone_params pheromone;
+  gmaco_signal_params signal;
+  gmaco_routing_params routing;
+  gmaco_colony_params colony;
+} gmaco_sim_config;
+
+/* Road network as SoA: RoadNode / RoadEdge (net.hpp:29-43).  Edge i has id i;
+ * node i has id i (the reference requires dense ids, net.cpp:44-63). */
+typedef struct {
+  int32_t node_count;
+  int32_t edge_count;
+  const uint8_t* signalized;      /* [node_count] */
+  const int32_t* edge_from;       /* [edge_count] */
+  const int32_t* edge_to;         /* [edge_count] */
+  const int64_t* edge_length_mm;  /* [edge_count] */
+  const int32_t* edge_lanes;      /* [edge_count] */
+} gmaco_graph_desc;
+
+/* Distance service: what the candidate filter reads (routing.cpp:16-30). */
+typedef struct {
+  int32_t kind;            /* gmaco_distance_kind */
+  int32_t grid_rows, grid_cols;
+  const int64_t* dist_mm;  /* DENSE: [n*n], dist(u,v) at u*n+v, INT64_MAX = unreachable */
+  const int32_t* targets;  /* TARGETS: destination node ids (vehicles must end there) */
+  int32_t target_count;
+  int32_t _pad;
+} gmaco_distance_desc;
+
+/* RunResult, engine.hpp:92-107 (diagnostic strings are rebuilt by the host
+ * wrapper from retired_vid / retired_node, engine.cpp:416-421). */
+typedef struct {
+  double mean_travel_s, mean_wait_s, mean_queue_len;
+  int32_t max_edge_occupancy;
+  int32_t completed_count;
+  int32_t retired_count;
+  int32_t _pad;
+  int64_t steps_executed;
+  int64_t wall_clock_ms;
+} gmaco_run_result;
+
+/* Vehicle snapshot (Vehicle, engine.hpp:61-90); any pointer may be NULL. */
+typedef struct {
+  int32_t *origin, *dest;
+  double* speed_mps;
+  int64_t* advance_mm;
+  uint8_t* state;
+  int32_t *at_node, *on_edge;
+  int64_t *progress_mm, *overshoot_mm;
+  int32_t* queued_phase;
+  int64_t *queue_joined_step, *depart_step, *arrive_step, *latency_debt_us;
+  int64_t *driving_steps, *queued_steps, *latency_steps;
+  int32_t *decisions, *deviations;
+  int64_t* path_length_mm;
+} gmaco_vehicle_view;
+
+/* Signal snapshot (SignalState, signals.hpp:39-52); any pointer may be NULL.
+ * Per-phase arrays are [signal_count * 8]; queue_vid lists every queue FIFO
+ * head-to-tail, signal-major then phase, sized by the sum of queue_len. */
+typedef struct {
+  int32_t* node;
+  int32_t *green, *cycle_cursor, *discharge_lanes;
+  int64_t* green_elapsed_steps;
+  double* green_elapsed_s;
+  int32_t* queue_len;
+  double *head_wait_s, *service_remainder;
+  int32_t* queue_vid;
+  int64_t* queue_enqueue_step;
+} gmaco_signal_view;
+
+/* Device work counters (the bench metric's units). */
+typedef struct {
+  int64_t ant_steps;       /* next-hop selections (routing.cpp:16-115 equivalents) */
+  int64_t vehicle_routes;  /* complete best-of-K tours constructed */
+  int64_t decisions;       /* engine routing decisions (StepDecision count) */
+  int64_t candidates;      /* filtered candidates visited (sum of c) */
+  int64_t degree_sum;      /* out-edges scanned (sum of d) */
+} gmaco_counters;
+
+typedef struct gmaco_engine gmaco_engine;
+
+/* Library version / ABI check. */
+int32_t gmaco_abi_version(void);
+
+/* Builds the device world: CSR road graph, distance service, pheromone field,
+ * signal states, fleet.  Replaces init_world (engine.cpp:116-144) +
+ * spawn_vehicles (engine.cpp:71-114) + RoadNetwork validation (net.cpp:38-98).
+ * `device` is the CUDA ordinal. */
+int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist,
+                 const gmaco_sim_config* cfg, int32_t device, gmaco_engine** out);
+
+/* Multi-GPU: shard the fleet across `world` ranks (partition_entities,
+ * parallel.cpp:8-21) and exchange the per-step vectors over NCCL.  `nccl_id`
+ * is the 128-byte ncclUniqueId of rank 0.  Call before the first step. */
+int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id);
+int gmaco_nccl_unique_id(void* out128);
+
+/* Executes up to `steps` engine steps (sequential_step, engine.cpp:352-400),
+ * stopping early once finished() (engine.cpp:146-152) holds.  `executed`
+ * (may be NULL) receives the number of steps run. */
+int gmaco_step(gmaco_engine* h, int64_t steps, int64_t* executed);
+/* finished(w) (engine.cpp:146-152). */
+int gmaco_finished(gmaco_engine* h, int32_t* out);
+/* run(cfg, dist) (engine.cpp:435-444) / parallel_run(cfg, dist, workers)
+ * (parallel.cpp:276-285): steps to completion and collects. */
+int gmaco_run(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s);
+/* collect_result (engine.cpp:402-433).  travel_times_s is [vehicle_count] (or
+ * NULL); retired_* receive up to retired_cap entries in vid order. */
+int gmaco_collect(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s,
+                  int32_t* retired_vid, int32_t* retired_node, int32_t retired_cap);
+
+/* State snapshots for stage-level parity. */
+int gmaco_get_pheromone(gmaco_engine* h, int64_t* tau_micros /* [edge_count], edge-id order */);
+int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau_micros);
+int gmaco_get_occupancy(gmaco_engine* h, int32_t* occupancy /* [edge_count] */);
+int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* view);
+int gmaco_get_signals(gmaco_engine* h, const gmaco_signal_view* view, int64_t queue_cap);
+int gmaco_signal_count(gmaco_engine* h, int32_t* out);
+int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out);
+int gmaco_current_step(gmaco_engine* h, int64_t* out);
+
+/* Per-vehicle route query: the vehicle's realized path (path_edges,
+ * engine.hpp:88) when planned == 0, or its current best-of-K planned tour from
+ * the last colony iteration when planned == 1 (colony algorithm only). */
+int gmaco_route_query(gmaco_engine* h, int32_t vid, int32_t planned, int32_t* out_edges,
+                      int32_t cap, int32_t* out_len);
+
+/* Batched next-hop selection over the engine's current pheromone field and
+ * occupancy: next_node_dijkstra / next_node_aco / next_node_maco
+ * (routing.hpp:52-73).  For ACO, rng_entity[i] / rng_step[i] form the RngKey
+ * (routing.hpp:33-37).  Unroutable entries return next = via = -1. */
+int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int32_t* current,
+                    const int32_t* dest, const uint64_t* rng_entity, const uint64_t* rng_step,
+                    int64_t n_t, int32_t* out_next, int32_t* out_via, uint8_t* out_deviated);
+
+/* Device event timing of the last gmaco_step call's kernels (ms), for the
+ * bench roofline: walk kernel total and whole-step total. */
+int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches);
+int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
+
+const char* gmaco_last_error(const gmaco_engine* h);
+void gmaco_destroy(gmaco_engine* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GMACO_H_ */
