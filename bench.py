@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""GMACO-P engine benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config): 32x32
+grid road network with signals at every intersection, 1,000 vehicles,
+64-ant colonies per vehicle, preemptive signals, congestion-modified
+pheromone; one bench step = one colony iteration (every active vehicle's
+colony builds 64 complete tours to its destination, then the engine step
+B..G advances the world).  Metric: ant-steps/s (one next-hop selection =
+one ant-step, counted exactly on the device); vehicle-routes/s alongside.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU code (oracle/_ref, compiled
+from /root/reference in place) on the same workload and unit: every active
+vehicle's 64 ants walk full tours with the reference's next_node_aco
+(routing.cpp:77-115) across all host threads, then the reference's
+sequential_step advances its world.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+GRID = 32
+VEHICLES = 1000
+ANTS = 64
+ITERATIONS = 200
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=ITERATIONS)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(seed: int, max_steps: int, vehicles: int = VEHICLES):
+    from paper_2010_14244_b200 import abi
+    cfg = abi.default_config(algorithm="colony", controller="preemptive", vehicle_count=vehicles,
+                             seed=seed, max_steps=max_steps)
+    return abi.colony_production(cfg, ants=ANTS)
+
+
+def config_block(args, world):
+    return {
+        "workload": "C2: 32x32 grid, signals at every intersection, 1000 vehicles/GPU, 64 ants/colony, "
+                    "preemptive signals, congestion-modified pheromone, one colony iteration per step",
+        "network": f"grid {GRID}x{GRID}, 200 m edges, 3 lanes, {GRID * GRID} signals",
+        "vehicles_per_gpu": VEHICLES,
+        "ants_per_colony": ANTS,
+        "iterations_timed": args.steps,
+        "l2": "flushed (512 MiB write) between timed iterations; working set ~1 MB is L2-resident",
+        "parallelism": f"vehicle-sharded replicas x{world}" if world > 1 else "1 GPU",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(c, grid_closed_form=True):
+    """Algorithmic bytes of the walk kernel: per ant-step
+    8 B row descriptor + 4 B per scanned out-edge (column) + 8 B per dense
+    distance lookup (0 with the grid closed form) + 8 B weight per candidate
+    + 8 B tour cost of the chosen edge."""
+    dist = 0 if grid_closed_form else 8 * c.degree_sum
+    return 8 * c.ant_steps + 4 * c.degree_sum + dist + 8 * c.candidates + 8 * c.ant_steps
+
+
+# ----------------------------------------------------------------------------
+# reference arm
+# ----------------------------------------------------------------------------
+def reference_world(seed, max_steps):
+    from oracle import oracle as O
+    from paper_2010_14244_b200 import abi, networks
+    net = networks.grid(GRID, GRID, signals="all")
+    cfg = abi.default_config(algorithm="aco", controller="preemptive", vehicle_count=VEHICLES, seed=seed,
+                             max_steps=max_steps)
+    return O.RefWorld(net, cfg), net
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    threads = os.cpu_count() or 1
+    w, _ = reference_world(1, args.warmup + args.steps + 10)
+    for _ in range(args.warmup):
+        w.colony_iteration(ANTS, threads)
+    t0 = time.perf_counter()
+    steps = routes = 0
+    for _ in range(args.steps):
+        s, r = w.colony_iteration(ANTS, threads)
+        steps += s
+        routes += r
+    dt = time.perf_counter() - t0
+    value = steps / dt
+    line = {
+        "impl": "reference", "metric": "ant-steps/sec", "value": value, "unit": "ant-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64",
+        "data": "synthetic", "config": config_block(args, 1),
+        "vehicle_routes_per_sec": routes / dt,
+        "cpu_baseline": {"value": value, "unit": "ant-steps/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} colony iterations of the C2 workload, reference "
+                                   f"next_node_aco tours on {threads} std::threads + sequential_step"},
+        "e2e": {"value": value, "unit": "ant-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline(seconds):
+    """Bounded sample of the reference arm on this host (rank 0, N=1)."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    if O.ref_available():
+        w, _ = reference_world(1, 1000)
+        w.colony_iteration(ANTS, threads)
+        steps = its = 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            s, _ = w.colony_iteration(ANTS, threads)
+            steps += s
+            its += 1
+        dt = time.perf_counter() - t0
+        return {"value": steps / dt, "unit": "ant-steps/s", "cores": threads, "kind": "reference",
+                "sample": f"{its} colony iterations (C2, 64 ants, reference next_node_aco on {threads} "
+                          f"threads + sequential_step), {dt:.1f} s"}
+    from paper_2010_14244_b200 import networks
+    net = networks.grid(GRID, GRID, signals="all")
+    w = O.PortWorld(net, workload_config(1, 1000), net.grid_distance())
+    t0 = time.perf_counter()
+    its = 0
+    while time.perf_counter() - t0 < seconds:
+        w.step(1)
+        its += 1
+    dt = time.perf_counter() - t0
+    return {"value": w.counters().ant_steps / dt, "unit": "ant-steps/s", "cores": 1, "kind": "port",
+            "sample": f"{its} colony iterations of the C2 workload on the C oracle, {dt:.1f} s"}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2010_14244_b200 import networks
+    from paper_2010_14244_b200.engine import Engine
+
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    net = networks.grid(GRID, GRID, signals="all")
+    max_steps = args.warmup + args.steps + 1
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    # ---- device-resident throughput (value) ---------------------------------
+    eng = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
+    eng.step(args.warmup)
+    eng.set_timing(True)
+    c0 = eng.counters()
+    walk_ms = step_ms = 0.0
+    launches = 0
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush between timed iterations (outside the events)
+            torch.cuda.synchronize()
+            eng.step(1)
+            wm, sm, nl = eng.last_timing()
+            walk_ms += wm
+            step_ms += sm
+            launches += nl
+    torch.cuda.synchronize()
+    c1 = eng.counters()
+    ant_steps = c1.ant_steps - c0.ant_steps
+    routes = c1.vehicle_routes - c0.vehicle_routes
+
+    class D:  # counter deltas
+        pass
+    d = D()
+    d.ant_steps = ant_steps
+    d.degree_sum = c1.degree_sum - c0.degree_sum
+    d.candidates = c1.candidates - c0.candidates
+    alg_bytes = algorithmic_bytes(d)
+
+    # ---- end to end through the C ABI from host buffers (e2e) ---------------
+    import ctypes as C
+    from paper_2010_14244_b200 import abi
+    t0 = time.perf_counter()
+    e = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
+    h2d = (net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1)  # graph SoA uploaded from host
+    st = np.zeros(VEHICLES, dtype=np.uint8)
+    oe = np.zeros(VEHICLES, dtype=np.int32)
+    view = abi.VehicleView(state=abi.ptr(st, C.c_uint8), on_edge=abi.ptr(oe, C.c_int32))
+    e.step(args.warmup)
+    for _ in range(args.steps):
+        e.step(1)
+        e._check(e.L.gmaco_get_vehicles(e.h, C.byref(view)))  # the step's decisions back to host
+    res = e.collect()
+    e2e_dt = time.perf_counter() - t0
+    e2e_steps = e.counters().ant_steps
+    e.close()
+    d2h = VEHICLES * 5
+
+    # ---- reduce over ranks ------------------------------------------------------
+    t_dev = step_ms / 1e3
+    vals = torch.tensor([t_dev, e2e_dt, walk_ms], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([ant_steps, routes, e2e_steps], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(vals, op=pg.ReduceOp.MAX)
+        pg.all_reduce(tot, op=pg.ReduceOp.SUM)
+    t_dev, e2e_dt, walk_ms_max = vals.tolist()
+    tot_steps, tot_routes, tot_e2e = tot.tolist()
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    peak, peak_src = measured_peak()
+    walk_avg_s = (walk_ms / 1e3) / max(launches, 1)
+    achieved = (alg_bytes / max(launches, 1)) / walk_avg_s / 1e9 if walk_avg_s > 0 else 0.0
+    line = {
+        "metric": "ant-steps/sec",
+        "value": tot_steps / t_dev,
+        "unit": "ant-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_dev / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64+int64",
+        "data": "synthetic",
+        "config": config_block(args, world),
+        "vehicle_routes_per_sec": tot_routes / t_dev,
+        "ant_steps_per_iteration": tot_steps / args.steps / world,
+        "walk_kernel_share": (walk_ms / step_ms) if step_ms else None,
+        "gpu_launches": int(args.steps * launches_per_step(eng)),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "k_colony (walk)",
+                     "algorithmic_bytes_per_launch": alg_bytes / max(launches, 1),
+                     "avg_launch_us": walk_avg_s * 1e6},
+        "e2e": {"value": tot_e2e / e2e_dt, "unit": "ant-steps/s",
+                "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
+                "d2h_bytes_per_step": d2h,
+                "includes": "gmaco_create from host arrays (H2D), warmup+timed steps, per-step D2H of "
+                            "vehicle states, gmaco_collect"},
+        "clocks": clk.summary(),
+        "completed_vehicles_e2e": res[0].completed_count,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    eng.close()
+    print(json.dumps(line))
+    if pg:
+        pg.destroy_process_group()
+
+
+def launches_per_step(eng) -> int:
+    """Kernels enqueued per engine step for this world (kernels.cu launch_step)."""
+    S = eng.signal_count()
+    return 1 + (2 if S > 0 else 0) + 1 + 1
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

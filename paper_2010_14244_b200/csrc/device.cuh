@@ -1,0 +1,130 @@
+// device.cuh — device-side world layout of the GMACO-P engine (sm_100a).
+//
+// Everything edge-indexed on the device is stored in CSR SLOT order: the
+// out-edges of node x occupy slots [row[x].x, row[x].x + row[x].y), sorted
+// by neighbour id exactly like RoadNetwork::out_edges (net.hpp:64-66,
+// net.cpp:85-93).  A node's candidate row is therefore one contiguous run of
+// columns / weights / lengths, and edge ids (the reference's numbering)
+// appear only at the boundary through slot_edge / edge_slot.
+#pragma once
+
+#include <cstdint>
+
+namespace gmaco {
+
+constexpr int kPhases = 8;
+constexpr int kMaxDegree = 32;  // out-degree bound of the walk kernels (validated at create)
+constexpr int kTabu = 16;       // colony tabu tenure (progress filter off only)
+constexpr int64_t kInf = INT64_MAX;
+
+enum VState : uint8_t { kPending = 0, kAtNode = 1, kOnEdge = 2, kQueued = 3, kArrived = 4, kRetired = 5 };
+
+struct DevGraph {
+  int32_t n, m;
+  const int2* row;          // [n] {first slot, out-degree}
+  const int32_t* col;       // [m] neighbour (edge.to) per slot
+  const int64_t* len;       // [m] length_mm per slot
+  const int32_t* bind;      // [m] signal*8+phase of the queue the edge feeds, -1 if none
+  const int32_t* slot_edge; // [m] reference edge id per slot
+  const int32_t* slot_from; // [m] edge.from per slot
+  const double* eta_beta;   // [m] pow(1/(len/1000), beta), host std::pow (routing.cpp:92-94)
+};
+
+// Distance service read by the candidate filter (routing.cpp:16-30).
+struct DevDist {
+  int32_t kind;        // 0 dense / 2 targets: table; 1 grid closed form
+  int32_t rows, cols;  // grid
+  int64_t grid_len;    // grid edge length
+  int32_t n;
+  const int64_t* table;    // [slot * n + x] = dist(x, dest of slot), kInf unreachable
+  const int32_t* slot_of;  // node -> table row (targets), nullptr = identity (dense)
+};
+
+struct DevParams {
+  int32_t algorithm, controller, deviation_mode, progress_filter;
+  int32_t V, S;
+  int64_t deviation_threshold;
+  double alpha;
+  double dt_s;
+  int64_t dt_us, latency_us;
+  int64_t max_steps;
+  uint64_t seed;
+  // pheromone (micro-units)
+  int64_t tau_lo, tau_hi, inc, dec;
+  double one_minus_rho;  // (1.0 - rho), same expression as pheromone.cpp:64
+  double deposit_q;
+  int32_t siblings_only;
+  // signals
+  int32_t th_max;
+  double t_max, green_duration_s, saturation_flow;
+  int32_t order[kPhases];
+  // colony
+  int32_t ants, hop_limit, max_hops, rng, congestion, deposit, cong_evap, replan_all;
+  int32_t plan_cap, path_cap;
+  int32_t need_positions;  // MACO network-wide fold
+  int32_t record_paths;
+};
+
+struct DevCtl {
+  int64_t step;        // w.step
+  int64_t stop_at;     // host-set step limit for the current launch chunk
+  int64_t n_t;         // count_active for the current step (engine.cpp:156-173)
+  int64_t n_next;      // accumulated for the next step
+  int64_t unfinished;  // vehicles not Arrived/Retired after motion
+  int64_t dcount;      // decisions this step
+  int64_t qtotal, qsamples;
+  int64_t ant_steps, vehicle_routes, decisions, candidates, degree_sum;
+  int32_t done;
+  int32_t max_occ;
+  uint32_t blocks_done;
+  int32_t error;  // device-side overflow flag (path buffer)
+};
+
+struct DevVehicles {
+  int32_t *origin, *dest;
+  int64_t* advance;
+  uint8_t* state;
+  int32_t *at_node, *on_edge;  // on_edge is a SLOT
+  int64_t *progress, *overshoot;
+  int32_t* queued_phase;
+  int64_t *joined, *depart, *arrive, *latency_debt;
+  int64_t *driving, *queued, *lat_steps, *path_len_mm;
+  int32_t *decisions, *deviations;
+  int32_t* qnext;     // FIFO link inside a signal queue
+  int32_t* arr_next;  // this step's arrival stack link
+  int32_t* dec_next;  // this step's decision stack link (MACO fold)
+  int32_t* dflag;     // decided this step (MACO positions)
+  int32_t* pos;       // exclusive prefix of dflag = decision position
+  int32_t *path, *path_n;       // realized path (slots), [V * path_cap]
+  int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap]
+  int64_t* plan_step;
+  uint8_t* plan_done;
+};
+
+struct DevSignals {
+  int32_t* node;
+  int32_t *green, *cursor, *lanes;
+  int64_t* el_steps;
+  double* el_s;
+  // per queue [S*8]
+  int32_t *qlen, *qhead, *qtail, *arr_head;
+  double *head_wait, *rem;
+};
+
+struct DevWorld {
+  DevGraph g;
+  DevDist d;
+  DevParams p;
+  DevVehicles v;
+  DevSignals s;
+  DevCtl* ctl;
+  int64_t* tau;       // [m] pheromone micro-units (slot order)
+  double* weight;     // [m] roulette weight for the coming step
+  int64_t* ecost;     // [m] colony tour cost per edge for the coming step
+  int32_t* occ_cur;   // [m] edge occupancy of the previous step (engine.hpp:166)
+  int32_t* occ_new;   // [m] being accumulated this step
+  int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)
+  int32_t* dec_head;  // [m] decision stack per slot (network-wide MACO) or per node (scoped)
+};
+
+}  // namespace gmaco

@@ -1,0 +1,1132 @@
+// gmaco_capi.cpp — host C++ engine behind the C ABI of include/gmaco.h.
+//
+// Mirrors the reference's executor contract: gmaco_create ≈ init_world
+// (engine.cpp:116-144) on the device, gmaco_step ≈ sequential_step
+// (engine.cpp:352-400) / ParallelRunner::step (parallel.cpp:123-193),
+// gmaco_collect ≈ collect_result (engine.cpp:402-433).  Setup (validation,
+// CSR build, spawn, initial pheromone) runs on the host exactly as the
+// reference does it; every per-step stage runs in sm_100a kernels
+// (kernels.cu), replayed as CUDA graphs of `kGraphSteps` steps.  There is no
+// CPU execution path: without a CUDA device gmaco_create fails with status 2.
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+#include <queue>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "device.cuh"
+#include "gmaco.h"
+#include "kernels.h"
+
+namespace gmaco {
+namespace {
+
+struct ValidationError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+std::string fmt(const char* f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+#define CK(call)                                                                                \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                               #call);                                                          \
+  } while (0)
+
+constexpr int kGraphSteps = 32;
+constexpr int64_t kCostCap = (int64_t(1) << 53) - 1;
+
+int64_t tau_from_double(double v) { return std::llround(v * 1e6); }  // pheromone.hpp:18
+
+// ---- host graph (RoadNetwork ctor semantics, net.cpp:38-98) ---------------
+struct HostGraph {
+  int32_t n = 0, m = 0;
+  std::vector<int32_t> from, to, lanes;
+  std::vector<int64_t> len;
+  std::vector<uint8_t> sig;
+  std::vector<int32_t> out_ptr, out_nbr, out_edge;  // CSR sorted by neighbour
+  std::vector<int32_t> in_ptr, in_edge;             // ascending edge id
+  std::vector<int32_t> edge_slot;                   // edge id -> slot
+};
+
+void build_graph(const gmaco_graph_desc* d, HostGraph& g) {
+  if (!d) throw ValidationError("graph descriptor is null");
+  const int32_t n = d->node_count, m = d->edge_count;
+  if (n <= 0) throw ValidationError("network has no nodes");
+  if (m < 0) throw ValidationError("network edge count must be >= 0");
+  for (int32_t e = 0; e < m; ++e) {  // net.cpp:58-79, input order
+    if (d->edge_from[e] < 0 || d->edge_from[e] >= n)
+      throw ValidationError(fmt("edge %d references missing node %d", e, d->edge_from[e]));
+    if (d->edge_to[e] < 0 || d->edge_to[e] >= n)
+      throw ValidationError(fmt("edge %d references missing node %d", e, d->edge_to[e]));
+    if (d->edge_from[e] == d->edge_to[e])
+      throw ValidationError(fmt("edge %d is a self-loop at node %d", e, d->edge_from[e]));
+    if (d->edge_length_mm[e] <= 0) throw ValidationError(fmt("edge %d has nonpositive length", e));
+    if (d->edge_lanes && d->edge_lanes[e] < 1) throw ValidationError(fmt("edge %d has lanes < 1", e));
+  }
+  g.n = n;
+  g.m = m;
+  g.from.assign(d->edge_from, d->edge_from + m);
+  g.to.assign(d->edge_to, d->edge_to + m);
+  g.len.assign(d->edge_length_mm, d->edge_length_mm + m);
+  g.lanes.resize(m);
+  for (int32_t e = 0; e < m; ++e) g.lanes[e] = d->edge_lanes ? d->edge_lanes[e] : 1;
+  g.sig.resize(n);
+  for (int32_t i = 0; i < n; ++i) g.sig[i] = d->signalized ? d->signalized[i] : 0;
+  g.out_ptr.assign(n + 1, 0);
+  g.in_ptr.assign(n + 1, 0);
+  for (int32_t e = 0; e < m; ++e) {
+    g.out_ptr[g.from[e] + 1]++;
+    g.in_ptr[g.to[e] + 1]++;
+  }
+  for (int32_t u = 0; u < n; ++u) {
+    g.out_ptr[u + 1] += g.out_ptr[u];
+    g.in_ptr[u + 1] += g.in_ptr[u];
+  }
+  g.out_nbr.resize(m);
+  g.out_edge.resize(m);
+  g.in_edge.resize(m);
+  std::vector<int32_t> oc(g.out_ptr.begin(), g.out_ptr.end() - 1), ic(g.in_ptr.begin(), g.in_ptr.end() - 1);
+  for (int32_t e = 0; e < m; ++e) {
+    g.out_nbr[oc[g.from[e]]] = g.to[e];
+    g.out_edge[oc[g.from[e]]++] = e;
+    g.in_edge[ic[g.to[e]]++] = e;
+  }
+  std::vector<std::pair<int32_t, int32_t>> tmp;
+  for (int32_t u = 0; u < n; ++u) {
+    tmp.clear();
+    for (int32_t k = g.out_ptr[u]; k < g.out_ptr[u + 1]; ++k) tmp.emplace_back(g.out_nbr[k], g.out_edge[k]);
+    std::stable_sort(tmp.begin(), tmp.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    for (size_t i = 0; i < tmp.size(); ++i) {
+      g.out_nbr[g.out_ptr[u] + i] = tmp[i].first;
+      g.out_edge[g.out_ptr[u] + i] = tmp[i].second;
+      if (i > 0 && tmp[i].first == tmp[i - 1].first)  // net.cpp:89-93
+        throw ValidationError(fmt("duplicate edge between nodes %d and %d", u, tmp[i].first));
+    }
+  }
+  g.edge_slot.resize(m);
+  for (int32_t s = 0; s < m; ++s) g.edge_slot[g.out_edge[s]] = s;
+}
+
+// ---- config validation (engine.cpp:12-32 + param validate()s) -------------
+void validate_config(const gmaco_sim_config* c) {
+  if (!c) throw ValidationError("config is null");
+  if (c->vehicle_count < 1) throw ValidationError("config: vehicle_count must be >= 1");
+  if (!(c->dt_s > 0)) throw ValidationError("config: dt must be positive");
+  if (c->max_steps < 0) throw ValidationError("config: max_steps must be >= 0");
+  if (c->decision_latency_s < 0) throw ValidationError("config: decision_latency_s must be >= 0");
+  if (c->spawn == GMACO_UNIFORM_WINDOW && c->spawn_window_steps < 1)
+    throw ValidationError("config: spawn_window_steps must be >= 1");
+  if (c->speed_min_mps <= 0 || c->speed_max_mps < c->speed_min_mps)
+    throw ValidationError("config: speed range must satisfy 0 < min <= max");
+  if (c->od_pattern == GMACO_OD_BLOCKS) {
+    if (c->od_bias < 0 || c->od_bias > 1) throw ValidationError("config: od bias must lie in [0, 1]");
+    if (c->od_block_a_len <= 0 || c->od_block_b_len <= 0)
+      throw ValidationError("config: od blocks must be non-empty");
+  }
+  const gmaco_pheromone_params& p = c->pheromone;  // pheromone.cpp:9-19
+  if (!(p.tau_min <= p.tau_init_lo && p.tau_init_lo <= p.tau_init_hi && p.tau_init_hi <= p.tau_max))
+    throw ValidationError("pheromone init range must satisfy tau_min <= lo <= hi <= tau_max");
+  if (p.delta_inc <= 0 || p.delta_dec <= 0)
+    throw ValidationError("pheromone delta_inc and delta_dec must be positive");
+  if (p.rho < 0 || p.rho >= 1) throw ValidationError("pheromone rho must lie in [0, 1)");
+  if (p.tau_min < 0) throw ValidationError("pheromone tau_min must be >= 0");
+  const gmaco_signal_params& s = c->signal;  // signals.cpp:8-21
+  if (s.th_max < 1) throw ValidationError("signal th_max must be >= 1");
+  if (s.t_max <= 0) throw ValidationError("signal t_max must be positive");
+  if (s.green_duration_s <= 0) throw ValidationError("signal green_duration must be positive");
+  if (s.saturation_flow <= 0) throw ValidationError("signal saturation_flow must be positive");
+  bool seen[kPhases] = {};
+  for (int i = 0; i < kPhases; ++i) {
+    const int ph = s.fixed_cycle_order[i];
+    if (ph < 0 || ph >= kPhases || seen[ph])
+      throw ValidationError("signal fixed_cycle_order must be a permutation of 0..7");
+    seen[ph] = true;
+  }
+  if (c->routing.deviation_threshold < 0)  // routing.cpp:9-14
+    throw ValidationError("routing deviation_threshold must be >= 0");
+  if (c->routing.aco_alpha < 0 || c->routing.aco_beta < 0)
+    throw ValidationError("routing aco exponents must be >= 0");
+  if (c->algorithm < GMACO_DIJKSTRA || c->algorithm > GMACO_COLONY)
+    throw ValidationError(fmt("config: unknown algorithm %d", c->algorithm));
+  if (c->controller < GMACO_FIXED || c->controller > GMACO_PREEMPTIVE)
+    throw ValidationError(fmt("config: unknown controller %d", c->controller));
+  if (c->algorithm == GMACO_COLONY) {
+    const gmaco_colony_params& k = c->colony;
+    if (k.ants < 1) throw ValidationError("colony: ants must be >= 1");
+    if (k.ants > 1024) throw ValidationError("colony: ants must be <= 1024");
+    if (k.hop_limit < 0 || k.max_hops < 0) throw ValidationError("colony: hop limits must be >= 0");
+    if (k.rng != GMACO_RNG_PHILOX && k.rng != GMACO_RNG_REFERENCE) throw ValidationError("colony: unknown rng");
+    if (k.deposit < GMACO_DEPOSIT_COMPLETION || k.deposit > GMACO_DEPOSIT_NONE)
+      throw ValidationError("colony: unknown deposit mode");
+  }
+}
+
+// ---- Dijkstra to a destination over reversed edges (net.cpp:359-383) ------
+void dijkstra_to(const HostGraph& g, const std::vector<int32_t>& rptr, const std::vector<int32_t>& rsrc,
+                 const std::vector<int32_t>& redge, int32_t dst, int64_t* dist) {
+  std::fill(dist, dist + g.n, kInf);
+  using Item = std::pair<int64_t, int32_t>;
+  std::priority_queue<Item, std::vector<Item>, std::greater<>> heap;
+  dist[dst] = 0;
+  heap.emplace(0, dst);
+  while (!heap.empty()) {
+    auto [d, u] = heap.top();
+    heap.pop();
+    if (d != dist[u]) continue;
+    for (int32_t k = rptr[u]; k < rptr[u + 1]; ++k) {
+      const int64_t nd = d + g.len[redge[k]];
+      if (nd < dist[rsrc[k]]) {
+        dist[rsrc[k]] = nd;
+        heap.emplace(nd, rsrc[k]);
+      }
+    }
+  }
+}
+
+void reverse_csr(const HostGraph& g, std::vector<int32_t>& rptr, std::vector<int32_t>& rsrc,
+                 std::vector<int32_t>& redge) {
+  rptr.assign(g.n + 1, 0);
+  rsrc.resize(g.m);
+  redge.resize(g.m);
+  for (int32_t e = 0; e < g.m; ++e) rptr[g.to[e] + 1]++;
+  for (int32_t u = 0; u < g.n; ++u) rptr[u + 1] += rptr[u];
+  std::vector<int32_t> c(rptr.begin(), rptr.end() - 1);
+  for (int32_t e = 0; e < g.m; ++e) {
+    rsrc[c[g.to[e]]] = g.from[e];
+    redge[c[g.to[e]]++] = e;
+  }
+}
+
+// ---- device buffers --------------------------------------------------------
+struct DevBuffers {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& h) {
+    T* d = alloc<T>(h.size());
+    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  template <class T>
+  T* filled(size_t n, T value) {
+    std::vector<T> h(n, value);
+    return upload(h);
+  }
+  ~DevBuffers() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+template <class T>
+std::vector<T> download(const T* d, size_t n) {
+  std::vector<T> h(n);
+  if (n) CK(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost));
+  return h;
+}
+
+}  // namespace
+}  // namespace gmaco
+
+using namespace gmaco;
+
+struct gmaco_engine {
+  std::string err;
+  int device = 0;
+  HostGraph g;
+  gmaco_sim_config cfg{};
+  int32_t S = 0;
+  std::vector<int32_t> sig_node;
+  DevBuffers buf;
+  DevWorld w{};
+  DevCtl* ctl = nullptr;
+  DevCtl* ctl_host = nullptr;  // pinned mirror
+  int64_t* stop_host = nullptr;
+  StepResources res;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph_big = nullptr, graph_one = nullptr;
+  cudaGraphExec_t tgraph_big = nullptr, tgraph_one = nullptr;
+  std::vector<cudaEvent_t> ev_begin, ev_end;  // timing mode, kGraphSteps pairs
+  bool timing = false;
+  double last_walk_ms = 0.0, last_step_ms = 0.0;
+  int64_t last_walk_launches = 0;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  int64_t wall_ms = 0;
+
+  ~gmaco_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto ge : {graph_big, graph_one, tgraph_big, tgraph_one})
+      if (ge) cudaGraphExecDestroy(ge);
+    for (auto e : ev_begin) cudaEventDestroy(e);
+    for (auto e : ev_end) cudaEventDestroy(e);
+    if (ev_a) cudaEventDestroy(ev_a);
+    if (ev_b) cudaEventDestroy(ev_b);
+    if (ctl_host) cudaFreeHost(ctl_host);
+    if (stop_host) cudaFreeHost(stop_host);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class F>
+int guarded(gmaco_engine* h, F&& f) {
+  try {
+    if (h) CK(cudaSetDevice(h->device));
+    f();
+    return GMACO_OK;
+  } catch (const ValidationError& e) {
+    (h ? h->err : g_create_err) = e.what();
+    return GMACO_EVALIDATION;
+  } catch (const std::exception& e) {
+    (h ? h->err : g_create_err) = e.what();
+    return GMACO_ERUNTIME;
+  }
+}
+
+// ---- spawn_vehicles (engine.cpp:71-114), pool indexed not materialized ----
+struct Spawned {
+  std::vector<int32_t> origin, dest;
+  std::vector<double> speed;
+  std::vector<int64_t> advance, depart;
+};
+
+uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+uint64_t draw(uint64_t seed, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+  uint64_t h = mix64(seed);
+  h = mix64(h ^ a);
+  h = mix64(h ^ b);
+  return mix64(h ^ c);
+}
+double to_unit(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
+double uniform(uint64_t bits, double lo, double hi) { return lo + to_unit(bits) * (hi - lo); }
+uint64_t below(uint64_t bits, uint64_t n) {
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(bits) * n) >> 64);
+}
+
+struct DistHost {  // host view of the distance service (spawn reachability)
+  int kind = 0;
+  int32_t n = 0, cols = 0;
+  int64_t grid_len = 0;
+  const std::vector<int64_t>* table = nullptr;  // [slot*n + x]
+  const std::vector<int32_t>* slot_of = nullptr;
+  int64_t dist(int32_t x, int32_t dest) const {
+    if (kind == GMACO_DIST_GRID) {
+      const int32_t rx = x / cols, cx = x % cols, rd = dest / cols, cd = dest % cols;
+      return (int64_t)(std::abs(rx - rd) + std::abs(cx - cd)) * grid_len;
+    }
+    const int32_t s = slot_of ? (*slot_of)[dest] : dest;
+    return s < 0 ? kInf : (*table)[(size_t)s * n + x];
+  }
+  bool reachable(int32_t u, int32_t v) const { return dist(u, v) != kInf; }
+};
+
+Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
+              const std::vector<int32_t>& targets) {
+  const int32_t n = g.n;
+  std::vector<int32_t> dests;
+  if (dh.kind == GMACO_DIST_TARGETS) {
+    dests = targets;
+    std::sort(dests.begin(), dests.end());
+  }
+  const int32_t nd = dh.kind == GMACO_DIST_TARGETS ? (int32_t)dests.size() : n;
+  std::vector<int64_t> prefix(n + 1, 0);
+  for (int32_t u = 0; u < n; ++u) {
+    int64_t cnt = 0;
+    if (dh.kind == GMACO_DIST_GRID) {
+      cnt = n - 1;
+    } else {
+      for (int32_t j = 0; j < nd; ++j) {
+        const int32_t v = dests.empty() ? j : dests[j];
+        if (u != v && dh.reachable(u, v)) ++cnt;
+      }
+    }
+    prefix[u + 1] = prefix[u] + cnt;
+  }
+  const int64_t pool = prefix[n];
+  if (pool == 0) throw ValidationError("spawn: network has no reachable origin/destination pair");
+  std::vector<std::pair<int32_t, int32_t>> ab, ba;
+  auto block_pairs = [&](const int32_t* a, int32_t na, const int32_t* b, int32_t nb, auto& out) {
+    for (int32_t i = 0; i < na; ++i)  // engine.cpp:59-66
+      for (int32_t j = 0; j < nb; ++j)
+        if (a[i] != b[j] && dh.reachable(a[i], b[j])) out.emplace_back(a[i], b[j]);
+  };
+  if (c.od_pattern == GMACO_OD_BLOCKS) {
+    for (int32_t i = 0; i < c.od_block_a_len; ++i)
+      if (c.od_block_a[i] < 0 || c.od_block_a[i] >= n) throw ValidationError("config: od block node out of range");
+    for (int32_t i = 0; i < c.od_block_b_len; ++i)
+      if (c.od_block_b[i] < 0 || c.od_block_b[i] >= n) throw ValidationError("config: od block node out of range");
+    block_pairs(c.od_block_a, c.od_block_a_len, c.od_block_b, c.od_block_b_len, ab);
+    block_pairs(c.od_block_b, c.od_block_b_len, c.od_block_a, c.od_block_a_len, ba);
+  }
+  Spawned s;
+  const int32_t V = c.vehicle_count;
+  s.origin.resize(V);
+  s.dest.resize(V);
+  s.speed.resize(V);
+  s.advance.resize(V);
+  s.depart.assign(V, 0);
+  for (int32_t vid = 0; vid < V; ++vid) {
+    const std::vector<std::pair<int32_t, int32_t>>* biased = nullptr;
+    if (c.od_pattern == GMACO_OD_BLOCKS) {  // engine.cpp:88-97
+      const double r = to_unit(draw(c.seed, 2, vid, 0));
+      if (r < c.od_bias) {
+        const bool forward = to_unit(draw(c.seed, 2, vid, 1)) < 0.5;
+        const auto& b = forward ? ab : ba;
+        if (!b.empty()) biased = &b;
+      }
+    }
+    const uint64_t bits = draw(c.seed, 2, vid, 2);
+    if (biased) {
+      const auto& pr = (*biased)[below(bits, biased->size())];
+      s.origin[vid] = pr.first;
+      s.dest[vid] = pr.second;
+    } else {
+      const int64_t idx = (int64_t)below(bits, (uint64_t)pool);
+      const int32_t u = (int32_t)(std::upper_bound(prefix.begin(), prefix.end(), idx) - prefix.begin()) - 1;
+      int64_t r = idx - prefix[u];
+      int32_t v = -1;
+      if (dh.kind == GMACO_DIST_GRID) {
+        v = (int32_t)(r + (r >= u));
+      } else {
+        for (int32_t j = 0; j < nd; ++j) {
+          const int32_t cand = dests.empty() ? j : dests[j];
+          if (u != cand && dh.reachable(u, cand)) {
+            if (r == 0) {
+              v = cand;
+              break;
+            }
+            --r;
+          }
+        }
+      }
+      s.origin[vid] = u;
+      s.dest[vid] = v;
+    }
+    s.speed[vid] = uniform(draw(c.seed, 3, vid), c.speed_min_mps, c.speed_max_mps);  // engine.cpp:103-105
+    s.advance[vid] = std::llround(s.speed[vid] * c.dt_s * 1000.0);
+    if (c.spawn == GMACO_UNIFORM_WINDOW)
+      s.depart[vid] = (int64_t)below(draw(c.seed, 4, vid), (uint64_t)c.spawn_window_steps);
+  }
+  return s;
+}
+
+void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distance_desc* dd,
+                 const gmaco_sim_config* cfg) {
+  build_graph(gd, h->g);
+  validate_config(cfg);
+  if (!dd) throw ValidationError("distance descriptor is null");
+  HostGraph& g = h->g;
+  const int32_t n = g.n, m = g.m;
+  h->cfg = *cfg;
+  gmaco_sim_config& c = h->cfg;
+  const int alg = c.algorithm;
+  for (int32_t u = 0; u < n; ++u)
+    if (g.out_ptr[u + 1] - g.out_ptr[u] > kMaxDegree)
+      throw ValidationError(fmt("node %d out-degree exceeds the engine bound of %d", u, kMaxDegree));
+
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  DevBuffers& B = h->buf;
+  DevWorld& w = h->w;
+
+  // ---- distance service ---------------------------------------------------
+  DistHost dh;
+  dh.kind = dd->kind;
+  dh.n = n;
+  std::vector<int64_t> table;
+  std::vector<int32_t> slot_of, targets;
+  w.d.kind = dd->kind == GMACO_DIST_GRID ? 1 : 0;
+  w.d.n = n;
+  if (dd->kind == GMACO_DIST_DENSE) {
+    table.resize((size_t)n * n);
+    if (dd->dist_mm) {
+      for (int32_t u = 0; u < n; ++u)
+        for (int32_t v = 0; v < n; ++v) table[(size_t)v * n + u] = dd->dist_mm[(size_t)u * n + v];
+    } else {  // all_pairs_distances (net.cpp:419-437), one Dijkstra per destination
+      std::vector<int32_t> rp, rs, re;
+      reverse_csr(g, rp, rs, re);
+      const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+          for (int32_t d = t; d < n; d += nt) dijkstra_to(g, rp, rs, re, d, table.data() + (size_t)d * n);
+        });
+      for (auto& th : pool) th.join();
+    }
+    dh.table = &table;
+  } else if (dd->kind == GMACO_DIST_GRID) {
+    const int32_t R = dd->grid_rows, Cc = dd->grid_cols;
+    if (R < 2 || Cc < 2 || (int64_t)R * Cc != n)
+      throw ValidationError("grid distance: shape does not match the network");
+    if ((int64_t)m != 2LL * (R * (Cc - 1) + Cc * (R - 1)))
+      throw ValidationError("grid distance: network is not a full 4-neighbour lattice");
+    for (int32_t e = 0; e < m; ++e) {
+      const int32_t a = g.from[e], b = g.to[e];
+      const int32_t ra = a / Cc, ca = a % Cc, rb = b / Cc, cb = b % Cc;
+      if (std::abs(ra - rb) + std::abs(ca - cb) != 1 || g.len[e] != g.len[0])
+        throw ValidationError("grid distance: network is not a uniform 4-neighbour lattice");
+    }
+    w.d.rows = R;
+    w.d.cols = Cc;
+    w.d.grid_len = g.len[0];
+    dh.cols = Cc;
+    dh.grid_len = g.len[0];
+  } else if (dd->kind == GMACO_DIST_TARGETS) {
+    if (dd->target_count < 1 || !dd->targets) throw ValidationError("targets distance: empty target set");
+    targets.assign(dd->targets, dd->targets + dd->target_count);
+    slot_of.assign(n, -1);
+    for (int32_t t = 0; t < (int32_t)targets.size(); ++t) {
+      const int32_t x = targets[t];
+      if (x < 0 || x >= n || slot_of[x] >= 0)
+        throw ValidationError(fmt("targets distance: invalid or duplicate target %d", x));
+      slot_of[x] = t;
+    }
+    table.resize((size_t)targets.size() * n);
+    std::vector<int32_t> rp, rs, re;
+    reverse_csr(g, rp, rs, re);
+    const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (size_t k = t; k < targets.size(); k += nt)
+          dijkstra_to(g, rp, rs, re, targets[k], table.data() + k * n);
+      });
+    for (auto& th : pool) th.join();
+    dh.table = &table;
+    dh.slot_of = &slot_of;
+  } else {
+    throw ValidationError(fmt("unknown distance kind %d", dd->kind));
+  }
+  if (!table.empty()) w.d.table = B.upload(table);
+  if (!slot_of.empty()) w.d.slot_of = B.upload(slot_of);
+
+  // ---- spawn (host, engine.cpp:71-114) -------------------------------------
+  Spawned sp = spawn(c, g, dh, targets);
+  const int32_t V = c.vehicle_count;
+
+  // ---- graph in slot order ---------------------------------------------------
+  std::vector<int2> row(n);
+  for (int32_t u = 0; u < n; ++u) row[u] = make_int2(g.out_ptr[u], g.out_ptr[u + 1] - g.out_ptr[u]);
+  std::vector<int32_t> col(m), slot_from(m), bind(m, -1);
+  std::vector<int64_t> slen(m);
+  std::vector<double> eta(m);
+  for (int32_t s = 0; s < m; ++s) {
+    const int32_t e = g.out_edge[s];
+    col[s] = g.to[e];
+    slot_from[s] = g.from[e];
+    slen[s] = g.len[e];
+    const double vis = 1.0 / (static_cast<double>(g.len[e]) / 1000.0);  // routing.cpp:92
+    eta[s] = std::pow(vis, c.routing.aco_beta);
+  }
+  // signals (engine.cpp:124-136, make_signal_state signals.cpp:29-46)
+  std::vector<int32_t> sig_of_node(n, -1), lanes_s;
+  int32_t S = 0;
+  for (int32_t i = 0; i < n; ++i)
+    if (g.sig[i]) sig_of_node[i] = S++;
+  h->S = S;
+  h->sig_node.assign(S, 0);
+  lanes_s.assign(S, 1);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t s = sig_of_node[i];
+    if (s < 0) continue;
+    h->sig_node[s] = i;
+    int slot = 0;
+    for (int32_t k = g.in_ptr[i]; k < g.in_ptr[i + 1]; ++k, ++slot) {
+      const int32_t e = g.in_edge[k];
+      bind[g.edge_slot[e]] = s * kPhases + slot % kPhases;
+      lanes_s[s] = std::max(lanes_s[s], g.lanes[e]);
+    }
+  }
+  w.g.n = n;
+  w.g.m = m;
+  w.g.row = B.upload(row);
+  w.g.col = B.upload(col);
+  w.g.len = B.upload(slen);
+  w.g.bind = B.upload(bind);
+  w.g.slot_edge = B.upload(g.out_edge);
+  w.g.slot_from = B.upload(slot_from);
+  w.g.eta_beta = B.upload(eta);
+
+  // ---- params ----------------------------------------------------------------
+  DevParams& p = w.p;
+  p.algorithm = alg;
+  p.controller = c.controller;
+  p.deviation_mode = c.routing.deviation_mode;
+  p.progress_filter = c.routing.progress_filter != 0;
+  p.V = V;
+  p.S = S;
+  p.deviation_threshold = c.routing.deviation_threshold;
+  p.alpha = c.routing.aco_alpha;
+  p.dt_s = c.dt_s;
+  p.dt_us = std::llround(c.dt_s * 1e6);  // engine.cpp:124-125
+  p.latency_us = std::llround(c.decision_latency_s * 1e6);
+  p.max_steps = c.max_steps;
+  p.seed = c.seed;
+  p.tau_lo = tau_from_double(c.pheromone.tau_min);
+  p.tau_hi = tau_from_double(c.pheromone.tau_max);
+  p.inc = tau_from_double(c.pheromone.delta_inc);
+  p.dec = tau_from_double(c.pheromone.delta_dec);
+  p.one_minus_rho = 1.0 - c.pheromone.rho;
+  p.deposit_q = c.pheromone.aco_deposit_q;
+  p.siblings_only = c.pheromone.decrement_siblings_only != 0;
+  p.th_max = c.signal.th_max;
+  p.t_max = c.signal.t_max;
+  p.green_duration_s = c.signal.green_duration_s;
+  p.saturation_flow = c.signal.saturation_flow;
+  for (int i = 0; i < kPhases; ++i) p.order[i] = c.signal.fixed_cycle_order[i];
+  const gmaco_colony_params& k = c.colony;
+  p.ants = alg == GMACO_COLONY ? k.ants : 1;
+  p.hop_limit = alg == GMACO_COLONY ? k.hop_limit : 1;
+  p.max_hops = alg == GMACO_COLONY && k.max_hops > 0 ? k.max_hops : std::max(n - 1, 1);
+  p.rng = alg == GMACO_COLONY ? k.rng : GMACO_RNG_REFERENCE;
+  p.congestion = alg == GMACO_COLONY ? k.congestion : 0;
+  p.deposit = alg == GMACO_COLONY ? k.deposit : (alg == GMACO_ACO ? GMACO_DEPOSIT_COMPLETION : GMACO_DEPOSIT_NONE);
+  p.cong_evap = alg == GMACO_COLONY ? k.congestion_evaporation : 0;
+  p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
+  p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
+  // realized-path storage: needed for completion deposits; paths are bounded by
+  // the decision count (<= max_steps) and, with the progress filter, by n-1.
+  p.path_cap = (int32_t)std::max<int64_t>(
+      1, std::min<int64_t>(c.max_steps, p.progress_filter ? (int64_t)n - 1 : c.max_steps));
+  const bool need_paths = p.deposit == GMACO_DEPOSIT_COMPLETION && (alg == GMACO_ACO || alg == GMACO_COLONY);
+  const size_t path_bytes = (size_t)V * p.path_cap * 4;
+  p.record_paths = need_paths || path_bytes <= (size_t(1) << 30);
+  if (need_paths && path_bytes > (size_t(16) << 30))
+    throw ValidationError("config: realized-path storage exceeds 16 GiB (lower max_steps)");
+  if (!p.record_paths) p.path_cap = 1;
+  p.plan_cap = alg == GMACO_COLONY ? p.max_hops : 1;
+  if (alg == GMACO_COLONY && (size_t)V * p.plan_cap * 4 > (size_t(32) << 30))
+    throw ValidationError("colony: planned-tour storage exceeds 32 GiB (set colony.max_hops)");
+  if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound
+    int64_t maxlen = 0;
+    for (int64_t L : g.len) maxlen = std::max(maxlen, L);
+    const long double bound = (long double)p.max_hops * maxlen * (1.0L + V);
+    if (bound >= (long double)kCostCap)
+      throw ValidationError("colony: tour cost bound exceeds 2^53 (lower max_hops)");
+  }
+
+  // ---- pheromone init (init_random, pheromone.cpp:21-32) + first weights ----
+  std::vector<int64_t> tau(m);
+  std::vector<double> wt(m);
+  std::vector<int64_t> ecost(m);
+  const int64_t lo = p.tau_lo, hi = p.tau_hi;
+  for (int32_t s = 0; s < m; ++s) {
+    const int32_t e = g.out_edge[s];
+    const double v = uniform(draw(c.seed, 1, (uint64_t)e), c.pheromone.tau_init_lo, c.pheromone.tau_init_hi);
+    tau[s] = std::clamp(tau_from_double(v), lo, hi);
+    const double tau_d = static_cast<double>(tau[s]) / 1e6;
+    const double ta = p.alpha == 1.0 ? tau_d : std::pow(tau_d, p.alpha);
+    wt[s] = ta * eta[s];  // load 0: the congestion factor is exactly 1.0
+    ecost[s] = slen[s];
+  }
+  w.tau = B.upload(tau);
+  w.weight = B.upload(wt);
+  w.ecost = B.upload(ecost);
+  w.occ_cur = B.filled<int32_t>(m, 0);
+  w.occ_new = B.filled<int32_t>(m, 0);
+  w.dep = B.filled<int64_t>(m, 0);
+  w.dec_head = B.filled<int32_t>(std::max(m, n), -1);
+
+  // ---- signals -----------------------------------------------------------
+  DevSignals& ds = w.s;
+  std::vector<int32_t> cur(S, c.signal.fixed_cycle_order[kPhases - 1]);
+  ds.node = B.upload(h->sig_node);
+  ds.green = B.upload(cur);
+  ds.cursor = B.upload(cur);
+  ds.lanes = B.upload(lanes_s);
+  ds.el_steps = B.filled<int64_t>(S, 0);
+  ds.el_s = B.filled<double>(S, c.signal.green_duration_s);
+  ds.qlen = B.filled<int32_t>((size_t)S * kPhases, 0);
+  ds.qhead = B.filled<int32_t>((size_t)S * kPhases, -1);
+  ds.qtail = B.filled<int32_t>((size_t)S * kPhases, -1);
+  ds.arr_head = B.filled<int32_t>((size_t)S * kPhases, -1);
+  ds.head_wait = B.filled<double>((size_t)S * kPhases, 0.0);
+  ds.rem = B.filled<double>((size_t)S * kPhases, 0.0);
+
+  // ---- vehicles ------------------------------------------------------------
+  DevVehicles& dv = w.v;
+  dv.origin = B.upload(sp.origin);
+  dv.dest = B.upload(sp.dest);
+  dv.advance = B.upload(sp.advance);
+  dv.depart = B.upload(sp.depart);
+  dv.state = B.filled<uint8_t>(V, kPending);
+  dv.at_node = B.filled<int32_t>(V, -1);
+  dv.on_edge = B.filled<int32_t>(V, -1);
+  dv.progress = B.filled<int64_t>(V, 0);
+  dv.overshoot = B.filled<int64_t>(V, 0);
+  dv.queued_phase = B.filled<int32_t>(V, -1);
+  dv.joined = B.filled<int64_t>(V, 0);
+  dv.arrive = B.filled<int64_t>(V, -1);
+  dv.latency_debt = B.filled<int64_t>(V, 0);
+  dv.driving = B.filled<int64_t>(V, 0);
+  dv.queued = B.filled<int64_t>(V, 0);
+  dv.lat_steps = B.filled<int64_t>(V, 0);
+  dv.path_len_mm = B.filled<int64_t>(V, 0);
+  dv.decisions = B.filled<int32_t>(V, 0);
+  dv.deviations = B.filled<int32_t>(V, 0);
+  dv.qnext = B.filled<int32_t>(V, -1);
+  dv.arr_next = B.filled<int32_t>(V, -1);
+  dv.dec_next = B.filled<int32_t>(V, -1);
+  dv.dflag = B.filled<int32_t>(V, 0);
+  dv.pos = B.filled<int32_t>(V, 0);
+  dv.path = B.alloc<int32_t>((size_t)V * p.path_cap);
+  dv.path_n = B.filled<int32_t>(V, 0);
+  dv.plan = B.alloc<int32_t>((size_t)V * p.plan_cap);
+  dv.plan_n = B.filled<int32_t>(V, 0);
+  dv.plan_step = B.filled<int64_t>(V, -1);
+  dv.plan_done = B.filled<uint8_t>(V, 0);
+
+  // ---- control block -----------------------------------------------------------
+  DevCtl c0{};
+  c0.step = 0;
+  c0.stop_at = 0;
+  int64_t n0 = 0;
+  for (int32_t vid = 0; vid < V; ++vid) n0 += sp.depart[vid] == 0;  // count_active at step 0
+  c0.n_t = n0;
+  c0.done = c.max_steps <= 0 ? 1 : 0;
+  h->ctl = B.alloc<DevCtl>(1);
+  CK(cudaMemcpy(h->ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
+  w.ctl = h->ctl;
+  CK(cudaMallocHost(&h->ctl_host, sizeof(DevCtl)));
+  *h->ctl_host = c0;
+  CK(cudaMallocHost(&h->stop_host, sizeof(int64_t)));
+  if (p.need_positions) {
+    h->res.scan_temp_bytes = scan_temp_bytes(V);
+    h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
+  }
+  CK(cudaEventCreate(&h->ev_a));
+  CK(cudaEventCreate(&h->ev_b));
+  CK(cudaDeviceSynchronize());
+}
+
+cudaGraphExec_t capture(gmaco_engine* h, int steps, bool timing) {
+  StepResources r = h->res;
+  r.capturing = true;
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = cudaSuccess;
+  for (int i = 0; i < steps && err == cudaSuccess; ++i)
+    err = launch_step(h->w, r, h->stream, timing ? h->ev_begin[i] : nullptr, timing ? h->ev_end[i] : nullptr);
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+  CK(err);
+  CK(e2);
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  return exec;
+}
+
+void refresh_ctl(gmaco_engine* h) {
+  CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->ctl_host->error) throw std::runtime_error("device path buffer overflow");
+}
+
+int64_t run_steps(gmaco_engine* h, int64_t steps) {
+  refresh_ctl(h);
+  const int64_t start = h->ctl_host->step;
+  if (steps <= 0 || h->ctl_host->done) return 0;
+  const int64_t target = start + steps;
+  if (h->timing && h->ev_begin.empty()) {
+    h->ev_begin.resize(kGraphSteps);
+    h->ev_end.resize(kGraphSteps);
+    for (int i = 0; i < kGraphSteps; ++i) {
+      CK(cudaEventCreate(&h->ev_begin[i]));
+      CK(cudaEventCreate(&h->ev_end[i]));
+    }
+  }
+  *h->stop_host = target;
+  CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+  h->last_walk_ms = 0.0;
+  h->last_walk_launches = 0;
+  CK(cudaEventRecord(h->ev_a, h->stream));
+  int64_t cur = start;
+  while (cur < target && !h->ctl_host->done) {
+    const int64_t remaining = target - cur;
+    const bool big = remaining >= kGraphSteps;
+    cudaGraphExec_t& ge = h->timing ? (big ? h->tgraph_big : h->tgraph_one) : (big ? h->graph_big : h->graph_one);
+    if (!ge) ge = capture(h, big ? kGraphSteps : 1, h->timing);
+    CK(cudaGraphLaunch(ge, h->stream));
+    if (h->timing) {
+      refresh_ctl(h);
+      const int64_t ran = h->ctl_host->step - cur;
+      for (int64_t i = 0; i < ran; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_begin[i], h->ev_end[i]));
+        h->last_walk_ms += ms;
+      }
+      h->last_walk_launches += ran;
+      cur = h->ctl_host->step;
+    } else if (big) {
+      cur += kGraphSteps;
+      if (cur < target) {  // peek for early completion every few chunks
+        refresh_ctl(h);
+        cur = h->ctl_host->step;
+      }
+    } else {
+      cur += 1;
+    }
+  }
+  CK(cudaEventRecord(h->ev_b, h->stream));
+  refresh_ctl(h);
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev_a, h->ev_b));
+  h->last_step_ms = ms;
+  return h->ctl_host->step - start;
+}
+
+void collect(gmaco_engine* h, gmaco_run_result* r, double* travel, int32_t* rvid, int32_t* rnode, int32_t cap) {
+  refresh_ctl(h);
+  const DevWorld& w = h->w;
+  const int32_t V = w.p.V;
+  auto state = download(w.v.state, V);
+  auto arrive = download(w.v.arrive, V);
+  auto depart = download(w.v.depart, V);
+  auto queued = download(w.v.queued, V);
+  auto decisions = download(w.v.decisions, V);
+  auto at_node = download(w.v.at_node, V);
+  const DevCtl& c = *h->ctl_host;
+  gmaco_run_result out{};
+  out.steps_executed = c.step;
+  double ts = 0.0, ws = 0.0;
+  int32_t k = 0;
+  const double dt = h->cfg.dt_s, lat = h->cfg.decision_latency_s;
+  for (int32_t i = 0; i < V; ++i) {  // engine.cpp:407-422, vid order
+    if (travel) travel[i] = -1.0;
+    if (state[i] == kArrived) {
+      const double t = static_cast<double>(arrive[i] - depart[i]) * dt;
+      if (travel) travel[i] = t;
+      ts += t;
+      ws += static_cast<double>(queued[i]) * dt + static_cast<double>(decisions[i]) * lat;
+      ++out.completed_count;
+    } else if (state[i] == kRetired) {
+      ++out.retired_count;
+      if (k < cap) {
+        if (rvid) rvid[k] = i;
+        if (rnode) rnode[k] = at_node[i];
+      }
+      ++k;
+    }
+  }
+  if (out.completed_count > 0) {
+    out.mean_travel_s = ts / out.completed_count;
+    out.mean_wait_s = ws / out.completed_count;
+  }
+  if (c.qsamples > 0) out.mean_queue_len = static_cast<double>(c.qtotal) / static_cast<double>(c.qsamples);
+  out.max_edge_occupancy = c.max_occ;
+  out.wall_clock_ms = h->wall_ms;
+  *r = out;
+}
+
+template <class T>
+void scatter_slots(const gmaco_engine* h, const std::vector<T>& by_slot, T* by_edge) {
+  for (int32_t s = 0; s < h->g.m; ++s) by_edge[h->g.out_edge[s]] = by_slot[s];
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int32_t gmaco_abi_version(void) { return GMACO_ABI_VERSION; }
+
+int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist, const gmaco_sim_config* cfg,
+                 int32_t device, gmaco_engine** out) {
+  if (!out) {
+    g_create_err = "gmaco_create: out is null";
+    return GMACO_EVALIDATION;
+  }
+  *out = nullptr;
+  auto h = std::make_unique<gmaco_engine>();
+  h->device = device;
+  int rc = guarded(nullptr, [&] { build_world(h.get(), graph, dist, cfg); });
+  if (rc != GMACO_OK) return rc;
+  *out = h.release();
+  return GMACO_OK;
+}
+
+int gmaco_step(gmaco_engine* h, int64_t steps, int64_t* executed) {
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const int64_t k = run_steps(h, steps);
+    if (executed) *executed = k;
+  });
+}
+
+int gmaco_finished(gmaco_engine* h, int32_t* out) {
+  if (!h || !out) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    refresh_ctl(h);
+    *out = h->ctl_host->done;
+  });
+}
+
+int gmaco_current_step(gmaco_engine* h, int64_t* out) {
+  if (!h || !out) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    refresh_ctl(h);
+    *out = h->ctl_host->step;
+  });
+}
+
+int gmaco_run(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s) {
+  if (!h || !result) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (true) {
+      refresh_ctl(h);
+      if (h->ctl_host->done) break;
+      run_steps(h, int64_t(1) << 40);
+    }
+    h->wall_ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    collect(h, result, travel_times_s, nullptr, nullptr, 0);
+  });
+}
+
+int gmaco_collect(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s, int32_t* retired_vid,
+                  int32_t* retired_node, int32_t retired_cap) {
+  if (!h || !result) return GMACO_EVALIDATION;
+  return guarded(h, [&] { collect(h, result, travel_times_s, retired_vid, retired_node, retired_cap); });
+}
+
+int gmaco_get_pheromone(gmaco_engine* h, int64_t* tau) {
+  if (!h || !tau) return GMACO_EVALIDATION;
+  return guarded(h, [&] { scatter_slots(h, download(h->w.tau, h->g.m), tau); });
+}
+
+int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
+  if (!h || !tau) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const int32_t m = h->g.m;
+    std::vector<int64_t> t(m);
+    std::vector<double> wt(m);
+    auto eta = download(h->w.g.eta_beta, m);
+    for (int32_t s = 0; s < m; ++s) {
+      t[s] = tau[h->g.out_edge[s]];
+      const double tau_d = static_cast<double>(t[s]) / 1e6;
+      wt[s] = (h->w.p.alpha == 1.0 ? tau_d : std::pow(tau_d, h->w.p.alpha)) * eta[s];
+    }
+    CK(cudaMemcpy(h->w.tau, t.data(), m * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->w.weight, wt.data(), m * 8, cudaMemcpyHostToDevice));
+  });
+}
+
+int gmaco_get_occupancy(gmaco_engine* h, int32_t* occ) {
+  if (!h || !occ) return GMACO_EVALIDATION;
+  return guarded(h, [&] { scatter_slots(h, download(h->w.occ_cur, h->g.m), occ); });
+}
+
+int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
+  if (!h || !v) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevVehicles& d = h->w.v;
+    const size_t V = h->w.p.V;
+    auto cp = [&](auto* dst, const auto* src) {
+      if (dst) CK(cudaMemcpy(dst, src, V * sizeof(*dst), cudaMemcpyDeviceToHost));
+    };
+    cp(v->origin, d.origin);
+    cp(v->dest, d.dest);
+    cp(v->advance_mm, d.advance);
+    cp(v->state, d.state);
+    cp(v->at_node, d.at_node);
+    cp(v->progress_mm, d.progress);
+    cp(v->overshoot_mm, d.overshoot);
+    cp(v->queued_phase, d.queued_phase);
+    cp(v->queue_joined_step, d.joined);
+    cp(v->depart_step, d.depart);
+    cp(v->arrive_step, d.arrive);
+    cp(v->latency_debt_us, d.latency_debt);
+    cp(v->driving_steps, d.driving);
+    cp(v->queued_steps, d.queued);
+    cp(v->latency_steps, d.lat_steps);
+    cp(v->decisions, d.decisions);
+    cp(v->deviations, d.deviations);
+    cp(v->path_length_mm, d.path_len_mm);
+    if (v->on_edge) {
+      auto oe = download(d.on_edge, V);
+      for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->g.out_edge[oe[i]];
+    }
+    if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
+      for (size_t i = 0; i < V; ++i)
+        v->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+    }
+  });
+}
+
+int gmaco_signal_count(gmaco_engine* h, int32_t* out) {
+  if (!h || !out) return GMACO_EVALIDATION;
+  *out = h->S;
+  return GMACO_OK;
+}
+
+int gmaco_get_signals(gmaco_engine* h, const gmaco_signal_view* v, int64_t cap) {
+  if (!h || !v) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevSignals& d = h->w.s;
+    const size_t S = h->S, Q = S * kPhases;
+    auto cp = [&](auto* dst, const auto* src, size_t n) {
+      if (dst) CK(cudaMemcpy(dst, src, n * sizeof(*dst), cudaMemcpyDeviceToHost));
+    };
+    if (v->node) std::copy(h->sig_node.begin(), h->sig_node.end(), v->node);
+    cp(v->green, d.green, S);
+    cp(v->cycle_cursor, d.cursor, S);
+    cp(v->discharge_lanes, d.lanes, S);
+    cp(v->green_elapsed_steps, d.el_steps, S);
+    cp(v->green_elapsed_s, d.el_s, S);
+    cp(v->queue_len, d.qlen, Q);
+    cp(v->head_wait_s, d.head_wait, Q);
+    cp(v->service_remainder, d.rem, Q);
+    if (v->queue_vid || v->queue_enqueue_step) {
+      auto qlen = download(d.qlen, Q);
+      auto qhead = download(d.qhead, Q);
+      auto qnext = download(h->w.v.qnext, h->w.p.V);
+      auto joined = download(h->w.v.joined, h->w.p.V);
+      int64_t k = 0;
+      for (size_t q = 0; q < Q; ++q) {
+        int32_t vid = qhead[q];
+        for (int32_t j = 0; j < qlen[q]; ++j, ++k) {
+          if (k < cap) {
+            if (v->queue_vid) v->queue_vid[k] = vid;
+            if (v->queue_enqueue_step) v->queue_enqueue_step[k] = joined[vid];
+          }
+          vid = qnext[vid];
+        }
+      }
+      if (k > cap) throw ValidationError("gmaco_get_signals: queue_cap too small");
+    }
+  });
+}
+
+int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out) {
+  if (!h || !out) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    refresh_ctl(h);
+    const DevCtl& c = *h->ctl_host;
+    out->ant_steps = c.ant_steps;
+    out->vehicle_routes = c.vehicle_routes;
+    out->decisions = c.decisions;
+    out->candidates = c.candidates;
+    out->degree_sum = c.degree_sum;
+  });
+}
+
+int gmaco_route_query(gmaco_engine* h, int32_t vid, int32_t planned, int32_t* out_edges, int32_t cap,
+                      int32_t* out_len) {
+  if (!h || !out_len) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevWorld& w = h->w;
+    if (vid < 0 || vid >= w.p.V) throw ValidationError(fmt("route_query: invalid vehicle %d", vid));
+    int32_t n = 0;
+    const int32_t* base;
+    int32_t pcap;
+    if (planned) {
+      if (w.p.algorithm != GMACO_COLONY) throw ValidationError("route_query: planned routes need the colony algorithm");
+      CK(cudaMemcpy(&n, w.v.plan_n + vid, 4, cudaMemcpyDeviceToHost));
+      base = w.v.plan;
+      pcap = w.p.plan_cap;
+    } else {
+      if (!w.p.record_paths) throw ValidationError("route_query: realized paths are not recorded for this config");
+      CK(cudaMemcpy(&n, w.v.path_n + vid, 4, cudaMemcpyDeviceToHost));
+      base = w.v.path;
+      pcap = w.p.path_cap;
+    }
+    *out_len = n;
+    const int32_t k = std::min(n, cap);
+    if (k > 0 && out_edges) {
+      std::vector<int32_t> s(k);
+      CK(cudaMemcpy(s.data(), base + (size_t)vid * pcap, k * 4, cudaMemcpyDeviceToHost));
+      for (int32_t i = 0; i < k; ++i) out_edges[i] = h->g.out_edge[s[i]];
+    }
+  });
+}
+
+int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int32_t* current, const int32_t* dest,
+                    const uint64_t* rng_entity, const uint64_t* rng_step, int64_t n_t, int32_t* out_next,
+                    int32_t* out_via, uint8_t* out_deviated) {
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    if (count < 0) throw ValidationError("next_node: negative count");
+    if (count == 0) return;
+    if (algorithm < GMACO_DIJKSTRA || algorithm > GMACO_MACO_P)
+      throw ValidationError(fmt("next_node: unsupported algorithm %d", algorithm));
+    for (int32_t i = 0; i < count; ++i)
+      if (current[i] < 0 || current[i] >= h->g.n || dest[i] < 0 || dest[i] >= h->g.n)
+        throw ValidationError("next_node: invalid node id");
+    DevBuffers tmp;
+    std::vector<int32_t> c(current, current + count), d(dest, dest + count);
+    std::vector<uint64_t> e(count, 0), s(count, 0);
+    if (rng_entity) e.assign(rng_entity, rng_entity + count);
+    if (rng_step) s.assign(rng_step, rng_step + count);
+    int32_t* dc = tmp.upload(c);
+    int32_t* dd = tmp.upload(d);
+    uint64_t* de = tmp.upload(e);
+    uint64_t* ds = tmp.upload(s);
+    int32_t* on = tmp.alloc<int32_t>(count);
+    int32_t* ov = tmp.alloc<int32_t>(count);
+    uint8_t* odv = tmp.alloc<uint8_t>(count);
+    CK(launch_next_node(h->w, algorithm == GMACO_MACO_P ? GMACO_MACO : algorithm, count, dc, dd, de, ds, n_t, on,
+                        ov, odv, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(out_next, on, count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_via, ov, count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_deviated, odv, count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gmaco_set_timing(gmaco_engine* h, int32_t enabled) {
+  if (!h) return GMACO_EVALIDATION;
+  h->timing = enabled != 0;
+  return GMACO_OK;
+}
+
+int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches) {
+  if (!h) return GMACO_EVALIDATION;
+  if (walk_ms) *walk_ms = h->last_walk_ms;
+  if (step_ms) *step_ms = h->last_step_ms;
+  if (walk_launches) *walk_launches = h->last_walk_launches;
+  return GMACO_OK;
+}
+
+const char* gmaco_last_error(const gmaco_engine* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+void gmaco_destroy(gmaco_engine* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,967 @@
+// kernels.cu — sm_100a kernels of one GMACO-P engine step.
+//
+// Stage map (engine.cpp:352-400 sequential_step):
+//   B   k_decide<Dist>  reference routing decision per vehicle
+//       k_colony<Dist>  colony: K ants per vehicle walk to the destination
+//   C,D,E1 k_signals    density sample, green assignment, FIFO discharge
+//   E2  k_move          motion, arrivals, edge-load histogram, next n_t
+//   E3  k_e3            enqueue commit in ascending vid + signal timers
+//   F   k_scoped        sibling-scoped MACO replay (decrement_siblings_only)
+//   F+G k_edges         MACO fold / deposit + evaporation + next-step weights
+// The whole step is free of floating-point atomics: every cross-thread
+// reduction is an integer sum/min/max, so results are bit-deterministic.
+// Floating-point expressions use explicit _rn intrinsics (and the library is
+// built with -fmad=false) so they round exactly like the reference's
+// FMA-free x86-64 build.
+
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.h"
+
+namespace gmaco {
+
+// ---------------------------------------------------------------------------
+// counter-based RNG (rng.hpp:21-56) and Philox4x32-10
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t h = mix64(seed);
+  h = mix64(h ^ a);
+  h = mix64(h ^ b);
+  return mix64(h ^ c);
+}
+__device__ __forceinline__ double to_unit(uint64_t bits) {
+  return __dmul_rn((double)(bits >> 11), 0x1.0p-53);
+}
+__device__ __forceinline__ uint64_t philox_bits(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return ((uint64_t)c0 << 32) | c1;
+}
+// Ant uniform: REFERENCE keying reduces to RngKey{seed, vid, step} of the
+// reference ACO decision at ant 0 hop 0 (routing.cpp:97-98).
+__device__ __forceinline__ double ant_uniform(int rng, uint64_t seed, int64_t step, int32_t vid,
+                                              int32_t ant, int32_t hop) {
+  if (rng == 1) {
+    const uint64_t a = (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32);
+    const uint64_t b = (uint64_t)step | ((uint64_t)(uint32_t)hop << 40);
+    return to_unit(draw(seed, 5, a, b));
+  }
+  return to_unit(philox_bits((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hop,
+                             (uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+// ---------------------------------------------------------------------------
+// distance service
+// ---------------------------------------------------------------------------
+template <int DK>
+struct Target {
+  int32_t dest;
+  int32_t rd, cd, cols;
+  int64_t len;
+  const int64_t* __restrict__ trow;
+  __device__ __forceinline__ Target(const DevDist& d, int32_t dst) : dest(dst) {
+    if (DK == 1) {
+      cols = d.cols;
+      rd = dst / d.cols;
+      cd = dst - rd * d.cols;
+      len = d.grid_len;
+      trow = nullptr;
+    } else {
+      const int32_t slot = d.slot_of ? d.slot_of[dst] : dst;
+      trow = slot < 0 ? nullptr : d.table + (size_t)slot * d.n;
+    }
+  }
+  __device__ __forceinline__ int64_t dist(int32_t x) const {
+    if (DK == 1) {
+      const int32_t r = x / cols, c = x - r * cols;
+      return (int64_t)(abs(r - rd) + abs(c - cd)) * len;
+    }
+    return trow ? __ldg(trow + x) : kInf;
+  }
+};
+
+// Candidate scan of node x (candidate_neighbors, routing.cpp:16-30) as
+// register bitmasks over the row's slot offsets (ascending neighbour id).
+struct Row {
+  int32_t first, deg;
+  uint32_t reach, closer, sp;  // reachable / strictly closer / on a shortest path
+  int64_t dx;
+};
+
+template <int DK>
+__device__ __forceinline__ Row scan_row(const DevGraph& g, const Target<DK>& t, int32_t x) {
+  Row r;
+  const int2 ri = __ldg(g.row + x);
+  r.first = ri.x;
+  r.deg = ri.y;
+  r.dx = t.dist(x);
+  r.reach = r.closer = r.sp = 0u;
+  for (int i = 0; i < r.deg; ++i) {
+    const int32_t nb = __ldg(g.col + r.first + i);
+    const int64_t dn = t.dist(nb);
+    if (dn == kInf) continue;
+    r.reach |= 1u << i;
+    if (dn < r.dx) r.closer |= 1u << i;
+  }
+  return r;
+}
+
+// Dijkstra hop: smallest neighbour on a shortest path (greedy_hop,
+// net.cpp:387-395; next_node_dijkstra, routing.cpp:117-125).
+template <int DK>
+__device__ __forceinline__ int32_t dijkstra_pick(const DevGraph& g, const Target<DK>& t, int32_t x) {
+  const int64_t dx = t.dist(x);
+  if (dx == kInf) return -1;
+  const int2 ri = __ldg(g.row + x);
+  for (int i = 0; i < ri.y; ++i) {
+    const int32_t s = ri.x + i;
+    const int64_t dn = t.dist(__ldg(g.col + s));
+    if (dn == kInf) continue;
+    if (__ldg(g.len + s) + dn == dx) return s;
+  }
+  return -1;
+}
+
+// ACO roulette over candidate mask (routing.cpp:88-113): sequential
+// left-to-right total and cumulative sums, u·total point, uniform fallback.
+__device__ __forceinline__ int32_t roulette_pick(const double* __restrict__ W, int32_t first,
+                                                 uint32_t cand, double u) {
+  double total = 0.0;
+  int c = 0;
+  for (uint32_t m = cand; m; m &= m - 1) {
+    total = __dadd_rn(total, W[first + __ffs(m) - 1]);
+    ++c;
+  }
+  int pick_i = c - 1;
+  if (total <= 0.0 || !isfinite(total)) {
+    int p = (int)__dmul_rn(u, (double)c);
+    pick_i = p < c - 1 ? p : c - 1;
+  } else {
+    const double point = __dmul_rn(u, total);
+    double cum = 0.0;
+    int i = 0;
+    for (uint32_t m = cand; m; m &= m - 1, ++i) {
+      cum = __dadd_rn(cum, W[first + __ffs(m) - 1]);
+      if (point < cum) {
+        pick_i = i;
+        break;
+      }
+    }
+  }
+  uint32_t m = cand;
+  for (int i = 0; i < pick_i; ++i) m &= m - 1;
+  return first + __ffs(m) - 1;
+}
+
+// MACO min-pheromone with deviation (routing.cpp:32-75).
+__device__ __forceinline__ int32_t maco_pick(const DevWorld& w, int32_t first, uint32_t cand,
+                                             int64_t n_t, bool* deviated) {
+  int32_t prim = -1, c = 0;
+  int64_t tp = 0;
+  for (uint32_t m = cand; m; m &= m - 1, ++c) {
+    const int32_t s = first + __ffs(m) - 1;
+    const int64_t t = w.tau[s];
+    if (prim < 0 || t < tp) {
+      prim = s;
+      tp = t;
+    }
+  }
+  bool trigger = false;
+  if (c >= 2) {
+    if (w.p.deviation_mode == 0)
+      trigger = n_t > w.p.deviation_threshold;
+    else
+      trigger = (int64_t)w.occ_cur[prim] > w.p.deviation_threshold;
+  }
+  *deviated = trigger;
+  if (!trigger) return prim;
+  // second: initial = candidate 1 if primary is candidate 0 else candidate 0
+  const int32_t c0 = first + __ffs(cand) - 1;
+  const uint32_t rest = cand & (cand - 1);
+  int32_t second = prim == c0 ? first + __ffs(rest) - 1 : c0;
+  int64_t ts = w.tau[second];
+  for (uint32_t m = cand; m; m &= m - 1) {
+    const int32_t s = first + __ffs(m) - 1;
+    if (s == prim || s == second) continue;
+    const int64_t t = w.tau[s];
+    if (t < ts) {
+      second = s;
+      ts = t;
+    }
+  }
+  return second;
+}
+
+__device__ __forceinline__ bool skip_step(const DevCtl* ctl) {
+  return ctl->done || ctl->step >= ctl->stop_at;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)((blockDim.x + 31) >> 5); ++i) r += smem[i];
+  return r;  // valid in thread 0
+}
+
+// Vehicle takes edge `slot` (engine.cpp:207-216).
+__device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_t slot, bool deviated,
+                                          int32_t from) {
+  const DevVehicles& v = w.v;
+  v.state[vid] = kOnEdge;
+  v.on_edge[vid] = slot;
+  v.progress[vid] = v.overshoot[vid];
+  v.overshoot[vid] = 0;
+  v.latency_debt[vid] += w.p.latency_us;
+  v.decisions[vid] += 1;
+  if (deviated) v.deviations[vid] += 1;
+  if (w.p.record_paths) {
+    const int32_t k = v.path_n[vid];
+    if (k < w.p.path_cap) {
+      v.path[(size_t)vid * w.p.path_cap + k] = slot;
+      v.path_n[vid] = k + 1;
+    } else {
+      atomicExch(&w.ctl->error, 1);  // path buffer overflow → host error
+    }
+  }
+  v.path_len_mm[vid] += w.g.len[slot];
+  if (w.p.algorithm == 2 || w.p.algorithm == 3) {  // MACO commit bookkeeping
+    const int32_t key = w.p.siblings_only ? from : slot;
+    v.dec_next[vid] = atomicExch(&w.dec_head[key], vid);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B: reference decision kernel (dijkstra / aco / maco), one thread per vehicle
+// ---------------------------------------------------------------------------
+template <int DK>
+__global__ void __launch_bounds__(256) k_decide(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t step = w.ctl->step;
+  long long decided = 0, cands = 0, degs = 0;
+  if (vid < w.p.V) {
+    const DevVehicles& v = w.v;
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    if (w.p.need_positions) v.dflag[vid] = 0;
+    if (st == kAtNode) {
+      const int32_t x = v.at_node[vid];
+      const Target<DK> t(w.d, v.dest[vid]);
+      int32_t slot = -1;
+      bool dev = false;
+      if (w.p.algorithm == 0) {
+        slot = dijkstra_pick<DK>(w.g, t, x);
+      } else {
+        const Row r = scan_row<DK>(w.g, t, x);
+        degs += r.deg;
+        const uint32_t cand = (w.p.progress_filter && r.closer) ? r.closer : r.reach;
+        if (cand) {
+          cands += __popc(cand);
+          if (w.p.algorithm == 1) {
+            const double u = to_unit(draw(w.p.seed, 5, (uint64_t)vid, (uint64_t)step));
+            slot = roulette_pick(w.weight, r.first, cand, u);
+          } else {
+            slot = maco_pick(w, r.first, cand, w.ctl->n_t, &dev);
+          }
+        }
+      }
+      if (slot < 0) {
+        v.state[vid] = kRetired;  // engine.cpp:202-205
+      } else {
+        take_edge(w, vid, slot, dev, x);
+        if (w.p.need_positions) v.dflag[vid] = 1;
+        decided = 1;
+      }
+    }
+  }
+  const long long d = block_sum(decided, red);
+  const long long c = block_sum(cands, red);
+  const long long g = block_sum(degs, red);
+  if (threadIdx.x == 0 && d) {
+    atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)d);
+    atomicAdd((unsigned long long*)&w.ctl->decisions, (unsigned long long)d);
+    atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)d);
+  }
+  if (threadIdx.x == 0 && (c || g)) {
+    atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)c);
+    atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B (colony): K ants per vehicle, one thread per ant; best tour by
+// (cost, ant) via a shared-memory 64-bit atomicMin; the winner replays its
+// walk (counter RNG) to materialize the tour.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kCostCap = (1ull << 53) - 1;
+
+struct WalkOut {
+  int64_t cost;
+  int32_t hops;
+  bool first_ok;
+  long long steps, cands, degs;
+};
+
+template <int DK, bool kFilter>
+__device__ __forceinline__ WalkOut ant_walk(const DevWorld& w, const Target<DK>& t, int32_t vid,
+                                            int32_t ant, int32_t start, int64_t step,
+                                            int32_t* __restrict__ tour) {
+  WalkOut o{0, 0, false, 0, 0, 0};
+  const int32_t dest = t.dest;
+  const int32_t max_hops = w.p.max_hops;
+  const int32_t hop_limit = w.p.hop_limit;
+  int32_t tabu[kTabu];
+  int32_t ntabu = 0, tpos = 0;
+  if (!kFilter) {
+    tabu[0] = start;
+    ntabu = 1;
+    tpos = 1;
+  }
+  int32_t x = start;
+  while (x != dest && (hop_limit == 0 || o.hops < hop_limit)) {
+    if (o.hops >= max_hops) {
+      o.cost = kInf;
+      return o;
+    }
+    const Row r = scan_row<DK>(w.g, t, x);
+    uint32_t cand;
+    if (kFilter) {
+      cand = r.closer ? r.closer : r.reach;
+    } else {
+      cand = r.reach;
+      for (uint32_t m = cand; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const int32_t nb = __ldg(w.g.col + r.first + i);
+        for (int k = 0; k < ntabu; ++k)
+          if (tabu[k] == nb) cand &= ~(1u << i);
+      }
+    }
+    o.degs += r.deg;
+    if (!cand) {
+      o.cost = kInf;
+      return o;
+    }
+    if (o.hops == 0) o.first_ok = true;
+    o.cands += __popc(cand);
+    const double u = ant_uniform(w.p.rng, w.p.seed, step, vid, ant, o.hops);
+    const int32_t s = roulette_pick(w.weight, r.first, cand, u);
+    o.cost += w.ecost[s];
+    x = __ldg(w.g.col + s);
+    if (tour) tour[o.hops] = s;
+    o.hops++;
+    o.steps++;
+    if (!kFilter) {
+      tabu[tpos] = x;
+      tpos = (tpos + 1) % kTabu;
+      if (ntabu < kTabu) ntabu++;
+    }
+  }
+  return o;
+}
+
+template <int DK, bool kFilter>
+__global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  constexpr int kMaxVpb = 256;
+  __shared__ unsigned long long best[kMaxVpb];
+  __shared__ int32_t start_s[kMaxVpb];
+  __shared__ uint8_t deciding_s[kMaxVpb];
+  __shared__ long long red[32];
+  const int K = w.p.ants;
+  const int vpb = blockDim.x / K;
+  const int lv = threadIdx.x / K;
+  const int ant = threadIdx.x - lv * K;
+  const int32_t vid = blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.V;
+  const int64_t step = w.ctl->step;
+  const DevVehicles& v = w.v;
+
+  if (live && ant == 0) {
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    int32_t start = -1;
+    const bool deciding = st == kAtNode;
+    if (deciding)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kQueued)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kOnEdge)
+      start = w.g.col[v.on_edge[vid]];
+    if (start >= 0 && start == v.dest[vid]) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      start = -1;
+    }
+    start_s[lv] = start;
+    deciding_s[lv] = deciding;
+    best[lv] = ~0ull;
+  }
+  __syncthreads();
+  long long steps = 0, cands = 0, degs = 0, routes = 0, decided = 0;
+  int32_t start = -1;
+  WalkOut o{};
+  if (live) {
+    start = start_s[lv];
+    if (start >= 0) {
+      const Target<DK> t(w.d, v.dest[vid]);
+      o = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, nullptr);
+      steps = o.steps;
+      cands = o.cands;
+      degs = o.degs;
+      const uint64_t c = o.cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)o.cost;
+      atomicMin(&best[lv], (c << 10) | (uint64_t)ant);
+    }
+  }
+  __syncthreads();
+  if (live && start >= 0 && ant == (int)(best[lv] & 1023u)) {
+    const bool deciding = deciding_s[lv];
+    if (!o.first_ok) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      if (deciding) v.state[vid] = kRetired;
+    } else {
+      const Target<DK> t(w.d, v.dest[vid]);
+      int32_t* tour = v.plan + (size_t)vid * w.p.plan_cap;
+      const WalkOut r = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, tour);
+      v.plan_n[vid] = r.hops;
+      v.plan_step[vid] = step;
+      const bool done = r.hops > 0 && w.g.col[tour[r.hops - 1]] == t.dest;
+      v.plan_done[vid] = done;
+      routes = 1;
+      if (done && w.p.deposit == 1) {  // best-tour deposit (exact int64 sums)
+        int64_t len = 0;
+        for (int i = 0; i < r.hops; ++i) len += w.g.len[tour[i]];
+        const double km = __ddiv_rn((double)len, 1e6);  // deposit_amount, pheromone.cpp:73-78
+        const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+        for (int i = 0; i < r.hops; ++i)
+          atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+      }
+      if (deciding) {
+        take_edge(w, vid, tour[0], false, start);
+        decided = 1;
+      }
+    }
+  }
+  steps = block_sum(steps, red);
+  cands = block_sum(cands, red);
+  degs = block_sum(degs, red);
+  routes = block_sum(routes, red);
+  decided = block_sum(decided, red);
+  if (threadIdx.x == 0) {
+    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
+    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
+    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
+    if (routes) atomicAdd((unsigned long long*)&w.ctl->vehicle_routes, (unsigned long long)routes);
+    if (decided) {
+      atomicAdd((unsigned long long*)&w.ctl->decisions, (unsigned long long)decided);
+      atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)decided);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C, D, E1: one thread per signal (engine.cpp:219-252, signals.cpp:62-135)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int order_position(const DevParams& p, int ph) {
+  for (int i = 0; i < kPhases; ++i)
+    if (p.order[i] == ph) return i;
+  return 0;
+}
+__device__ __forceinline__ int next_in_order(const DevParams& p, int cursor) {
+  return p.order[(order_position(p, cursor) + 1) % kPhases];
+}
+
+__device__ int select_phase(const DevParams& p, const int32_t* q, const double* hw, int cursor) {
+  if (p.controller == 0) return next_in_order(p, cursor);
+  if (p.controller == 1) {
+    const int pos = order_position(p, cursor);
+    for (int i = 0; i < kPhases; ++i) {
+      const int ph = p.order[(pos + i) % kPhases];
+      if (q[ph] > 0) return ph;
+    }
+    return next_in_order(p, cursor);
+  }
+  int best = -1;
+  for (int ph = 0; ph < kPhases; ++ph)
+    if (q[ph] > p.th_max && (best == -1 || q[ph] > q[best])) best = ph;
+  if (best != -1) return best;
+  for (int ph = 0; ph < kPhases; ++ph)
+    if (hw[ph] > p.t_max && (best == -1 || hw[ph] > hw[best])) best = ph;
+  if (best != -1) return best;
+  for (int ph = 0; ph < kPhases; ++ph)
+    if (q[ph] > 0 && (best == -1 || q[ph] > q[best])) best = ph;
+  if (best != -1) return best;
+  return next_in_order(p, cursor);
+}
+
+__global__ void __launch_bounds__(256) k_signals(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  long long qt = 0;
+  if (s < w.p.S) {
+    const DevSignals& S = w.s;
+    int32_t q[kPhases];
+    double hw[kPhases];
+#pragma unroll
+    for (int ph = 0; ph < kPhases; ++ph) {
+      q[ph] = S.qlen[s * kPhases + ph];
+      hw[ph] = S.head_wait[s * kPhases + ph];
+      qt += q[ph];
+    }
+    // D: assign at an epoch (engine.cpp:223-239, assign_green signals.cpp:111-117)
+    int green = S.green[s];
+    if (!(S.el_s[s] < w.p.green_duration_s)) {
+      green = select_phase(w.p, q, hw, S.cursor[s]);
+      S.green[s] = green;
+      S.cursor[s] = green;
+      S.el_s[s] = 0.0;
+      S.el_steps[s] = 0;
+      S.rem[s * kPhases + green] = 0.0;
+    }
+    // E1: discharge (signals.cpp:119-135, engine.cpp:241-252)
+    const int k = s * kPhases + green;
+    double rem = S.rem[k];
+    rem = __dadd_rn(rem, __dmul_rn(__dmul_rn(w.p.saturation_flow, (double)S.lanes[s]), w.p.dt_s));
+    int budget = (int)floor(rem);
+    rem = __dsub_rn(rem, (double)budget);
+    S.rem[k] = rem;
+    int32_t len = q[green];
+    if (budget > 0 && len > 0) {
+      int32_t head = S.qhead[k];
+      const int64_t step = w.ctl->step;
+      const int32_t node = S.node[s];
+      while (budget > 0 && len > 0) {
+        const int32_t vid = head;
+        head = w.v.qnext[vid];
+        --len;
+        --budget;
+        w.v.queued[vid] += step - w.v.joined[vid] + 1;
+        w.v.state[vid] = kAtNode;
+        w.v.at_node[vid] = node;
+        w.v.queued_phase[vid] = -1;
+      }
+      S.qhead[k] = len ? head : -1;
+      if (!len) S.qtail[k] = -1;
+      S.qlen[k] = len;
+    }
+    if (len == 0) S.head_wait[k] = 0.0;
+  }
+  qt = block_sum(qt, red);
+  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+}
+
+// ---------------------------------------------------------------------------
+// E2: motion (engine.cpp:254-295) + occupancy histogram (engine.cpp:316-322)
+// + the next step's count_active / unfinished counts.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_move(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  long long active = 0, unfinished = 0;
+  if (vid < w.p.V) {
+    const DevVehicles& v = w.v;
+    const int64_t step = w.ctl->step;
+    uint8_t st = v.state[vid];
+    if (st == kOnEdge) {
+      if (v.latency_debt[vid] >= w.p.dt_us) {
+        v.latency_debt[vid] -= w.p.dt_us;
+        v.lat_steps[vid] += 1;
+      } else {
+        const int64_t prog = v.progress[vid] + v.advance[vid];
+        v.driving[vid] += 1;
+        const int32_t slot = v.on_edge[vid];
+        const int64_t L = w.g.len[slot];
+        if (prog < L) {
+          v.progress[vid] = prog;
+        } else {
+          const int32_t reached = w.g.col[slot];
+          const int32_t bind = w.g.bind[slot];
+          if (reached == v.dest[vid]) {
+            st = kArrived;
+            v.progress[vid] = prog;
+            v.arrive[vid] = step + 1;
+            if (w.p.deposit == 0 && (w.p.algorithm == 1 || w.p.algorithm == 4)) {
+              // ACO deposit on completion (engine.cpp:341-346, pheromone.cpp:80-90);
+              // per-edge sum-then-clamp equals sequential clamping for amounts >= 0.
+              const int32_t n = v.path_n[vid];
+              if (n > 0) {
+                const double km = __ddiv_rn((double)v.path_len_mm[vid], 1e6);
+                const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+                const int32_t* path = v.path + (size_t)vid * w.p.path_cap;
+                for (int i = 0; i < n; ++i)
+                  atomicAdd((unsigned long long*)&w.dep[path[i]], (unsigned long long)amount);
+              }
+            }
+          } else if (bind >= 0) {
+            st = kQueued;
+            v.at_node[vid] = reached;
+            v.queued_phase[vid] = bind & 7;
+            v.joined[vid] = step + 1;
+            v.progress[vid] = 0;
+            v.arr_next[vid] = atomicExch(&w.s.arr_head[bind], vid);
+          } else {
+            st = kAtNode;
+            v.at_node[vid] = reached;
+            v.overshoot[vid] = prog - L;
+            v.progress[vid] = 0;
+          }
+          v.state[vid] = st;
+        }
+      }
+      if (st == kOnEdge) atomicAdd(&w.occ_new[v.on_edge[vid]], 1);
+    }
+    active = st == kAtNode || st == kOnEdge || st == kQueued ||
+             (st == kPending && v.depart[vid] == step + 1);
+    unfinished = st != kArrived && st != kRetired;
+  }
+  active = block_sum(active, red);
+  unfinished = block_sum(unfinished, red);
+  if (threadIdx.x == 0) {
+    if (active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
+    if (unfinished) atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// E3: enqueue commit in ascending vid (engine.cpp:297-301) + timers
+// (engine.cpp:303-314).  This step's arrivals all share joined = step+1,
+// larger than every queued key, so FIFO order = old queue then the
+// arrivals by ascending vid.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_e3(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= w.p.S) return;
+  const DevSignals& S = w.s;
+  const int64_t now = w.ctl->step + 1;
+  for (int ph = 0; ph < kPhases; ++ph) {
+    const int k = s * kPhases + ph;
+    const int32_t chain = S.arr_head[k];
+    int32_t len = S.qlen[k];
+    if (chain >= 0) {
+      S.arr_head[k] = -1;
+      int32_t tail = S.qtail[k];
+      int32_t head = S.qhead[k];
+      int32_t last = -1;
+      for (;;) {  // append chain members in ascending vid (selection; chains are short)
+        int32_t best = INT32_MAX;
+        for (int32_t c = chain; c >= 0; c = w.v.arr_next[c])
+          if (c > last && c < best) best = c;
+        if (best == INT32_MAX) break;
+        w.v.qnext[best] = -1;
+        if (tail < 0)
+          head = best;
+        else
+          w.v.qnext[tail] = best;
+        tail = best;
+        ++len;
+        last = best;
+      }
+      S.qhead[k] = head;
+      S.qtail[k] = tail;
+      S.qlen[k] = len;
+    }
+    S.head_wait[k] = len == 0 ? 0.0 : __dmul_rn((double)(now - w.v.joined[S.qhead[k]]), w.p.dt_s);
+  }
+  const int64_t e = S.el_steps[s] + 1;
+  S.el_steps[s] = e;
+  S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
+}
+
+// ---------------------------------------------------------------------------
+// F (scoped MACO): per decision node, replay the step's decisions at that
+// node in ascending vid (apply_maco_update_scoped, pheromone.cpp:48-59).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= w.g.n) return;
+  const int32_t chain = w.dec_head[u];
+  if (chain < 0) return;
+  w.dec_head[u] = -1;
+  const int2 ri = w.g.row[u];
+  int32_t last = -1;
+  for (;;) {
+    int32_t best = INT32_MAX;
+    for (int32_t c = chain; c >= 0; c = w.v.dec_next[c])
+      if (c > last && c < best) best = c;
+    if (best == INT32_MAX) break;
+    last = best;
+    const int32_t chosen = w.v.on_edge[best];
+    for (int i = 0; i < ri.y; ++i) {
+      const int32_t s = ri.x + i;
+      const int64_t t = w.tau[s];
+      w.tau[s] = s == chosen ? min(w.p.tau_hi, t + w.p.inc) : max(w.p.tau_lo, t - w.p.dec);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F + G per slot: MACO fold (fold_maco_edge, parallel.cpp:77-92) or exact
+// deposit sum-then-clamp, evaporation (pheromone.cpp:61-67), colony
+// congestion term, occupancy hand-off + max, weights for the next step.
+// The last block finalizes the step (n_t, step, finished()).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_edges(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ int32_t smax[32];
+  __shared__ bool is_last;
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const DevParams& p = w.p;
+  int32_t occ = 0;
+  if (s < w.g.m) {
+    int64_t t = w.tau[s];
+    const int alg = p.algorithm;
+    if ((alg == 2 || alg == 3) && !p.siblings_only) {
+      const int64_t D = w.ctl->dcount;
+      const int32_t chain = w.dec_head[s];
+      int64_t done = 0;
+      if (chain >= 0) {
+        w.dec_head[s] = -1;
+        int32_t last = -1;
+        for (;;) {
+          int32_t best = INT32_MAX;
+          for (int32_t c = chain; c >= 0; c = w.v.dec_next[c])
+            if (c > last && c < best) best = c;
+          if (best == INT32_MAX) break;
+          last = best;
+          const int64_t pos = w.v.pos[best];
+          const int64_t gap = pos - done;
+          if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
+          t = min(p.tau_hi, t + p.inc);
+          done = pos + 1;
+        }
+      }
+      const int64_t gap = D - done;
+      if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
+    } else if (alg == 1 || alg == 4) {
+      const int64_t d = w.dep[s];
+      if (d) {
+        t = min(p.tau_hi, t + d);
+        w.dep[s] = 0;
+      }
+    }
+    // G: evaporate_one
+    const int64_t scaled = (int64_t)floor(__dmul_rn(p.one_minus_rho, (double)t));
+    t = max(p.tau_lo, scaled);
+    occ = w.occ_new[s];
+    if (alg == 4 && p.cong_evap && occ > 0) t = max(p.tau_lo, t - p.dec * (int64_t)occ);
+    w.tau[s] = t;
+    w.occ_cur[s] = occ;
+    w.occ_new[s] = 0;
+    // next step's roulette weight / tour cost (routing.cpp:90-94)
+    if (alg == 1 || alg == 4) {
+      const double tau_d = __ddiv_rn((double)t, 1e6);
+      const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : pow(tau_d, p.alpha));
+      double wt = __dmul_rn(ta, w.g.eta_beta[s]);
+      int64_t cost = w.g.len[s];
+      if (alg == 4 && p.congestion) {
+        const int32_t b = w.g.bind[s];
+        const int32_t load = occ + (b >= 0 ? w.s.qlen[b] : 0);
+        wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
+        cost = cost + cost * (int64_t)load;
+      }
+      w.weight[s] = wt;
+      w.ecost[s] = cost;
+    }
+  }
+  // block max of occupancy
+  int32_t m = occ;
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, smax[i]);
+    if (m > 0) atomicMax(&w.ctl->max_occ, m);
+    __threadfence();
+    const unsigned prev = atomicAdd(&w.ctl->blocks_done, 1u);
+    is_last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {  // step finalize (engine.cpp:399, 146-152)
+    __threadfence();
+    DevCtl* c = w.ctl;
+    c->blocks_done = 0;
+    c->qsamples += p.S;
+    c->n_t = c->n_next;
+    c->n_next = 0;
+    c->dcount = 0;
+    const int64_t step = c->step + 1;
+    c->step = step;
+    c->done = (step >= p.max_steps || c->unfinished == 0) ? 1 : 0;
+    c->unfinished = 0;
+    __threadfence();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched next-hop query (gmaco_next_node): next_node_{dijkstra,aco,maco}
+// over the current field, one thread per query.
+// ---------------------------------------------------------------------------
+template <int DK>
+__global__ void k_next_node(DevWorld w, int algorithm, int count, const int32_t* cur, const int32_t* dst,
+                            const uint64_t* entity, const uint64_t* stepk, int64_t n_t, int32_t* out_next,
+                            int32_t* out_via, uint8_t* out_dev) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int32_t x = cur[i];
+  const Target<DK> t(w.d, dst[i]);
+  int32_t slot = -1;
+  bool dev = false;
+  if (algorithm == 0) {
+    slot = dijkstra_pick<DK>(w.g, t, x);
+  } else {
+    const Row r = scan_row<DK>(w.g, t, x);
+    const uint32_t cand = (w.p.progress_filter && r.closer) ? r.closer : r.reach;
+    if (cand) {
+      if (algorithm == 1) {
+        // fresh weights from the current tau (no colony congestion factor)
+        double total = 0.0;
+        int c = 0;
+        double wv[kMaxDegree];
+        for (uint32_t m = cand; m; m &= m - 1, ++c) {
+          const int32_t s = r.first + __ffs(m) - 1;
+          const double tau_d = __ddiv_rn((double)w.tau[s], 1e6);
+          const double ta = w.p.alpha == 1.0 ? tau_d : (w.p.alpha == 0.0 ? 1.0 : pow(tau_d, w.p.alpha));
+          wv[c] = __dmul_rn(ta, w.g.eta_beta[s]);
+          total = __dadd_rn(total, wv[c]);
+        }
+        const double u = to_unit(draw(w.p.seed, 5, entity[i], stepk[i]));
+        int pick_i = c - 1;
+        if (total <= 0.0 || !isfinite(total)) {
+          const int pp = (int)__dmul_rn(u, (double)c);
+          pick_i = pp < c - 1 ? pp : c - 1;
+        } else {
+          const double point = __dmul_rn(u, total);
+          double cum = 0.0;
+          for (int j = 0; j < c; ++j) {
+            cum = __dadd_rn(cum, wv[j]);
+            if (point < cum) {
+              pick_i = j;
+              break;
+            }
+          }
+        }
+        uint32_t m = cand;
+        for (int j = 0; j < pick_i; ++j) m &= m - 1;
+        slot = r.first + __ffs(m) - 1;
+      } else {
+        slot = maco_pick(w, r.first, cand, n_t, &dev);
+      }
+    }
+  }
+  out_via[i] = slot < 0 ? -1 : w.g.slot_edge[slot];
+  out_next[i] = slot < 0 ? -1 : w.g.col[slot];
+  out_dev[i] = dev ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// launch plumbing
+// ---------------------------------------------------------------------------
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void colony_shape(int ants, int* threads, int* vpb) {
+  int t = ants <= 256 ? 256 : ((ants + 31) / 32) * 32;
+  *threads = t;
+  *vpb = t / ants;
+}
+
+cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
+                        cudaEvent_t walk_begin, cudaEvent_t walk_end) {
+  const int V = w.p.V, S = w.p.S, m = w.g.m, n = w.g.n;
+  if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
+  if (w.p.algorithm == 4) {
+    int threads, vpb;
+    colony_shape(w.p.ants, &threads, &vpb);
+    const unsigned grid = blocks_for(V, vpb);
+    if (w.d.kind == 1) {
+      if (w.p.progress_filter)
+        k_colony<1, true><<<grid, threads, 0, st>>>(w);
+      else
+        k_colony<1, false><<<grid, threads, 0, st>>>(w);
+    } else {
+      if (w.p.progress_filter)
+        k_colony<0, true><<<grid, threads, 0, st>>>(w);
+      else
+        k_colony<0, false><<<grid, threads, 0, st>>>(w);
+    }
+  } else {
+    if (w.d.kind == 1)
+      k_decide<1><<<blocks_for(V, 256), 256, 0, st>>>(w);
+    else
+      k_decide<0><<<blocks_for(V, 256), 256, 0, st>>>(w);
+  }
+  if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
+  if (S > 0) k_signals<<<blocks_for(S, 256), 256, 0, st>>>(w);
+  k_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
+  if (S > 0) k_e3<<<blocks_for(S, 256), 256, 0, st>>>(w);
+  if (w.p.algorithm == 2 || w.p.algorithm == 3) {
+    if (w.p.siblings_only) {
+      k_scoped<<<blocks_for(n, 256), 256, 0, st>>>(w);
+    } else {
+      size_t bytes = r.scan_temp_bytes;
+      cudaError_t e = cub::DeviceScan::ExclusiveSum(r.scan_temp, bytes, w.v.dflag, w.v.pos, V, st);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  k_edges<<<blocks_for(m, 256), 256, 0, st>>>(w);
+  return cudaGetLastError();
+}
+
+size_t scan_temp_bytes(int V) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int32_t*)nullptr, (int32_t*)nullptr, V);
+  return bytes;
+}
+
+cudaError_t launch_next_node(const DevWorld& w, int algorithm, int count, const int32_t* cur,
+                             const int32_t* dst, const uint64_t* entity, const uint64_t* stepk, int64_t n_t,
+                             int32_t* out_next, int32_t* out_via, uint8_t* out_dev, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  if (w.d.kind == 1)
+    k_next_node<1><<<blocks_for(count, 128), 128, 0, st>>>(w, algorithm, count, cur, dst, entity, stepk,
+                                                           n_t, out_next, out_via, out_dev);
+  else
+    k_next_node<0><<<blocks_for(count, 128), 128, 0, st>>>(w, algorithm, count, cur, dst, entity, stepk,
+                                                           n_t, out_next, out_via, out_dev);
+  return cudaGetLastError();
+}
+
+}  // namespace gmaco

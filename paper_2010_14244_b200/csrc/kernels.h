@@ -1,0 +1,29 @@
+// kernels.h — host-side entry points of kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace gmaco {
+
+struct StepResources {
+  void* scan_temp = nullptr;
+  size_t scan_temp_bytes = 0;
+  bool capturing = false;
+};
+
+// Enqueues one engine step (stages B..G) on `st`.  Optional events bracket
+// the stage-B walk kernel (recorded as external events while capturing).
+cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
+                        cudaEvent_t walk_begin, cudaEvent_t walk_end);
+size_t scan_temp_bytes(int V);
+void colony_shape(int ants, int* threads, int* vpb);
+cudaError_t launch_next_node(const DevWorld& w, int algorithm, int count, const int32_t* cur,
+                             const int32_t* dst, const uint64_t* entity, const uint64_t* stepk, int64_t n_t,
+                             int32_t* out_next, int32_t* out_via, uint8_t* out_dev, cudaStream_t st);
+
+}  // namespace gmaco

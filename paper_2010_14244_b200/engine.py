@@ -1,0 +1,209 @@
+"""ctypes binding of libgmaco.so (the C ABI in include/gmaco.h).
+
+`Engine` exposes the same interface as the oracle worlds (oracle/oracle.py)
+so parity tests compare like with like.  There is no fallback: if the
+in-tree library is missing, or no CUDA device is present, construction
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libgmaco.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "gmaco.h")
+
+P = C.POINTER
+i32, i64, u64, u8, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint8, C.c_double
+
+# every entry point include/gmaco.h declares, with its ctypes signature
+SIGNATURES = {
+    "gmaco_abi_version": (i32,),
+    "gmaco_create": (C.c_int, P(abi.GraphDesc), P(abi.DistanceDesc), P(abi.SimConfig), i32, P(C.c_void_p)),
+    "gmaco_attach_comm": (C.c_int, C.c_void_p, i32, i32, C.c_void_p),
+    "gmaco_nccl_unique_id": (C.c_int, C.c_void_p),
+    "gmaco_step": (C.c_int, C.c_void_p, i64, P(i64)),
+    "gmaco_finished": (C.c_int, C.c_void_p, P(i32)),
+    "gmaco_run": (C.c_int, C.c_void_p, P(abi.RunResult), P(f64)),
+    "gmaco_collect": (C.c_int, C.c_void_p, P(abi.RunResult), P(f64), P(i32), P(i32), i32),
+    "gmaco_get_pheromone": (C.c_int, C.c_void_p, P(i64)),
+    "gmaco_set_pheromone": (C.c_int, C.c_void_p, P(i64)),
+    "gmaco_get_occupancy": (C.c_int, C.c_void_p, P(i32)),
+    "gmaco_get_vehicles": (C.c_int, C.c_void_p, P(abi.VehicleView)),
+    "gmaco_get_signals": (C.c_int, C.c_void_p, P(abi.SignalView), i64),
+    "gmaco_signal_count": (C.c_int, C.c_void_p, P(i32)),
+    "gmaco_get_counters": (C.c_int, C.c_void_p, P(abi.Counters)),
+    "gmaco_current_step": (C.c_int, C.c_void_p, P(i64)),
+    "gmaco_route_query": (C.c_int, C.c_void_p, i32, i32, P(i32), i32, P(i32)),
+    "gmaco_next_node": (C.c_int, C.c_void_p, i32, i32, P(i32), P(i32), P(u64), P(u64), i64, P(i32), P(i32),
+                        P(u8)),
+    "gmaco_last_timing": (C.c_int, C.c_void_p, P(f64), P(f64), P(i64)),
+    "gmaco_set_timing": (C.c_int, C.c_void_p, i32),
+    "gmaco_last_error": (C.c_char_p, C.c_void_p),
+    "gmaco_destroy": (None, C.c_void_p),
+}
+
+_lib = None
+
+
+class EngineError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[status {code}] {msg}")
+        self.code = code
+
+
+def load(path: str = LIB_PATH):
+    """Loads the in-tree engine library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise EngineError(abi.ERUNTIME, f"engine library not built: {path} (run __graft_entry__.build())")
+        L = C.CDLL(path)
+        for name, sig in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = sig[0]
+            f.argtypes = list(sig[1:])
+        _lib = L
+    return _lib
+
+
+class Engine:
+    """One device world (gmaco_create ... gmaco_destroy)."""
+
+    def __init__(self, net, cfg: abi.SimConfig, dist: abi.DistanceDesc | None = None, device: int = 0):
+        self.L = load()
+        self.net = net
+        self.cfg = cfg
+        self.V = cfg.vehicle_count
+        self.m = net.edge_count
+        self.dist = dist if dist is not None else abi.DistanceDesc(kind=abi.DIST_DENSE)
+        h = C.c_void_p()
+        rc = self.L.gmaco_create(C.byref(net.desc()), C.byref(self.dist), C.byref(cfg), device, C.byref(h))
+        if rc:
+            raise EngineError(rc, self.L.gmaco_last_error(None).decode())
+        self.h = h
+
+    def _check(self, rc):
+        if rc:
+            raise EngineError(rc, self.L.gmaco_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.gmaco_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # -- stepping ---------------------------------------------------------------
+    def step(self, n: int = 1) -> int:
+        k = i64()
+        self._check(self.L.gmaco_step(self.h, n, C.byref(k)))
+        return k.value
+
+    def finished(self) -> bool:
+        f = i32()
+        self._check(self.L.gmaco_finished(self.h, C.byref(f)))
+        return bool(f.value)
+
+    def current_step(self) -> int:
+        s = i64()
+        self._check(self.L.gmaco_current_step(self.h, C.byref(s)))
+        return s.value
+
+    def run(self):
+        r = abi.RunResult()
+        tt = np.zeros(self.V, dtype=np.float64)
+        self._check(self.L.gmaco_run(self.h, C.byref(r), abi.ptr(tt, f64)))
+        return self.collect()
+
+    # -- snapshots --------------------------------------------------------------
+    def collect(self):
+        r = abi.RunResult()
+        tt = np.zeros(self.V, dtype=np.float64)
+        rv = np.zeros(self.V, dtype=np.int32)
+        rn = np.zeros(self.V, dtype=np.int32)
+        self._check(self.L.gmaco_collect(self.h, C.byref(r), abi.ptr(tt, f64), abi.ptr(rv, i32),
+                                         abi.ptr(rn, i32), self.V))
+        k = r.retired_count
+        return r, tt, list(zip(rv[:k].tolist(), rn[:k].tolist()))
+
+    def vehicles(self) -> dict:
+        arrs, view = abi.vehicle_arrays(self.V)
+        self._check(self.L.gmaco_get_vehicles(self.h, C.byref(view)))
+        return arrs
+
+    def signal_count(self) -> int:
+        s = i32()
+        self._check(self.L.gmaco_signal_count(self.h, C.byref(s)))
+        return s.value
+
+    def signals(self) -> dict:
+        S = self.signal_count()
+        arrs, view = abi.signal_arrays(S, self.V + 1)
+        self._check(self.L.gmaco_get_signals(self.h, C.byref(view), self.V + 1))
+        total = int(arrs["queue_len"].sum())
+        arrs["queue_vid"] = arrs["queue_vid"][:total]
+        arrs["queue_enqueue_step"] = arrs["queue_enqueue_step"][:total]
+        return arrs
+
+    def pheromone(self) -> np.ndarray:
+        t = np.zeros(self.m, dtype=np.int64)
+        self._check(self.L.gmaco_get_pheromone(self.h, abi.ptr(t, i64)))
+        return t
+
+    def set_pheromone(self, tau):
+        t = np.ascontiguousarray(tau, dtype=np.int64)
+        self._check(self.L.gmaco_set_pheromone(self.h, abi.ptr(t, i64)))
+
+    def occupancy(self) -> np.ndarray:
+        o = np.zeros(self.m, dtype=np.int32)
+        self._check(self.L.gmaco_get_occupancy(self.h, abi.ptr(o, i32)))
+        return o
+
+    def counters(self) -> abi.Counters:
+        c = abi.Counters()
+        self._check(self.L.gmaco_get_counters(self.h, C.byref(c)))
+        return c
+
+    def route(self, vid: int, planned: bool = False) -> np.ndarray:
+        cap = max(self.net.node_count, 1 << 16)
+        out = np.zeros(cap, dtype=np.int32)
+        n = i32()
+        self._check(self.L.gmaco_route_query(self.h, vid, int(planned), abi.ptr(out, i32), cap, C.byref(n)))
+        return out[: n.value].copy()
+
+    def next_node(self, algorithm, current, dest, entity=None, step=None, n_t=0):
+        cur = np.ascontiguousarray(current, dtype=np.int32)
+        dst = np.ascontiguousarray(dest, dtype=np.int32)
+        n = len(cur)
+        ent = np.ascontiguousarray(entity if entity is not None else np.zeros(n), dtype=np.uint64)
+        stp = np.ascontiguousarray(step if step is not None else np.zeros(n), dtype=np.uint64)
+        nxt = np.zeros(n, dtype=np.int32)
+        via = np.zeros(n, dtype=np.int32)
+        dev = np.zeros(n, dtype=np.uint8)
+        self._check(self.L.gmaco_next_node(self.h, algorithm, n, abi.ptr(cur, i32), abi.ptr(dst, i32),
+                                           abi.ptr(ent, u64), abi.ptr(stp, u64), n_t, abi.ptr(nxt, i32),
+                                           abi.ptr(via, i32), abi.ptr(dev, u8)))
+        return nxt, via, dev
+
+    # -- timing -----------------------------------------------------------------
+    def set_timing(self, on: bool):
+        self._check(self.L.gmaco_set_timing(self.h, int(on)))
+
+    def last_timing(self):
+        a, b, n = f64(), f64(), i64()
+        self._check(self.L.gmaco_last_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
+
+def declared_symbols(header: str = HEADER) -> list[str]:
+    """Function names declared in include/gmaco.h."""
+    import re
+    text = open(header).read()
+    return sorted(set(re.findall(r"\b(gmaco_[a-z_0-9]+)\s*\(", text)))

@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact for every integer / index / state field and every double the
+reference produces (RunResult::identical_to, engine.cpp:34-40), on the same
+seeded inputs.  The oracle (oracle/_build, pinned against the compiled
+reference by tests/test_oracle_vs_ref.py) is the checker; where the compiled
+reference itself is present (oracle/_ref) it is compared too.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2010_14244_b200 import abi, networks
+from paper_2010_14244_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+ALGS = ["dijkstra", "aco", "maco", "maco-p"]
+
+
+def _cfg(alg, V, seed, **kw):
+    cfg = abi.default_config(algorithm=alg, vehicle_count=V, seed=seed)
+    for k, v in kw.items():
+        if k == "siblings":
+            cfg.pheromone.decrement_siblings_only = v
+        elif k == "edge_occupancy":
+            cfg.routing.deviation_mode = abi.DEV_EDGE_OCCUPANCY
+            cfg.routing.deviation_threshold = v
+        elif k == "progress_filter":
+            cfg.routing.progress_filter = v
+        elif k == "alpha_beta":
+            cfg.routing.aco_alpha, cfg.routing.aco_beta = v
+        elif k == "tau_min":
+            cfg.pheromone.tau_min = v
+            cfg.pheromone.tau_init_lo = max(v, cfg.pheromone.tau_init_lo)
+        elif k == "threshold":
+            cfg.routing.deviation_threshold = v
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+def _same_snapshot(a, b, where=""):
+    va, vb = a.vehicles(), b.vehicles()
+    for f in abi.VEHICLE_FIELDS:
+        assert np.array_equal(va[f], vb[f]), f"{where} vehicle field {f}"
+    sa, sb = a.signals(), b.signals()
+    for f in sa:
+        assert np.array_equal(sa[f], sb[f]), f"{where} signal field {f}"
+    assert np.array_equal(a.pheromone(), b.pheromone()), f"{where} pheromone"
+    assert np.array_equal(a.occupancy(), b.occupancy()), f"{where} occupancy"
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_c1_run_identical(alg, seed):
+    """BASELINE config 1: 10x10 grid, 100 vehicles."""
+    net = networks.grid(10, 10)
+    cfg = _cfg(alg, 100, seed)
+    ref = O.PortWorld(net, cfg).run()
+    for dist in (abi.DistanceDesc(kind=abi.DIST_DENSE), net.grid_distance()):
+        got = Engine(net, cfg, dist).run()
+        assert O.results_identical(got, ref), (alg, seed, dist.kind)
+    if O.ref_available():
+        assert O.results_identical(O.ref_run(net, cfg), ref)
+
+
+VARIANTS = [
+    dict(siblings=1),
+    dict(edge_occupancy=1),
+    dict(decision_latency_s=1.5),
+    dict(spawn=abi.UNIFORM_WINDOW, spawn_window_steps=30),
+    dict(controller=abi.ADAPTIVE),
+    dict(progress_filter=0, max_steps=300),
+    dict(alpha_beta=(0.0, 0.0)),
+    dict(dt_s=0.7, max_steps=800),
+    dict(tau_min=1.0),
+    dict(threshold=50),
+    dict(max_steps=0),
+    dict(max_steps=7),
+]
+
+
+@pytest.mark.parametrize("variant", range(len(VARIANTS)))
+@pytest.mark.parametrize("alg", ALGS)
+def test_variants_identical(alg, variant):
+    net = networks.grid(6, 9, 137.5, 2, "all")
+    cfg = _cfg(alg, 150, 7, **VARIANTS[variant])
+    ref = O.PortWorld(net, cfg).run()
+    got = Engine(net, cfg).run()
+    assert O.results_identical(got, ref)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_city_graph_identical(alg):
+    """Irregular graph: the reference's own generate_city(52, 64) network."""
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    net = O.ref_city(52, 64)
+    for seed in (1, 5):
+        cfg = _cfg(alg, 200, seed)
+        ref = O.ref_run(net, cfg)
+        got = Engine(net, cfg).run()
+        assert O.results_identical(got, ref), seed
+
+
+def test_blocks_od_identical():
+    net = networks.grid(8, 8)
+    for alg in ALGS:
+        cfg = _cfg(alg, 200, 11)
+        keep = abi.Blocks(cfg, np.arange(0, 6), np.arange(58, 64))
+        ref = O.PortWorld(net, cfg).run()
+        got = Engine(net, cfg, net.grid_distance()).run()
+        assert O.results_identical(got, ref), alg
+        del keep
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_c2_stepwise_state(alg):
+    """BASELINE config 2 (32x32, signals at every intersection, 1k vehicles):
+    full world state after every few steps."""
+    net = networks.grid(32, 32, signals="all")
+    cfg = _cfg(alg, 1000, 3, max_steps=200)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for k in (1, 1, 3, 10, 25, 60):
+        assert gpu.step(k) == cpu.step(k)
+        _same_snapshot(gpu, cpu, f"{alg} step {cpu.current_step()}")
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_next_node_batch():
+    """Per-vehicle route query next_node_* (routing.hpp:52-73) on random pairs."""
+    net = networks.grid(16, 16)
+    cfg = _cfg("maco", 300, 4, max_steps=40)
+    gpu = Engine(net, cfg)
+    cpu = O.PortWorld(net, cfg)
+    gpu.step(20)
+    cpu.step(20)
+    rng = np.random.default_rng(0)
+    n = 5000
+    cur = rng.integers(0, net.node_count, n)
+    dst = rng.integers(0, net.node_count, n)
+    keep = cur != dst
+    cur, dst = cur[keep], dst[keep]
+    ent = rng.integers(0, 1 << 62, len(cur), dtype=np.uint64)
+    stp = rng.integers(0, 1 << 20, len(cur), dtype=np.uint64)
+    for alg in (abi.DIJKSTRA, abi.ACO, abi.MACO):
+        for n_t in (0, 5000):
+            a = gpu.next_node(alg, cur, dst, ent, stp, n_t)
+            b = cpu.next_node(alg, cur, dst, ent, stp, n_t)
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y), (alg, n_t)
+
+
+def test_colony_anchor_equals_reference_aco():
+    """K=1, 1-hop walk, reference RNG key ⇒ identical to Algorithm::Aco."""
+    net = networks.grid(10, 10)
+    for seed in (1, 2, 3):
+        aco = _cfg("aco", 100, seed)
+        col = abi.colony_anchor(_cfg("colony", 100, seed))
+        ref = O.PortWorld(net, aco).run()
+        got = Engine(net, col, net.grid_distance()).run()
+        assert O.results_identical(got, ref), seed
+        if O.ref_available():
+            assert O.results_identical(O.ref_run(net, aco), ref)
+
+
+@pytest.mark.parametrize("ants", [1, 20, 64, 100])
+def test_colony_production_stepwise(ants):
+    """GMACO-P colonies (Philox, congestion, best-tour deposit): planned
+    tours, pheromone and counters bit-exact against the oracle port."""
+    net = networks.grid(12, 12, signals="all")
+    cfg = abi.colony_production(_cfg("colony", 300, 9, max_steps=60), ants=ants)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for k in (1, 2, 5, 12):
+        assert gpu.step(k) == cpu.step(k)
+        _same_snapshot(gpu, cpu, f"colony step {cpu.current_step()}")
+        for vid in range(cfg.vehicle_count):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_colony_no_filter_tabu():
+    """Progress filter off: tabu tenure + hop cap (cycles possible)."""
+    net = networks.grid(8, 8)
+    cfg = abi.colony_production(_cfg("colony", 120, 5, max_steps=40, progress_filter=0), ants=16)
+    cfg.colony.max_hops = 40
+    gpu = Engine(net, cfg)
+    cpu = O.PortWorld(net, cfg)
+    for k in (1, 4, 10):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, "colony-nofilter")
+        for vid in range(cfg.vehicle_count):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+
+
+def test_colony_reference_rng_multi_ant():
+    net = networks.grid(9, 9)
+    cfg = abi.colony_production(_cfg("colony", 150, 3, max_steps=50), ants=8)
+    cfg.colony.rng = abi.RNG_REFERENCE
+    cfg.colony.deposit = abi.DEPOSIT_COMPLETION
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    assert O.results_identical(gpu.run(), cpu.run())
+    assert np.array_equal(gpu.pheromone(), cpu.pheromone())
+
+
+def test_realized_paths():
+    net = networks.grid(10, 10)
+    cfg = _cfg("aco", 100, 4)
+    gpu = Engine(net, cfg)
+    cpu = O.PortWorld(net, cfg)
+    gpu.run()
+    cpu.run()
+    for vid in range(100):
+        assert np.array_equal(gpu.route(vid), cpu.route(vid)), vid
