@@ -154,6 +154,24 @@ def reference_world(seed, max_steps):
     return O.RefWorld(net, cfg), net
 
 
+class RefSampler:
+    """Reference colony iterations on a C2 world; a finished world is
+    replaced by a fresh one (next seed) so no timed iteration is empty."""
+
+    def __init__(self, threads):
+        self.threads = threads
+        self.seed = 1
+        self.w = None
+
+    def iteration(self):
+        if self.w is None or self.w.finished():
+            self.w, _ = reference_world(self.seed, 100000)
+            self.seed += 1
+        t0 = time.perf_counter()
+        s, r = self.w.colony_iteration(ANTS, self.threads)
+        return s, r, time.perf_counter() - t0
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -162,16 +180,16 @@ def run_reference(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
         return
     threads = os.cpu_count() or 1
-    w, _ = reference_world(1, args.warmup + args.steps + 10)
+    smp = RefSampler(threads)
     for _ in range(args.warmup):
-        w.colony_iteration(ANTS, threads)
-    t0 = time.perf_counter()
+        smp.iteration()
     steps = routes = 0
+    dt = 0.0
     for _ in range(args.steps):
-        s, r = w.colony_iteration(ANTS, threads)
+        s, r, t = smp.iteration()
         steps += s
         routes += r
-    dt = time.perf_counter() - t0
+        dt += t
     value = steps / dt
     line = {
         "impl": "reference", "metric": "ant-steps/sec", "value": value, "unit": "ant-steps/s",
@@ -192,18 +210,18 @@ def cpu_baseline(seconds):
     from oracle import oracle as O
     threads = os.cpu_count() or 1
     if O.ref_available():
-        w, _ = reference_world(1, 1000)
-        w.colony_iteration(ANTS, threads)
+        smp = RefSampler(threads)
+        smp.iteration()
         steps = its = 0
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < seconds:
-            s, _ = w.colony_iteration(ANTS, threads)
+        dt = 0.0
+        while dt < seconds:
+            s, _, t = smp.iteration()
             steps += s
+            dt += t
             its += 1
-        dt = time.perf_counter() - t0
         return {"value": steps / dt, "unit": "ant-steps/s", "cores": threads, "kind": "reference",
                 "sample": f"{its} colony iterations (C2, 64 ants, reference next_node_aco on {threads} "
-                          f"threads + sequential_step), {dt:.1f} s"}
+                          f"threads + sequential_step; finished worlds restarted), {dt:.1f} s"}
     from paper_2010_14244_b200 import networks
     net = networks.grid(GRID, GRID, signals="all")
     w = O.PortWorld(net, workload_config(1, 1000), net.grid_distance())
@@ -233,29 +251,21 @@ def run_ours(args, rank, world, local):
         pg = dist
     net = networks.grid(GRID, GRID, signals="all")
     max_steps = args.warmup + args.steps + 1
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     # ---- device-resident throughput (value) ---------------------------------
+    # K back-to-back iterations enqueued without host sync, each bracketed by
+    # CUDA events on the engine stream; a 512 MiB memset flushes L2 between
+    # iterations outside the events.
     eng = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
     eng.step(args.warmup)
-    eng.set_timing(True)
     c0 = eng.counters()
-    walk_ms = step_ms = 0.0
-    launches = 0
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.fill_(1.0)  # L2 flush between timed iterations (outside the events)
-            torch.cuda.synchronize()
-            eng.step(1)
-            wm, sm, nl = eng.last_timing()
-            walk_ms += wm
-            step_ms += sm
-            launches += nl
-    torch.cuda.synchronize()
+        walk, stepms = eng.bench_steps(args.steps, L2_FLUSH_BYTES)
     c1 = eng.counters()
+    walk_ms, step_ms, launches = float(walk.sum()), float(stepms.sum()), args.steps
     ant_steps = c1.ant_steps - c0.ant_steps
     routes = c1.vehicle_routes - c0.vehicle_routes
 
@@ -266,6 +276,17 @@ def run_ours(args, rank, world, local):
     d.degree_sum = c1.degree_sum - c0.degree_sum
     d.candidates = c1.candidates - c0.candidates
     alg_bytes = algorithmic_bytes(d)
+
+    # chained (no flush, multi-step CUDA graphs) on a fresh world, for reference
+    eng2 = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
+    eng2.step(args.warmup)
+    s0 = eng2.counters().ant_steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng2.step(args.steps)
+    chained_s = time.perf_counter() - t0
+    chained = (eng2.counters().ant_steps - s0) / chained_s
+    eng2.close()
 
     # ---- end to end through the C ABI from host buffers (e2e) ---------------
     import ctypes as C
@@ -319,6 +340,9 @@ def run_ours(args, rank, world, local):
         "vehicle_routes_per_sec": tot_routes / t_dev,
         "ant_steps_per_iteration": tot_steps / args.steps / world,
         "walk_kernel_share": (walk_ms / step_ms) if step_ms else None,
+        "chained_graph_value": chained,
+        "ms_per_step_p50": float(np.median(stepms)),
+        "walk_ms_per_step_p50": float(np.median(walk)),
         "gpu_launches": int(args.steps * launches_per_step(eng)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src,

@@ -253,6 +253,11 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
  * bench roofline: walk kernel total and whole-step total. */
 int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches);
 int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
+/* Benchmark entry point: enqueues `steps` engine steps without host
+ * synchronization, each bracketed by CUDA events on the engine stream
+ * (walk kernel, whole step), with an L2-flushing memset of flush_bytes
+ * between steps outside the events; returns per-step device times. */
+int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms);
 
 const char* gmaco_last_error(const gmaco_engine* h);
 void gmaco_destroy(gmaco_engine* h);

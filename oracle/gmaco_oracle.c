@@ -67,18 +67,20 @@ void og_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 
 /* Ant uniform.  REFERENCE keying reduces to RngKey{seed, vid, step} of the
  * reference ACO decision (routing.cpp:97-98, engine.cpp:189-194) at ant 0,
- * hop 0.  PHILOX keying: counter (step, vid, ant, hop), key = seed. */
+ * hop 0.  PHILOX keying: counter (step, vid, ant, hop/2), key = seed. */
 double og_ant_uniform(int rng, uint64_t seed, int64_t step, int32_t vid, int32_t ant, int32_t hop) {
   if (rng == GMACO_RNG_REFERENCE) {
     uint64_t a = (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32);
     uint64_t b = (uint64_t)step | ((uint64_t)(uint32_t)hop << 40);
     return og_to_unit(og_draw(seed, S_ACO, a, b));
   }
-  uint32_t ctr[4] = {(uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hop};
+  /* one 128-bit Philox block serves two hops: counter (step, vid, ant, hop/2),
+   * hop&1 selects the 64-bit half */
+  uint32_t ctr[4] = {(uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hop >> 1};
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t o[4];
   og_philox4x32_10(ctr, key, o);
-  return og_to_unit(((uint64_t)o[0] << 32) | o[1]);
+  return og_to_unit((hop & 1) ? (((uint64_t)o[2] << 32) | o[3]) : (((uint64_t)o[0] << 32) | o[1]));
 }
 
 /* ------------------------------------------------------------------------ */

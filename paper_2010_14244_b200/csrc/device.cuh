@@ -21,7 +21,11 @@ enum VState : uint8_t { kPending = 0, kAtNode = 1, kOnEdge = 2, kQueued = 3, kAr
 
 struct DevGraph {
   int32_t n, m;
+  int32_t ell;              // ELL row width (4 or 8; slot = x*ell + i) or 0 for plain CSR
+  int32_t M;                // slot-space size (n*ell for ELL, m for CSR); padding slots have slot_edge = -1
   const int2* row;          // [n] {first slot, out-degree}
+  const int32_t* key;       // [M] colony fast path: packed grid (row<<16|col) of the neighbour, or
+                            //     the neighbour id for table distances; -1 on padding
   const int32_t* col;       // [m] neighbour (edge.to) per slot
   const int64_t* len;       // [m] length_mm per slot
   const int32_t* bind;      // [m] signal*8+phase of the queue the edge feeds, -1 if none
@@ -61,6 +65,7 @@ struct DevParams {
   // colony
   int32_t ants, hop_limit, max_hops, rng, congestion, deposit, cong_evap, replan_all;
   int32_t plan_cap, path_cap;
+  int32_t scratch_mode;     // 1: every ant's tour kept in scratch, the plan is the winner's row
   int32_t need_positions;  // MACO network-wide fold
   int32_t record_paths;
 };
@@ -96,7 +101,9 @@ struct DevVehicles {
   int32_t* dflag;     // decided this step (MACO positions)
   int32_t* pos;       // exclusive prefix of dflag = decision position
   int32_t *path, *path_n;       // realized path (slots), [V * path_cap]
-  int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap]
+  int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
+  int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)
+  int32_t* plan_ant;            // winning ant per vehicle (scratch mode)
   int64_t* plan_step;
   uint8_t* plan_done;
 };

@@ -261,6 +261,8 @@ struct gmaco_engine {
   HostGraph g;
   gmaco_sim_config cfg{};
   int32_t S = 0;
+  int32_t ell = 0, M = 0;            // slot space (ELL width, size)
+  std::vector<int32_t> slot_edge;    // slot -> edge id (-1 padding)
   std::vector<int32_t> sig_node;
   DevBuffers buf;
   DevWorld w{};
@@ -271,6 +273,9 @@ struct gmaco_engine {
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph_big = nullptr, graph_one = nullptr;
   cudaGraphExec_t tgraph_big = nullptr, tgraph_one = nullptr;
+  cudaGraphExec_t graph_walk = nullptr, graph_tail = nullptr;  // bench split
+  void* flush = nullptr;
+  int64_t flush_bytes = 0;
   std::vector<cudaEvent_t> ev_begin, ev_end;  // timing mode, kGraphSteps pairs
   bool timing = false;
   double last_walk_ms = 0.0, last_step_ms = 0.0;
@@ -280,8 +285,9 @@ struct gmaco_engine {
 
   ~gmaco_engine() {
     if (device >= 0) cudaSetDevice(device);
-    for (auto ge : {graph_big, graph_one, tgraph_big, tgraph_one})
+    for (auto ge : {graph_big, graph_one, tgraph_big, tgraph_one, graph_walk, graph_tail})
       if (ge) cudaGraphExecDestroy(ge);
+    if (flush) cudaFree(flush);
     for (auto e : ev_begin) cudaEventDestroy(e);
     for (auto e : ev_end) cudaEventDestroy(e);
     if (ev_a) cudaEventDestroy(ev_a);
@@ -540,17 +546,35 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   Spawned sp = spawn(c, g, dh, targets);
   const int32_t V = c.vehicle_count;
 
-  // ---- graph in slot order ---------------------------------------------------
+  // ---- graph in slot order: ELL rows of width 4/8 when the out-degree allows
+  // (one aligned vector load per row), plain CSR otherwise ------------------
+  int32_t maxdeg = 0;
+  for (int32_t u = 0; u < n; ++u) maxdeg = std::max(maxdeg, g.out_ptr[u + 1] - g.out_ptr[u]);
+  const int32_t ell = maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 0);
+  const int32_t M = ell ? n * ell : m;
+  h->ell = ell;
+  h->M = M;
+  h->slot_edge.assign(M, -1);
   std::vector<int2> row(n);
-  for (int32_t u = 0; u < n; ++u) row[u] = make_int2(g.out_ptr[u], g.out_ptr[u + 1] - g.out_ptr[u]);
-  std::vector<int32_t> col(m), slot_from(m), bind(m, -1);
-  std::vector<int64_t> slen(m);
-  std::vector<double> eta(m);
-  for (int32_t s = 0; s < m; ++s) {
-    const int32_t e = g.out_edge[s];
+  for (int32_t u = 0; u < n; ++u) {
+    const int32_t first = ell ? u * ell : g.out_ptr[u];
+    row[u] = make_int2(first, g.out_ptr[u + 1] - g.out_ptr[u]);
+    for (int32_t i = 0; i < row[u].y; ++i) h->slot_edge[first + i] = g.out_edge[g.out_ptr[u] + i];
+  }
+  for (int32_t s = 0; s < M; ++s)
+    if (h->slot_edge[s] >= 0) g.edge_slot[h->slot_edge[s]] = s;
+  if (dd->kind == GMACO_DIST_GRID && (dd->grid_rows >= 32768 || dd->grid_cols >= 32768))
+    throw ValidationError("grid distance: rows and cols must be < 32768");
+  std::vector<int32_t> col(M, -1), slot_from(M, -1), bind(M, -1), key(M, -1);
+  std::vector<int64_t> slen(M, 0);
+  std::vector<double> eta(M, 0.0);
+  for (int32_t s = 0; s < M; ++s) {
+    const int32_t e = h->slot_edge[s];
+    if (e < 0) continue;
     col[s] = g.to[e];
     slot_from[s] = g.from[e];
     slen[s] = g.len[e];
+    key[s] = dd->kind == GMACO_DIST_GRID ? ((g.to[e] / dd->grid_cols) << 16) | (g.to[e] % dd->grid_cols) : g.to[e];
     const double vis = 1.0 / (static_cast<double>(g.len[e]) / 1000.0);  // routing.cpp:92
     eta[s] = std::pow(vis, c.routing.aco_beta);
   }
@@ -575,11 +599,14 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   }
   w.g.n = n;
   w.g.m = m;
+  w.g.ell = ell;
+  w.g.M = M;
   w.g.row = B.upload(row);
+  w.g.key = B.upload(key);
   w.g.col = B.upload(col);
   w.g.len = B.upload(slen);
   w.g.bind = B.upload(bind);
-  w.g.slot_edge = B.upload(g.out_edge);
+  w.g.slot_edge = B.upload(h->slot_edge);
   w.g.slot_from = B.upload(slot_from);
   w.g.eta_beta = B.upload(eta);
 
@@ -630,9 +657,17 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   if (need_paths && path_bytes > (size_t(16) << 30))
     throw ValidationError("config: realized-path storage exceeds 16 GiB (lower max_steps)");
   if (!p.record_paths) p.path_cap = 1;
-  p.plan_cap = alg == GMACO_COLONY ? p.max_hops : 1;
+  // Tour storage.  With the progress filter every hop strictly decreases the
+  // exact distance, so on a uniform grid a walk has at most rows+cols-2 hops;
+  // elsewhere the cap is max_hops.
+  int32_t walk_bound = p.max_hops;
+  if (dd->kind == GMACO_DIST_GRID && p.progress_filter)
+    walk_bound = std::min<int32_t>(walk_bound, dd->grid_rows + dd->grid_cols - 2);
+  p.plan_cap = alg == GMACO_COLONY ? std::max(walk_bound, 1) : 1;
   if (alg == GMACO_COLONY && (size_t)V * p.plan_cap * 4 > (size_t(32) << 30))
     throw ValidationError("colony: planned-tour storage exceeds 32 GiB (set colony.max_hops)");
+  // scratch mode keeps every ant's tour (no winner replay) when it fits 2 GiB
+  p.scratch_mode = alg == GMACO_COLONY && (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(2) << 30);
   if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound
     int64_t maxlen = 0;
     for (int64_t L : g.len) maxlen = std::max(maxlen, L);
@@ -642,12 +677,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   }
 
   // ---- pheromone init (init_random, pheromone.cpp:21-32) + first weights ----
-  std::vector<int64_t> tau(m);
-  std::vector<double> wt(m);
-  std::vector<int64_t> ecost(m);
+  std::vector<int64_t> tau(M, 0);
+  std::vector<double> wt(M, 0.0);
+  std::vector<int64_t> ecost(M, 0);
   const int64_t lo = p.tau_lo, hi = p.tau_hi;
-  for (int32_t s = 0; s < m; ++s) {
-    const int32_t e = g.out_edge[s];
+  for (int32_t s = 0; s < M; ++s) {
+    const int32_t e = h->slot_edge[s];
+    if (e < 0) continue;
     const double v = uniform(draw(c.seed, 1, (uint64_t)e), c.pheromone.tau_init_lo, c.pheromone.tau_init_hi);
     tau[s] = std::clamp(tau_from_double(v), lo, hi);
     const double tau_d = static_cast<double>(tau[s]) / 1e6;
@@ -658,10 +694,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.tau = B.upload(tau);
   w.weight = B.upload(wt);
   w.ecost = B.upload(ecost);
-  w.occ_cur = B.filled<int32_t>(m, 0);
-  w.occ_new = B.filled<int32_t>(m, 0);
-  w.dep = B.filled<int64_t>(m, 0);
-  w.dec_head = B.filled<int32_t>(std::max(m, n), -1);
+  w.occ_cur = B.filled<int32_t>(M, 0);
+  w.occ_new = B.filled<int32_t>(M, 0);
+  w.dep = B.filled<int64_t>(M, 0);
+  w.dec_head = B.filled<int32_t>(std::max(M, n), -1);
 
   // ---- signals -----------------------------------------------------------
   DevSignals& ds = w.s;
@@ -707,7 +743,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.pos = B.filled<int32_t>(V, 0);
   dv.path = B.alloc<int32_t>((size_t)V * p.path_cap);
   dv.path_n = B.filled<int32_t>(V, 0);
-  dv.plan = B.alloc<int32_t>((size_t)V * p.plan_cap);
+  dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
+  dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
+  dv.plan_ant = B.filled<int32_t>(V, 0);
   dv.plan_n = B.filled<int32_t>(V, 0);
   dv.plan_step = B.filled<int64_t>(V, -1);
   dv.plan_done = B.filled<uint8_t>(V, 0);
@@ -733,6 +771,23 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   CK(cudaEventCreate(&h->ev_a));
   CK(cudaEventCreate(&h->ev_b));
   CK(cudaDeviceSynchronize());
+}
+
+// part 1 = stage-B walk kernel only, part 2 = the rest of the step (C..G)
+cudaGraphExec_t capture_part(gmaco_engine* h, int part) {
+  StepResources r = h->res;
+  r.capturing = true;
+  r.part = part;
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = launch_step(h->w, r, h->stream, nullptr, nullptr);
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+  CK(err);
+  CK(e2);
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  return exec;
 }
 
 cudaGraphExec_t capture(gmaco_engine* h, int steps, bool timing) {
@@ -856,7 +911,8 @@ void collect(gmaco_engine* h, gmaco_run_result* r, double* travel, int32_t* rvid
 
 template <class T>
 void scatter_slots(const gmaco_engine* h, const std::vector<T>& by_slot, T* by_edge) {
-  for (int32_t s = 0; s < h->g.m; ++s) by_edge[h->g.out_edge[s]] = by_slot[s];
+  for (int32_t s = 0; s < h->M; ++s)
+    if (h->slot_edge[s] >= 0) by_edge[h->slot_edge[s]] = by_slot[s];
 }
 
 }  // namespace
@@ -929,18 +985,19 @@ int gmaco_collect(gmaco_engine* h, gmaco_run_result* result, double* travel_time
 
 int gmaco_get_pheromone(gmaco_engine* h, int64_t* tau) {
   if (!h || !tau) return GMACO_EVALIDATION;
-  return guarded(h, [&] { scatter_slots(h, download(h->w.tau, h->g.m), tau); });
+  return guarded(h, [&] { scatter_slots(h, download(h->w.tau, h->M), tau); });
 }
 
 int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
   if (!h || !tau) return GMACO_EVALIDATION;
   return guarded(h, [&] {
-    const int32_t m = h->g.m;
-    std::vector<int64_t> t(m);
-    std::vector<double> wt(m);
+    const int32_t m = h->M;
+    std::vector<int64_t> t(m, 0);
+    std::vector<double> wt(m, 0.0);
     auto eta = download(h->w.g.eta_beta, m);
     for (int32_t s = 0; s < m; ++s) {
-      t[s] = tau[h->g.out_edge[s]];
+      if (h->slot_edge[s] < 0) continue;
+      t[s] = tau[h->slot_edge[s]];
       const double tau_d = static_cast<double>(t[s]) / 1e6;
       wt[s] = (h->w.p.alpha == 1.0 ? tau_d : std::pow(tau_d, h->w.p.alpha)) * eta[s];
     }
@@ -951,7 +1008,7 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
 
 int gmaco_get_occupancy(gmaco_engine* h, int32_t* occ) {
   if (!h || !occ) return GMACO_EVALIDATION;
-  return guarded(h, [&] { scatter_slots(h, download(h->w.occ_cur, h->g.m), occ); });
+  return guarded(h, [&] { scatter_slots(h, download(h->w.occ_cur, h->M), occ); });
 }
 
 int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
@@ -982,7 +1039,7 @@ int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
     cp(v->path_length_mm, d.path_len_mm);
     if (v->on_edge) {
       auto oe = download(d.on_edge, V);
-      for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->g.out_edge[oe[i]];
+      for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
     }
     if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
       for (size_t i = 0; i < V; ++i)
@@ -1060,20 +1117,26 @@ int gmaco_route_query(gmaco_engine* h, int32_t vid, int32_t planned, int32_t* ou
     if (planned) {
       if (w.p.algorithm != GMACO_COLONY) throw ValidationError("route_query: planned routes need the colony algorithm");
       CK(cudaMemcpy(&n, w.v.plan_n + vid, 4, cudaMemcpyDeviceToHost));
-      base = w.v.plan;
       pcap = w.p.plan_cap;
+      if (w.p.scratch_mode) {  // the winner's row of the per-ant tour scratch
+        int32_t ant = 0;
+        CK(cudaMemcpy(&ant, w.v.plan_ant + vid, 4, cudaMemcpyDeviceToHost));
+        base = w.v.scratch + ((size_t)vid * w.p.ants + ant) * pcap;
+      } else {
+        base = w.v.plan + (size_t)vid * pcap;
+      }
     } else {
       if (!w.p.record_paths) throw ValidationError("route_query: realized paths are not recorded for this config");
       CK(cudaMemcpy(&n, w.v.path_n + vid, 4, cudaMemcpyDeviceToHost));
-      base = w.v.path;
       pcap = w.p.path_cap;
+      base = w.v.path + (size_t)vid * pcap;
     }
     *out_len = n;
     const int32_t k = std::min(n, cap);
     if (k > 0 && out_edges) {
       std::vector<int32_t> s(k);
-      CK(cudaMemcpy(s.data(), base + (size_t)vid * pcap, k * 4, cudaMemcpyDeviceToHost));
-      for (int32_t i = 0; i < k; ++i) out_edges[i] = h->g.out_edge[s[i]];
+      CK(cudaMemcpy(s.data(), base, k * 4, cudaMemcpyDeviceToHost));
+      for (int32_t i = 0; i < k; ++i) out_edges[i] = h->slot_edge[s[i]];
     }
   });
 }
@@ -1108,6 +1171,42 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
     CK(cudaMemcpy(out_next, on, count * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_via, ov, count * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_deviated, odv, count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms) {
+  if (!h || steps < 0) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    refresh_ctl(h);
+    *h->stop_host = h->ctl_host->step + steps;
+    CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    if (!h->graph_walk) h->graph_walk = capture_part(h, 1);
+    if (!h->graph_tail) h->graph_tail = capture_part(h, 2);
+    if (flush_bytes > 0 && h->flush_bytes < flush_bytes) {
+      if (h->flush) cudaFree(h->flush);
+      CK(cudaMalloc(&h->flush, flush_bytes));
+      h->flush_bytes = flush_bytes;
+    }
+    std::vector<cudaEvent_t> ev(3 * (size_t)steps);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int32_t i = 0; i < steps; ++i) {
+      if (flush_bytes > 0) CK(cudaMemsetAsync(h->flush, i & 0xff, flush_bytes, h->stream));
+      CK(cudaEventRecord(ev[3 * i], h->stream));
+      CK(cudaGraphLaunch(h->graph_walk, h->stream));
+      CK(cudaEventRecord(ev[3 * i + 1], h->stream));
+      CK(cudaGraphLaunch(h->graph_tail, h->stream));
+      CK(cudaEventRecord(ev[3 * i + 2], h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    for (int32_t i = 0; i < steps; ++i) {
+      float a = 0.f, b = 0.f;
+      CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+      CK(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 2]));
+      if (walk_ms) walk_ms[i] = a;
+      if (step_ms) step_ms[i] = b;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    refresh_ctl(h);
   });
 }
 

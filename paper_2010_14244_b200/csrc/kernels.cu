@@ -42,18 +42,21 @@ __device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t a, uint64_t b, 
 __device__ __forceinline__ double to_unit(uint64_t bits) {
   return __dmul_rn((double)(bits >> 11), 0x1.0p-53);
 }
-__device__ __forceinline__ uint64_t philox_bits(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                                uint32_t k0, uint32_t k1) {
+// Philox4x32-10 (Salmon et al., SC'11).  One call serves two hops: the
+// counter is (step, vehicle, ant, hop/2) and hop&1 selects the 64-bit half.
+__device__ __forceinline__ uint4 philox4(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  return ((uint64_t)c0 << 32) | c1;
+  return c;
+}
+__device__ __forceinline__ uint64_t philox_half(uint4 o, int32_t hop) {
+  return (hop & 1) ? (((uint64_t)o.z << 32) | o.w) : (((uint64_t)o.x << 32) | o.y);
 }
 // Ant uniform: REFERENCE keying reduces to RngKey{seed, vid, step} of the
 // reference ACO decision at ant 0 hop 0 (routing.cpp:97-98).
@@ -64,8 +67,9 @@ __device__ __forceinline__ double ant_uniform(int rng, uint64_t seed, int64_t st
     const uint64_t b = (uint64_t)step | ((uint64_t)(uint32_t)hop << 40);
     return to_unit(draw(seed, 5, a, b));
   }
-  return to_unit(philox_bits((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hop,
-                             (uint32_t)seed, (uint32_t)(seed >> 32)));
+  const uint4 o = philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hop >> 1),
+                          (uint32_t)seed, (uint32_t)(seed >> 32));
+  return to_unit(philox_half(o, hop));
 }
 
 // ---------------------------------------------------------------------------
@@ -388,6 +392,25 @@ __device__ __forceinline__ WalkOut ant_walk(const DevWorld& w, const Target<DK>&
   return o;
 }
 
+// Winner epilogue: plan bookkeeping, best-tour deposit (exact int64 sums,
+// deposit_amount pheromone.cpp:73-78) and, at a node, the first hop.
+__device__ __forceinline__ void finish_colony(const DevWorld& w, int32_t vid, int32_t start,
+                                              const int32_t* tour, int32_t hops, bool deciding, int64_t step) {
+  const DevVehicles& v = w.v;
+  v.plan_n[vid] = hops;
+  v.plan_step[vid] = step;
+  const bool done = hops > 0 && w.g.col[tour[hops - 1]] == v.dest[vid];
+  v.plan_done[vid] = done;
+  if (done && w.p.deposit == 1) {
+    int64_t len = 0;
+    for (int i = 0; i < hops; ++i) len += w.g.len[tour[i]];
+    const double km = __ddiv_rn((double)len, 1e6);
+    const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+    for (int i = 0; i < hops; ++i) atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+  }
+  if (deciding) take_edge(w, vid, tour[0], false, start);
+}
+
 template <int DK, bool kFilter>
 __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
   if (skip_step(w.ctl)) return;
@@ -438,7 +461,10 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
     start = start_s[lv];
     if (start >= 0) {
       const Target<DK> t(w.d, v.dest[vid]);
-      o = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, nullptr);
+      int32_t* tour = w.p.scratch_mode
+                          ? v.scratch + ((size_t)vid * w.p.ants + ant) * (size_t)w.p.plan_cap
+                          : nullptr;
+      o = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, tour);
       steps = o.steps;
       cands = o.cands;
       degs = o.degs;
@@ -455,26 +481,244 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
       v.plan_done[vid] = 0;
       if (deciding) v.state[vid] = kRetired;
     } else {
-      const Target<DK> t(w.d, v.dest[vid]);
-      int32_t* tour = v.plan + (size_t)vid * w.p.plan_cap;
-      const WalkOut r = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, tour);
-      v.plan_n[vid] = r.hops;
-      v.plan_step[vid] = step;
-      const bool done = r.hops > 0 && w.g.col[tour[r.hops - 1]] == t.dest;
-      v.plan_done[vid] = done;
+      int32_t* tour;
+      int32_t hops;
+      if (w.p.scratch_mode) {
+        tour = v.scratch + ((size_t)vid * w.p.ants + ant) * (size_t)w.p.plan_cap;
+        hops = o.hops;
+        v.plan_ant[vid] = ant;
+      } else {
+        const Target<DK> t(w.d, v.dest[vid]);
+        tour = v.plan + (size_t)vid * w.p.plan_cap;
+        hops = ant_walk<DK, kFilter>(w, t, vid, ant, start, step, tour).hops;
+      }
+      finish_colony(w, vid, start, tour, hops, deciding, step);
       routes = 1;
-      if (done && w.p.deposit == 1) {  // best-tour deposit (exact int64 sums)
-        int64_t len = 0;
-        for (int i = 0; i < r.hops; ++i) len += w.g.len[tour[i]];
-        const double km = __ddiv_rn((double)len, 1e6);  // deposit_amount, pheromone.cpp:73-78
-        const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
-        for (int i = 0; i < r.hops; ++i)
-          atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+      decided = deciding;
+    }
+  }
+  steps = block_sum(steps, red);
+  cands = block_sum(cands, red);
+  degs = block_sum(degs, red);
+  routes = block_sum(routes, red);
+  decided = block_sum(decided, red);
+  if (threadIdx.x == 0) {
+    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
+    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
+    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
+    if (routes) atomicAdd((unsigned long long*)&w.ctl->vehicle_routes, (unsigned long long)routes);
+    if (decided) {
+      atomicAdd((unsigned long long*)&w.ctl->decisions, (unsigned long long)decided);
+      atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)decided);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B (colony) fast path: ELL-4 rows (out-degree <= 4), progress filter on.
+// One thread per ant.  Per hop the thread issues ONE round of independent
+// row loads — 4 neighbour keys (16 B), 4 roulette weights (32 B), 4 tour
+// costs (32 B) — then decides in registers: candidate mask, sequential
+// left-to-right roulette (routing.cpp:88-113), Philox draw shared by two
+// hops.  Grid distances come from packed (row<<16|col) keys, so the filter
+// needs no division and no distance table.  Same semantics as k_colony.
+// ---------------------------------------------------------------------------
+template <int DK>
+__global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  constexpr int kMaxVpb = 256;
+  __shared__ unsigned long long best[kMaxVpb];
+  __shared__ int32_t start_s[kMaxVpb];
+  __shared__ uint8_t deciding_s[kMaxVpb];
+  __shared__ long long red[32];
+  const int K = w.p.ants;
+  const int vpb = blockDim.x / K;
+  const int lv = threadIdx.x / K;
+  const int ant = threadIdx.x - lv * K;
+  const int32_t vid = blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.V;
+  const int64_t step = w.ctl->step;
+  const DevVehicles& v = w.v;
+
+  if (live && ant == 0) {
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    int32_t start = -1;
+    const bool deciding = st == kAtNode;
+    if (deciding)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kQueued)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kOnEdge)
+      start = w.g.col[v.on_edge[vid]];
+    if (start >= 0 && start == v.dest[vid]) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      start = -1;
+    }
+    start_s[lv] = start;
+    deciding_s[lv] = deciding;
+    best[lv] = ~0ull;
+  }
+  __syncthreads();
+  long long steps = 0, cands = 0, degs = 0, routes = 0, decided = 0;
+  int32_t start = -1, hops = 0;
+  int64_t cost = 0;
+  bool first_ok = false;
+  int32_t* tour = nullptr;
+  if (live) start = start_s[lv];
+  if (live && start >= 0) {
+    const int32_t dest = v.dest[vid];
+    const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit;
+    const uint32_t k0 = (uint32_t)w.p.seed, k1 = (uint32_t)(w.p.seed >> 32);
+    const int rng = w.p.rng;
+    const int4* __restrict__ keys = reinterpret_cast<const int4*>(w.g.key);
+    const double2* __restrict__ W2 = reinterpret_cast<const double2*>(w.weight);
+    const longlong2* __restrict__ C2 = reinterpret_cast<const longlong2*>(w.ecost);
+    if (w.p.scratch_mode) tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+    // destination / current position
+    int32_t cols = 0, rd = 0, cd = 0, rx = 0, cx = 0;
+    const int64_t* __restrict__ trow = nullptr;
+    if (DK == 1) {
+      cols = w.d.cols;
+      rd = dest / cols;
+      cd = dest - rd * cols;
+      rx = start / cols;
+      cx = start - rx * cols;
+    } else {
+      const int32_t slot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+      trow = slot < 0 ? nullptr : w.d.table + (size_t)slot * w.d.n;
+    }
+    int32_t x = start;
+    uint4 rnd = make_uint4(0, 0, 0, 0);
+    while (x != dest && (hop_limit == 0 || hops < hop_limit)) {
+      if (hops >= max_hops) {
+        cost = kInf;
+        break;
       }
-      if (deciding) {
-        take_edge(w, vid, tour[0], false, start);
-        decided = 1;
+      const int4 kk = keys[x];
+      const double2 wa = W2[2 * x], wb = W2[2 * x + 1];
+      const longlong2 ca = C2[2 * x], cb = C2[2 * x + 1];
+      const int32_t kv[4] = {kk.x, kk.y, kk.z, kk.w};
+      uint32_t reach = 0, closer = 0;
+      int deg = 0;
+      if (DK == 1) {
+        const int32_t dx = abs(rx - rd) + abs(cx - cd);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (kv[i] < 0) continue;
+          ++deg;
+          reach |= 1u << i;
+          const int32_t dn = abs((kv[i] >> 16) - rd) + abs((kv[i] & 0xffff) - cd);
+          if (dn < dx) closer |= 1u << i;
+        }
+      } else {
+        if (trow) {
+          const int64_t dx = __ldg(trow + x);
+          int64_t dn[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dn[i] = kv[i] >= 0 ? __ldg(trow + kv[i]) : kInf;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (kv[i] < 0) continue;
+            ++deg;
+            if (dn[i] == kInf) continue;
+            reach |= 1u << i;
+            if (dn[i] < dx) closer |= 1u << i;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) deg += kv[i] >= 0;
+        }
       }
+      degs += deg;
+      const uint32_t cand = closer ? closer : reach;
+      if (!cand) {
+        cost = kInf;
+        break;
+      }
+      if (hops == 0) first_ok = true;
+      cands += __popc(cand);
+      double u;
+      if (rng == 1) {
+        u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                         (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
+      } else {
+        if ((hops & 1) == 0)
+          rnd = philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hops >> 1), k0, k1);
+        u = to_unit(philox_half(rnd, hops));
+      }
+      const double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+      double total = 0.0;
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (cand & (1u << i)) {
+          total = __dadd_rn(total, wv[i]);
+          ++c;
+        }
+      int pick = 31 - __clz(cand);  // default: last candidate
+      if (total <= 0.0 || !isfinite(total)) {
+        int p = (int)__dmul_rn(u, (double)c);
+        p = p < c - 1 ? p : c - 1;
+        uint32_t m = cand;
+        for (int j = 0; j < p; ++j) m &= m - 1;
+        pick = __ffs(m) - 1;
+      } else {
+        const double point = __dmul_rn(u, total);
+        double cum = 0.0;
+        bool found = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (!found && (cand & (1u << i))) {
+            cum = __dadd_rn(cum, wv[i]);
+            if (point < cum) {
+              pick = i;
+              found = true;
+            }
+          }
+      }
+      const int64_t cv[4] = {ca.x, ca.y, cb.x, cb.y};
+      cost += cv[pick];
+      if (tour) tour[hops] = 4 * x + pick;
+      const int32_t nk = kv[pick];
+      if (DK == 1) {
+        rx = nk >> 16;
+        cx = nk & 0xffff;
+        x = rx * cols + cx;
+      } else {
+        x = nk;
+      }
+      ++hops;
+      ++steps;
+    }
+    const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
+    atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
+  }
+  __syncthreads();
+  if (live && start >= 0 && ant == (int)(best[lv] & 1023u)) {
+    const bool deciding = deciding_s[lv];
+    if (!first_ok) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      if (deciding) v.state[vid] = kRetired;
+    } else {
+      if (w.p.scratch_mode) {
+        v.plan_ant[vid] = ant;
+      } else {  // replay the winner with the generic walker to materialize its tour
+        tour = v.plan + (size_t)vid * w.p.plan_cap;
+        const Target<DK> t(w.d, v.dest[vid]);
+        hops = ant_walk<DK, true>(w, t, vid, ant, start, step, tour).hops;
+      }
+      finish_colony(w, vid, start, tour, hops, deciding, step);
+      routes = 1;
+      decided = deciding;
     }
   }
   steps = block_sum(steps, red);
@@ -746,7 +990,7 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const DevParams& p = w.p;
   int32_t occ = 0;
-  if (s < w.g.m) {
+  if (s < w.g.M && w.g.slot_edge[s] >= 0) {
     int64_t t = w.tau[s];
     const int alg = p.algorithm;
     if ((alg == 2 || alg == 3) && !p.siblings_only) {
@@ -907,7 +1151,14 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
                         cudaEvent_t walk_begin, cudaEvent_t walk_end) {
   const int V = w.p.V, S = w.p.S, m = w.g.m, n = w.g.n;
   if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
-  if (w.p.algorithm == 4) {
+  if (r.part == 2) goto tail;
+  if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
+    const int threads = 256, vpb = 256 / w.p.ants;
+    if (w.d.kind == 1)
+      k_colony_ell4<1><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+    else
+      k_colony_ell4<0><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+  } else if (w.p.algorithm == 4) {
     int threads, vpb;
     colony_shape(w.p.ants, &threads, &vpb);
     const unsigned grid = blocks_for(V, vpb);
@@ -929,6 +1180,8 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       k_decide<0><<<blocks_for(V, 256), 256, 0, st>>>(w);
   }
   if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
+  if (r.part == 1) return cudaGetLastError();
+tail:
   if (S > 0) k_signals<<<blocks_for(S, 256), 256, 0, st>>>(w);
   k_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
   if (S > 0) k_e3<<<blocks_for(S, 256), 256, 0, st>>>(w);
@@ -941,7 +1194,7 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       if (e != cudaSuccess) return e;
     }
   }
-  k_edges<<<blocks_for(m, 256), 256, 0, st>>>(w);
+  k_edges<<<blocks_for(w.g.M, 256), 256, 0, st>>>(w);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@ struct StepResources {
   void* scan_temp = nullptr;
   size_t scan_temp_bytes = 0;
   bool capturing = false;
+  int part = 0;  // 0 whole step, 1 stage-B walk only, 2 stages C..G only
 };
 
 // Enqueues one engine step (stages B..G) on `st`.  Optional events bracket

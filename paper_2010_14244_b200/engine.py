@@ -44,6 +44,7 @@ SIGNATURES = {
                         P(u8)),
     "gmaco_last_timing": (C.c_int, C.c_void_p, P(f64), P(f64), P(i64)),
     "gmaco_set_timing": (C.c_int, C.c_void_p, i32),
+    "gmaco_bench_steps": (C.c_int, C.c_void_p, i32, i64, P(f64), P(f64)),
     "gmaco_last_error": (C.c_char_p, C.c_void_p),
     "gmaco_destroy": (None, C.c_void_p),
 }
@@ -195,6 +196,14 @@ class Engine:
     # -- timing -----------------------------------------------------------------
     def set_timing(self, on: bool):
         self._check(self.L.gmaco_set_timing(self.h, int(on)))
+
+    def bench_steps(self, steps: int, flush_bytes: int):
+        """Per-step device times (walk kernel, whole step) in ms of `steps`
+        back-to-back steps with an L2 flush between them (outside the events)."""
+        walk = np.zeros(steps, dtype=np.float64)
+        step = np.zeros(steps, dtype=np.float64)
+        self._check(self.L.gmaco_bench_steps(self.h, steps, flush_bytes, abi.ptr(walk, f64), abi.ptr(step, f64)))
+        return walk, step
 
     def last_timing(self):
         a, b, n = f64(), f64(), i64()

@@ -220,3 +220,67 @@ def test_realized_paths():
     cpu.run()
     for vid in range(100):
         assert np.array_equal(gpu.route(vid), cpu.route(vid)), vid
+
+
+def test_colony_bench_workload_c2():
+    """The bench workload itself (C2: 32x32 all-signalized, 1000 vehicles,
+    64 ants, preemptive): a few iterations bit-exact against the oracle."""
+    import bench
+    net = networks.grid(32, 32, signals="all")
+    cfg = bench.workload_config(1, 400)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for k in (1, 2, 3):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, "bench workload")
+    for vid in range(0, 1000, 37):
+        assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    assert (a.ant_steps, a.candidates, a.degree_sum) == (b.ant_steps, b.candidates, b.degree_sum)
+
+
+@pytest.mark.parametrize("dist_kind", ["dense", "grid"])
+def test_colony_ell4_table_and_grid(dist_kind):
+    """Fast ELL-4 walk with dense-table distances (DK=0) and closed form (DK=1)."""
+    net = networks.grid(10, 11, signals="all")
+    cfg = abi.colony_production(_cfg("colony", 200, 13, max_steps=80, controller=abi.PREEMPTIVE), ants=32)
+    dist = net.grid_distance() if dist_kind == "grid" else abi.DistanceDesc(kind=abi.DIST_DENSE)
+    gpu = Engine(net, cfg, dist)
+    cpu = O.PortWorld(net, cfg, dist)
+    for k in (1, 3, 9):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, dist_kind)
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_colony_city_generic_path():
+    """Irregular graph (ELL-8 rows, generic walk kernel, dense distances)."""
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    net = O.ref_city(52, 64)
+    cfg = abi.colony_production(_cfg("colony", 200, 3, max_steps=120), ants=24)
+    gpu = Engine(net, cfg)
+    cpu = O.PortWorld(net, cfg)
+    for k in (1, 5, 20):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, "city colony")
+        for vid in range(200):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_colony_replay_mode_large_ants():
+    """ants=512 on a 24x24 grid exceeds nothing but exercises the generic
+    kernel (ants > 256) with scratch tours."""
+    net = networks.grid(24, 24)
+    cfg = abi.colony_production(_cfg("colony", 40, 21, max_steps=30), ants=512)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    gpu.step(4)
+    cpu.step(4)
+    _same_snapshot(gpu, cpu, "ants=512")
+    for vid in range(40):
+        assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
