@@ -67,6 +67,7 @@ struct DevParams {
   int32_t plan_cap, path_cap;
   int32_t scratch_mode;     // 1: every ant's tour kept in scratch, the plan is the winner's row
   int32_t need_positions;  // MACO network-wide fold
+  int32_t prefetch;        // bulk-prefetch the step's state into L2 at the start of stage B
   int32_t record_paths;
 };
 

@@ -647,6 +647,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.cong_evap = alg == GMACO_COLONY ? k.congestion_evaporation : 0;
   p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
+  p.prefetch = 1;
   // realized-path storage: needed for completion deposits; paths are bounded by
   // the decision count (<= max_steps) and, with the progress filter, by n-1.
   p.path_cap = (int32_t)std::max<int64_t>(

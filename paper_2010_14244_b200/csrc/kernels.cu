@@ -231,6 +231,88 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
   return r;  // valid in thread 0
 }
 
+// Bulk L2 prefetch (TMA engine, cp.async.bulk.prefetch.L2) of every array
+// the rest of the step touches, issued by one block at the start of the walk
+// so stages C..G find their state in L2.  Fire-and-forget: no completion wait.
+__device__ __forceinline__ void bulk_prefetch(const void* p, size_t bytes, int lane, int lanes) {
+  const char* c = static_cast<const char*>(p);
+  const size_t n = bytes & ~size_t(15);
+  constexpr size_t kChunk = 1 << 16;
+  for (size_t off = (size_t)lane * kChunk; off < n; off += (size_t)lanes * kChunk) {
+    const uint32_t sz = (uint32_t)min(n - off, kChunk);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c + off), "r"(sz) : "memory");
+  }
+}
+
+__device__ void prefetch_tail_state(const DevWorld& w) {
+  const size_t V = w.p.V, Q = (size_t)w.p.S * kPhases, S = w.p.S, M = w.g.M;
+  const int lane = threadIdx.x, lanes = blockDim.x;
+  const DevVehicles& v = w.v;
+  const DevSignals& g = w.s;
+  bulk_prefetch(v.state, V, lane, lanes);
+  bulk_prefetch(v.on_edge, 4 * V, lane, lanes);
+  bulk_prefetch(v.at_node, 4 * V, lane, lanes);
+  bulk_prefetch(v.dest, 4 * V, lane, lanes);
+  bulk_prefetch(v.progress, 8 * V, lane, lanes);
+  bulk_prefetch(v.advance, 8 * V, lane, lanes);
+  bulk_prefetch(v.latency_debt, 8 * V, lane, lanes);
+  bulk_prefetch(v.driving, 8 * V, lane, lanes);
+  bulk_prefetch(v.depart, 8 * V, lane, lanes);
+  bulk_prefetch(v.joined, 8 * V, lane, lanes);
+  bulk_prefetch(v.queued, 8 * V, lane, lanes);
+  bulk_prefetch(v.qnext, 4 * V, lane, lanes);
+  bulk_prefetch(g.qlen, 4 * Q, lane, lanes);
+  bulk_prefetch(g.qhead, 4 * Q, lane, lanes);
+  bulk_prefetch(g.qtail, 4 * Q, lane, lanes);
+  bulk_prefetch(g.arr_head, 4 * Q, lane, lanes);
+  bulk_prefetch(g.head_wait, 8 * Q, lane, lanes);
+  bulk_prefetch(g.rem, 8 * Q, lane, lanes);
+  bulk_prefetch(g.green, 4 * S, lane, lanes);
+  bulk_prefetch(g.cursor, 4 * S, lane, lanes);
+  bulk_prefetch(g.lanes, 4 * S, lane, lanes);
+  bulk_prefetch(g.node, 4 * S, lane, lanes);
+  bulk_prefetch(g.el_s, 8 * S, lane, lanes);
+  bulk_prefetch(g.el_steps, 8 * S, lane, lanes);
+  bulk_prefetch(w.tau, 8 * M, lane, lanes);
+  bulk_prefetch(w.occ_new, 4 * M, lane, lanes);
+  bulk_prefetch(w.dep, 8 * M, lane, lanes);
+  bulk_prefetch(w.g.slot_edge, 4 * M, lane, lanes);
+  bulk_prefetch(w.g.bind, 4 * M, lane, lanes);
+  bulk_prefetch(w.g.len, 8 * M, lane, lanes);
+  bulk_prefetch(w.g.eta_beta, 8 * M, lane, lanes);
+}
+
+// Five block-wide sums with a single barrier; valid in thread 0.
+struct Sum5 {
+  long long v[5];
+};
+__device__ __forceinline__ Sum5 block_sum5(Sum5 x, long long (*smem)[32]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    long long a = x.v[k];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0) smem[k][wid] = a;
+  }
+  __syncthreads();
+  Sum5 r{};
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 5; ++k)
+      for (int i = 0; i < (int)((blockDim.x + 31) >> 5); ++i) r.v[k] += smem[k][i];
+  return r;
+}
+
+__device__ __forceinline__ void flush_counters(DevCtl* c, const Sum5& t) {
+  if (t.v[0]) atomicAdd((unsigned long long*)&c->ant_steps, (unsigned long long)t.v[0]);
+  if (t.v[1]) atomicAdd((unsigned long long*)&c->candidates, (unsigned long long)t.v[1]);
+  if (t.v[2]) atomicAdd((unsigned long long*)&c->degree_sum, (unsigned long long)t.v[2]);
+  if (t.v[3]) atomicAdd((unsigned long long*)&c->vehicle_routes, (unsigned long long)t.v[3]);
+  if (t.v[4]) {
+    atomicAdd((unsigned long long*)&c->decisions, (unsigned long long)t.v[4]);
+    atomicAdd((unsigned long long*)&c->dcount, (unsigned long long)t.v[4]);
+  }
+}
+
 // Vehicle takes edge `slot` (engine.cpp:207-216).
 __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_t slot, bool deviated,
                                           int32_t from) {
@@ -264,6 +346,7 @@ __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_
 template <int DK>
 __global__ void __launch_bounds__(256) k_decide(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   __shared__ long long red[32];
   const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t step = w.ctl->step;
@@ -414,11 +497,12 @@ __device__ __forceinline__ void finish_colony(const DevWorld& w, int32_t vid, in
 template <int DK, bool kFilter>
 __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   constexpr int kMaxVpb = 256;
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
-  __shared__ long long red[32];
+  __shared__ long long red5[5][32];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
@@ -497,21 +581,8 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
       decided = deciding;
     }
   }
-  steps = block_sum(steps, red);
-  cands = block_sum(cands, red);
-  degs = block_sum(degs, red);
-  routes = block_sum(routes, red);
-  decided = block_sum(decided, red);
-  if (threadIdx.x == 0) {
-    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
-    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
-    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
-    if (routes) atomicAdd((unsigned long long*)&w.ctl->vehicle_routes, (unsigned long long)routes);
-    if (decided) {
-      atomicAdd((unsigned long long*)&w.ctl->decisions, (unsigned long long)decided);
-      atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)decided);
-    }
-  }
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -526,11 +597,12 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
 template <int DK>
 __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   constexpr int kMaxVpb = 256;
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
-  __shared__ long long red[32];
+  __shared__ long long red5[5][32];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
@@ -604,7 +676,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
       const int4 kk = keys[x];
       const double2 wa = W2[2 * x], wb = W2[2 * x + 1];
       const longlong2 ca = C2[2 * x], cb = C2[2 * x + 1];
-      const int32_t kv[4] = {kk.x, kk.y, kk.z, kk.w};
+      const int32_t kv[4] = {kk.x, kk.y, kk.z, kk.w};  // constant-indexed only (unrolled)
       uint32_t reach = 0, closer = 0;
       int deg = 0;
       if (DK == 1) {
@@ -653,40 +725,33 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
           rnd = philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hops >> 1), k0, k1);
         u = to_unit(philox_half(rnd, hops));
       }
-      const double wv[4] = {wa.x, wa.y, wb.x, wb.y};
-      double total = 0.0;
-      int c = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (cand & (1u << i)) {
-          total = __dadd_rn(total, wv[i]);
-          ++c;
-        }
+      // sequential left-to-right roulette over the candidates (register-only)
+      const double w0 = (cand & 1u) ? wa.x : 0.0, w1 = (cand & 2u) ? wa.y : 0.0;
+      const double w2 = (cand & 4u) ? wb.x : 0.0, w3 = (cand & 8u) ? wb.y : 0.0;
+      // adding an exact 0.0 for a non-candidate leaves every partial sum unchanged
+      const double s0 = w0, s1 = __dadd_rn(s0, w1), s2 = __dadd_rn(s1, w2), total = __dadd_rn(s2, w3);
+      const int c = __popc(cand);
       int pick = 31 - __clz(cand);  // default: last candidate
       if (total <= 0.0 || !isfinite(total)) {
         int p = (int)__dmul_rn(u, (double)c);
         p = p < c - 1 ? p : c - 1;
         uint32_t m = cand;
-        for (int j = 0; j < p; ++j) m &= m - 1;
+        if (p >= 1) m &= m - 1;
+        if (p >= 2) m &= m - 1;
+        if (p >= 3) m &= m - 1;
         pick = __ffs(m) - 1;
       } else {
         const double point = __dmul_rn(u, total);
-        double cum = 0.0;
-        bool found = false;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (!found && (cand & (1u << i))) {
-            cum = __dadd_rn(cum, wv[i]);
-            if (point < cum) {
-              pick = i;
-              found = true;
-            }
-          }
+        // first candidate i whose cumulative sum exceeds point
+        if ((cand & 8u) && point < total) pick = 3;
+        if ((cand & 4u) && point < s2) pick = 2;
+        if ((cand & 2u) && point < s1) pick = 1;
+        if ((cand & 1u) && point < s0) pick = 0;
       }
-      const int64_t cv[4] = {ca.x, ca.y, cb.x, cb.y};
-      cost += cv[pick];
+      const int64_t cpk = pick == 0 ? ca.x : pick == 1 ? ca.y : pick == 2 ? cb.x : cb.y;
+      cost += cpk;
       if (tour) tour[hops] = 4 * x + pick;
-      const int32_t nk = kv[pick];
+      const int32_t nk = pick == 0 ? kk.x : pick == 1 ? kk.y : pick == 2 ? kk.z : kk.w;
       if (DK == 1) {
         rx = nk >> 16;
         cx = nk & 0xffff;
@@ -721,21 +786,158 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
       decided = deciding;
     }
   }
-  steps = block_sum(steps, red);
-  cands = block_sum(cands, red);
-  degs = block_sum(degs, red);
-  routes = block_sum(routes, red);
-  decided = block_sum(decided, red);
-  if (threadIdx.x == 0) {
-    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
-    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
-    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
-    if (routes) atomicAdd((unsigned long long*)&w.ctl->vehicle_routes, (unsigned long long)routes);
-    if (decided) {
-      atomicAdd((unsigned long long*)&w.ctl->decisions, (unsigned long long)decided);
-      atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)decided);
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
+}
+
+// ---------------------------------------------------------------------------
+// B (colony) on a validated uniform lattice (GMACO_DIST_GRID, progress filter
+// on).  The distance service is closed-form and the lattice is checked at
+// create, so a node's candidate set needs no loads at all: the strictly
+// closer neighbours are the one horizontal and the one vertical move toward
+// the destination, and their ELL slots follow from the ascending-id row
+// order [up, left, right, down].  A hop is then 1-2 weight loads, a 2-way
+// sequential roulette and one tour-cost load — identical decisions to
+// k_colony / k_colony_ell4 (same candidate order, same arithmetic).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
+  constexpr int kMaxVpb = 256;
+  __shared__ unsigned long long best[kMaxVpb];
+  __shared__ int32_t start_s[kMaxVpb];
+  __shared__ uint8_t deciding_s[kMaxVpb];
+  __shared__ long long red5[5][32];
+  const int K = w.p.ants;
+  const int vpb = blockDim.x / K;
+  const int lv = threadIdx.x / K;
+  const int ant = threadIdx.x - lv * K;
+  const int32_t vid = blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.V;
+  const int64_t step = w.ctl->step;
+  const DevVehicles& v = w.v;
+
+  if (live && ant == 0) {
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
     }
+    int32_t start = -1;
+    const bool deciding = st == kAtNode;
+    if (deciding)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kQueued)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kOnEdge)
+      start = w.g.col[v.on_edge[vid]];
+    if (start >= 0 && start == v.dest[vid]) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      start = -1;
+    }
+    start_s[lv] = start;
+    deciding_s[lv] = deciding;
+    best[lv] = ~0ull;
   }
+  __syncthreads();
+  long long steps = 0, cands = 0, degs = 0, routes = 0, decided = 0;
+  int32_t start = -1, hops = 0;
+  int64_t cost = 0;
+  int32_t* tour = nullptr;
+  if (live) start = start_s[lv];
+  if (live && start >= 0) {
+    const int32_t dest = v.dest[vid];
+    const int32_t cols = w.d.cols, rows = w.d.rows;
+    const int32_t rd = dest / cols, cd = dest - rd * cols;
+    int32_t rx = start / cols, cx = start - rx * cols;
+    const int32_t hop_limit = w.p.hop_limit;
+    const uint32_t k0 = (uint32_t)w.p.seed, k1 = (uint32_t)(w.p.seed >> 32);
+    const bool ref_rng = w.p.rng == 1;
+    const double* __restrict__ W = w.weight;
+    const int64_t* __restrict__ Cst = w.ecost;
+    if (w.p.scratch_mode) tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+    uint4 rnd = ref_rng ? make_uint4(0, 0, 0, 0)
+                        : philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, 0u), k0, k1);
+    const int32_t max_hops = w.p.max_hops;
+    while ((rx != rd || cx != cd) && (hop_limit == 0 || hops < hop_limit)) {
+      if (hops >= max_hops) {
+        cost = kInf;
+        break;
+      }
+      const int32_t x = rx * cols + cx;
+      const int up = rx > 0, left = cx > 0, right = cx < cols - 1, down = rx < rows - 1;
+      const int dc = cd > cx ? 1 : (cd < cx ? -1 : 0);
+      const int dr = rd > rx ? 1 : (rd < rx ? -1 : 0);
+      // ELL offsets of the (at most two) candidates, in ascending neighbour id
+      const int off_h = dc > 0 ? up + left : up;  // right : left
+      const int off_v = dr > 0 ? up + left + right : 0;  // down : up
+      int oa, ob;  // first / second candidate offsets (ob < 0: single candidate)
+      int32_t na_r, na_c, nb_r, nb_c;
+      if (dr == 0) {
+        oa = off_h; ob = -1; na_r = rx; na_c = cx + dc; nb_r = 0; nb_c = 0;
+      } else if (dc == 0) {
+        oa = off_v; ob = -1; na_r = rx + dr; na_c = cx; nb_r = 0; nb_c = 0;
+      } else if (dr < 0) {  // up (x-cols) precedes the horizontal move
+        oa = off_v; ob = off_h; na_r = rx - 1; na_c = cx; nb_r = rx; nb_c = cx + dc;
+      } else {  // horizontal move precedes down (x+cols)
+        oa = off_h; ob = off_v; na_r = rx; na_c = cx + dc; nb_r = rx + 1; nb_c = cx;
+      }
+      const double wa = W[4 * x + oa];
+      const double wb = ob >= 0 ? W[4 * x + ob] : 0.0;
+      // this hop's uniform (Philox block shared by hops 2k, 2k+1)
+      double u;
+      if (ref_rng) {
+        u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                         (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
+      } else {
+        u = to_unit(philox_half(rnd, hops));
+        if (hops & 1)  // next block for hops+1, +2: off the load/decision chain
+          rnd = philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)(hops + 1) >> 1), k0, k1);
+      }
+      const int c = ob >= 0 ? 2 : 1;
+      const double total = ob >= 0 ? __dadd_rn(wa, wb) : wa;
+      bool take_b;
+      if (total <= 0.0 || !isfinite(total)) {
+        const int p = (int)__dmul_rn(u, (double)c);
+        take_b = ob >= 0 && p >= 1;
+      } else {
+        // cumulative: first candidate with point < cum, default the last one
+        take_b = ob >= 0 && !(__dmul_rn(u, total) < wa);
+      }
+      const int off = take_b ? ob : oa;
+      const int32_t s = 4 * x + off;
+      cost += Cst[s];
+      if (tour) tour[hops] = s;
+      rx = take_b ? nb_r : na_r;
+      cx = take_b ? nb_c : na_c;
+      degs += up + left + right + down;
+      cands += c;
+      ++hops;
+      ++steps;
+    }
+    const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
+    atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
+  }
+  __syncthreads();
+  if (live && start >= 0 && ant == (int)(best[lv] & 1023u)) {
+    // every lattice node != dest has a closer neighbour, so hop 0 succeeds
+    const bool deciding = deciding_s[lv];
+    if (w.p.scratch_mode) {
+      v.plan_ant[vid] = ant;
+    } else {
+      tour = v.plan + (size_t)vid * w.p.plan_cap;
+      const Target<1> t(w.d, v.dest[vid]);
+      hops = ant_walk<1, true>(w, t, vid, ant, start, step, tour).hops;
+    }
+    finish_colony(w, vid, start, tour, hops, deciding, step);
+    routes = 1;
+    decided = deciding;
+  }
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -773,146 +975,123 @@ __device__ int select_phase(const DevParams& p, const int32_t* q, const double* 
   return next_in_order(p, cursor);
 }
 
-__global__ void __launch_bounds__(256) k_signals(DevWorld w) {
-  if (skip_step(w.ctl)) return;
-  __shared__ long long red[32];
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+// C, D, E1 for one signal: density sample (returned), green assignment at an
+// epoch (engine.cpp:223-239, assign_green signals.cpp:111-117), FIFO
+// discharge (signals.cpp:119-135, engine.cpp:241-252).
+__device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
+  const DevSignals& S = w.s;
+  int32_t q[kPhases];
+  double hw[kPhases];
   long long qt = 0;
-  if (s < w.p.S) {
-    const DevSignals& S = w.s;
-    int32_t q[kPhases];
-    double hw[kPhases];
 #pragma unroll
-    for (int ph = 0; ph < kPhases; ++ph) {
-      q[ph] = S.qlen[s * kPhases + ph];
-      hw[ph] = S.head_wait[s * kPhases + ph];
-      qt += q[ph];
-    }
-    // D: assign at an epoch (engine.cpp:223-239, assign_green signals.cpp:111-117)
-    int green = S.green[s];
-    if (!(S.el_s[s] < w.p.green_duration_s)) {
-      green = select_phase(w.p, q, hw, S.cursor[s]);
-      S.green[s] = green;
-      S.cursor[s] = green;
-      S.el_s[s] = 0.0;
-      S.el_steps[s] = 0;
-      S.rem[s * kPhases + green] = 0.0;
-    }
-    // E1: discharge (signals.cpp:119-135, engine.cpp:241-252)
-    const int k = s * kPhases + green;
-    double rem = S.rem[k];
-    rem = __dadd_rn(rem, __dmul_rn(__dmul_rn(w.p.saturation_flow, (double)S.lanes[s]), w.p.dt_s));
-    int budget = (int)floor(rem);
-    rem = __dsub_rn(rem, (double)budget);
-    S.rem[k] = rem;
-    int32_t len = q[green];
-    if (budget > 0 && len > 0) {
-      int32_t head = S.qhead[k];
-      const int64_t step = w.ctl->step;
-      const int32_t node = S.node[s];
-      while (budget > 0 && len > 0) {
-        const int32_t vid = head;
-        head = w.v.qnext[vid];
-        --len;
-        --budget;
-        w.v.queued[vid] += step - w.v.joined[vid] + 1;
-        w.v.state[vid] = kAtNode;
-        w.v.at_node[vid] = node;
-        w.v.queued_phase[vid] = -1;
-      }
-      S.qhead[k] = len ? head : -1;
-      if (!len) S.qtail[k] = -1;
-      S.qlen[k] = len;
-    }
-    if (len == 0) S.head_wait[k] = 0.0;
+  for (int ph = 0; ph < kPhases; ++ph) {
+    q[ph] = S.qlen[s * kPhases + ph];
+    hw[ph] = S.head_wait[s * kPhases + ph];
+    qt += q[ph];
   }
-  qt = block_sum(qt, red);
-  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
-}
-
-// ---------------------------------------------------------------------------
-// E2: motion (engine.cpp:254-295) + occupancy histogram (engine.cpp:316-322)
-// + the next step's count_active / unfinished counts.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_move(DevWorld w) {
-  if (skip_step(w.ctl)) return;
-  __shared__ long long red[32];
-  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
-  long long active = 0, unfinished = 0;
-  if (vid < w.p.V) {
-    const DevVehicles& v = w.v;
+  int green = S.green[s];
+  if (!(S.el_s[s] < w.p.green_duration_s)) {
+    green = select_phase(w.p, q, hw, S.cursor[s]);
+    S.green[s] = green;
+    S.cursor[s] = green;
+    S.el_s[s] = 0.0;
+    S.el_steps[s] = 0;
+    S.rem[s * kPhases + green] = 0.0;
+  }
+  const int k = s * kPhases + green;
+  double rem = S.rem[k];
+  rem = __dadd_rn(rem, __dmul_rn(__dmul_rn(w.p.saturation_flow, (double)S.lanes[s]), w.p.dt_s));
+  int budget = (int)floor(rem);
+  rem = __dsub_rn(rem, (double)budget);
+  S.rem[k] = rem;
+  int32_t len = 0;  // q[green] without dynamic register indexing
+#pragma unroll
+  for (int ph = 0; ph < kPhases; ++ph)
+    if (ph == green) len = q[ph];
+  if (budget > 0 && len > 0) {
+    int32_t head = S.qhead[k];
     const int64_t step = w.ctl->step;
-    uint8_t st = v.state[vid];
-    if (st == kOnEdge) {
-      if (v.latency_debt[vid] >= w.p.dt_us) {
-        v.latency_debt[vid] -= w.p.dt_us;
-        v.lat_steps[vid] += 1;
-      } else {
-        const int64_t prog = v.progress[vid] + v.advance[vid];
-        v.driving[vid] += 1;
-        const int32_t slot = v.on_edge[vid];
-        const int64_t L = w.g.len[slot];
-        if (prog < L) {
-          v.progress[vid] = prog;
-        } else {
-          const int32_t reached = w.g.col[slot];
-          const int32_t bind = w.g.bind[slot];
-          if (reached == v.dest[vid]) {
-            st = kArrived;
-            v.progress[vid] = prog;
-            v.arrive[vid] = step + 1;
-            if (w.p.deposit == 0 && (w.p.algorithm == 1 || w.p.algorithm == 4)) {
-              // ACO deposit on completion (engine.cpp:341-346, pheromone.cpp:80-90);
-              // per-edge sum-then-clamp equals sequential clamping for amounts >= 0.
-              const int32_t n = v.path_n[vid];
-              if (n > 0) {
-                const double km = __ddiv_rn((double)v.path_len_mm[vid], 1e6);
-                const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
-                const int32_t* path = v.path + (size_t)vid * w.p.path_cap;
-                for (int i = 0; i < n; ++i)
-                  atomicAdd((unsigned long long*)&w.dep[path[i]], (unsigned long long)amount);
-              }
-            }
-          } else if (bind >= 0) {
-            st = kQueued;
-            v.at_node[vid] = reached;
-            v.queued_phase[vid] = bind & 7;
-            v.joined[vid] = step + 1;
-            v.progress[vid] = 0;
-            v.arr_next[vid] = atomicExch(&w.s.arr_head[bind], vid);
-          } else {
-            st = kAtNode;
-            v.at_node[vid] = reached;
-            v.overshoot[vid] = prog - L;
-            v.progress[vid] = 0;
-          }
-          v.state[vid] = st;
-        }
-      }
-      if (st == kOnEdge) atomicAdd(&w.occ_new[v.on_edge[vid]], 1);
+    const int32_t node = S.node[s];
+    while (budget > 0 && len > 0) {
+      const int32_t vid = head;
+      head = w.v.qnext[vid];
+      --len;
+      --budget;
+      w.v.queued[vid] += step - w.v.joined[vid] + 1;
+      w.v.state[vid] = kAtNode;
+      w.v.at_node[vid] = node;
+      w.v.queued_phase[vid] = -1;
     }
-    active = st == kAtNode || st == kOnEdge || st == kQueued ||
-             (st == kPending && v.depart[vid] == step + 1);
-    unfinished = st != kArrived && st != kRetired;
+    S.qhead[k] = len ? head : -1;
+    if (!len) S.qtail[k] = -1;
+    S.qlen[k] = len;
   }
-  active = block_sum(active, red);
-  unfinished = block_sum(unfinished, red);
-  if (threadIdx.x == 0) {
-    if (active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
-    if (unfinished) atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
-  }
+  if (len == 0) S.head_wait[k] = 0.0;
+  return qt;
 }
 
-// ---------------------------------------------------------------------------
-// E3: enqueue commit in ascending vid (engine.cpp:297-301) + timers
-// (engine.cpp:303-314).  This step's arrivals all share joined = step+1,
-// larger than every queued key, so FIFO order = old queue then the
+// E2 for one vehicle: motion (engine.cpp:254-295), arrival deposit (ACO,
+// engine.cpp:341-346; per-edge sum-then-clamp equals sequential clamping for
+// amounts >= 0), queue arrival push, occupancy histogram (engine.cpp:316-322)
+// and the next step's count_active / unfinished contributions.
+__device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished) {
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  uint8_t st = v.state[vid];
+  if (st == kOnEdge) {
+    if (v.latency_debt[vid] >= w.p.dt_us) {
+      v.latency_debt[vid] -= w.p.dt_us;
+      v.lat_steps[vid] += 1;
+    } else {
+      const int64_t prog = v.progress[vid] + v.advance[vid];
+      v.driving[vid] += 1;
+      const int32_t slot = v.on_edge[vid];
+      const int64_t L = w.g.len[slot];
+      if (prog < L) {
+        v.progress[vid] = prog;
+      } else {
+        const int32_t reached = w.g.col[slot];
+        const int32_t bind = w.g.bind[slot];
+        if (reached == v.dest[vid]) {
+          st = kArrived;
+          v.progress[vid] = prog;
+          v.arrive[vid] = step + 1;
+          if (w.p.deposit == 0 && (w.p.algorithm == 1 || w.p.algorithm == 4)) {
+            const int32_t n = v.path_n[vid];
+            if (n > 0) {
+              const double km = __ddiv_rn((double)v.path_len_mm[vid], 1e6);
+              const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+              const int32_t* path = v.path + (size_t)vid * w.p.path_cap;
+              for (int i = 0; i < n; ++i) atomicAdd((unsigned long long*)&w.dep[path[i]], (unsigned long long)amount);
+            }
+          }
+        } else if (bind >= 0) {
+          st = kQueued;
+          v.at_node[vid] = reached;
+          v.queued_phase[vid] = bind & 7;
+          v.joined[vid] = step + 1;
+          v.progress[vid] = 0;
+          v.arr_next[vid] = atomicExch(&w.s.arr_head[bind], vid);
+        } else {
+          st = kAtNode;
+          v.at_node[vid] = reached;
+          v.overshoot[vid] = prog - L;
+          v.progress[vid] = 0;
+        }
+        v.state[vid] = st;
+      }
+    }
+    if (st == kOnEdge) atomicAdd(&w.occ_new[v.on_edge[vid]], 1);
+  }
+  active += st == kAtNode || st == kOnEdge || st == kQueued || (st == kPending && v.depart[vid] == step + 1);
+  unfinished += st != kArrived && st != kRetired;
+}
+
+// E3 for one signal: enqueue commit in ascending vid (engine.cpp:297-301) and
+// timers (engine.cpp:303-314).  This step's arrivals all share joined =
+// step+1, larger than every queued key, so FIFO order = old queue then the
 // arrivals by ascending vid.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_e3(DevWorld w) {
-  if (skip_step(w.ctl)) return;
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= w.p.S) return;
+__device__ __forceinline__ void sig_e3(const DevWorld& w, int32_t s) {
   const DevSignals& S = w.s;
   const int64_t now = w.ctl->step + 1;
   for (int ph = 0; ph < kPhases; ++ph) {
@@ -949,14 +1128,9 @@ __global__ void __launch_bounds__(256) k_e3(DevWorld w) {
   S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
 }
 
-// ---------------------------------------------------------------------------
-// F (scoped MACO): per decision node, replay the step's decisions at that
+// F (scoped MACO) for one decision node: replay the step's decisions at that
 // node in ascending vid (apply_maco_update_scoped, pheromone.cpp:48-59).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
-  if (skip_step(w.ctl)) return;
-  const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= w.g.n) return;
+__device__ __forceinline__ void node_scoped(const DevWorld& w, int32_t u) {
   const int32_t chain = w.dec_head[u];
   if (chain < 0) return;
   w.dec_head[u] = -1;
@@ -977,100 +1151,146 @@ __global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// F + G per slot: MACO fold (fold_maco_edge, parallel.cpp:77-92) or exact
+// F + G for one slot: MACO fold (fold_maco_edge, parallel.cpp:77-92) or exact
 // deposit sum-then-clamp, evaporation (pheromone.cpp:61-67), colony
-// congestion term, occupancy hand-off + max, weights for the next step.
-// The last block finalizes the step (n_t, step, finished()).
+// congestion term, occupancy hand-off, next step's weight / tour cost
+// (routing.cpp:90-94).  Returns the slot's occupancy (for the running max).
+__device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
+  const DevParams& p = w.p;
+  int64_t t = w.tau[s];
+  const int alg = p.algorithm;
+  if ((alg == 2 || alg == 3) && !p.siblings_only) {
+    const int64_t D = w.ctl->dcount;
+    const int32_t chain = w.dec_head[s];
+    int64_t done = 0;
+    if (chain >= 0) {
+      w.dec_head[s] = -1;
+      int32_t last = -1;
+      for (;;) {
+        int32_t best = INT32_MAX;
+        for (int32_t c = chain; c >= 0; c = w.v.dec_next[c])
+          if (c > last && c < best) best = c;
+        if (best == INT32_MAX) break;
+        last = best;
+        const int64_t pos = w.v.pos[best];
+        const int64_t gap = pos - done;
+        if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
+        t = min(p.tau_hi, t + p.inc);
+        done = pos + 1;
+      }
+    }
+    const int64_t gap = D - done;
+    if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
+  } else if (alg == 1 || alg == 4) {
+    const int64_t d = w.dep[s];
+    if (d) {
+      t = min(p.tau_hi, t + d);
+      w.dep[s] = 0;
+    }
+  }
+  const int64_t scaled = (int64_t)floor(__dmul_rn(p.one_minus_rho, (double)t));
+  t = max(p.tau_lo, scaled);
+  const int32_t occ = w.occ_new[s];
+  if (alg == 4 && p.cong_evap && occ > 0) t = max(p.tau_lo, t - p.dec * (int64_t)occ);
+  w.tau[s] = t;
+  w.occ_cur[s] = occ;
+  w.occ_new[s] = 0;
+  if (alg == 1 || alg == 4) {
+    const double tau_d = __ddiv_rn((double)t, 1e6);
+    const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : pow(tau_d, p.alpha));
+    double wt = __dmul_rn(ta, w.g.eta_beta[s]);
+    int64_t cost = w.g.len[s];
+    if (alg == 4 && p.congestion) {
+      const int32_t b = w.g.bind[s];
+      const int32_t load = occ + (b >= 0 ? w.s.qlen[b] : 0);
+      wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
+      cost = cost + cost * (int64_t)load;
+    }
+    w.weight[s] = wt;
+    w.ecost[s] = cost;
+  }
+  return occ;
+}
+
+// Step finalize (engine.cpp:399 ++step, finished() engine.cpp:146-152).
+__device__ __forceinline__ void finalize_step(const DevWorld& w) {
+  DevCtl* c = w.ctl;
+  c->blocks_done = 0;
+  c->qsamples += w.p.S;
+  c->n_t = c->n_next;
+  c->n_next = 0;
+  c->dcount = 0;
+  const int64_t step = c->step + 1;
+  c->step = step;
+  c->done = (step >= w.p.max_steps || c->unfinished == 0) ? 1 : 0;
+  c->unfinished = 0;
+}
+
+__device__ __forceinline__ int32_t block_max(int32_t m, int32_t* smax) {
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 1; i < (int)((blockDim.x + 31) >> 5); ++i) m = max(m, smax[i]);
+  return m;  // valid in thread 0
+}
+
 // ---------------------------------------------------------------------------
+// multi-kernel tail (large worlds): one thread per entity per stage
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_signals(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  long long qt = s < w.p.S ? sig_cde1(w, s) : 0;
+  qt = block_sum(qt, red);
+  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+}
+
+__global__ void __launch_bounds__(256) k_move(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  long long active = 0, unfinished = 0;
+  if (vid < w.p.V) veh_move(w, vid, active, unfinished);
+  active = block_sum(active, red);
+  unfinished = block_sum(unfinished, red);
+  if (threadIdx.x == 0) {
+    if (active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
+    if (unfinished) atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_e3(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < w.p.S) sig_e3(w, s);
+}
+
+__global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < w.g.n) node_scoped(w, u);
+}
+
+// The last block to finish finalizes the step.
 __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   if (skip_step(w.ctl)) return;
   __shared__ int32_t smax[32];
   __shared__ bool is_last;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  const DevParams& p = w.p;
-  int32_t occ = 0;
-  if (s < w.g.M && w.g.slot_edge[s] >= 0) {
-    int64_t t = w.tau[s];
-    const int alg = p.algorithm;
-    if ((alg == 2 || alg == 3) && !p.siblings_only) {
-      const int64_t D = w.ctl->dcount;
-      const int32_t chain = w.dec_head[s];
-      int64_t done = 0;
-      if (chain >= 0) {
-        w.dec_head[s] = -1;
-        int32_t last = -1;
-        for (;;) {
-          int32_t best = INT32_MAX;
-          for (int32_t c = chain; c >= 0; c = w.v.dec_next[c])
-            if (c > last && c < best) best = c;
-          if (best == INT32_MAX) break;
-          last = best;
-          const int64_t pos = w.v.pos[best];
-          const int64_t gap = pos - done;
-          if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
-          t = min(p.tau_hi, t + p.inc);
-          done = pos + 1;
-        }
-      }
-      const int64_t gap = D - done;
-      if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
-    } else if (alg == 1 || alg == 4) {
-      const int64_t d = w.dep[s];
-      if (d) {
-        t = min(p.tau_hi, t + d);
-        w.dep[s] = 0;
-      }
-    }
-    // G: evaporate_one
-    const int64_t scaled = (int64_t)floor(__dmul_rn(p.one_minus_rho, (double)t));
-    t = max(p.tau_lo, scaled);
-    occ = w.occ_new[s];
-    if (alg == 4 && p.cong_evap && occ > 0) t = max(p.tau_lo, t - p.dec * (int64_t)occ);
-    w.tau[s] = t;
-    w.occ_cur[s] = occ;
-    w.occ_new[s] = 0;
-    // next step's roulette weight / tour cost (routing.cpp:90-94)
-    if (alg == 1 || alg == 4) {
-      const double tau_d = __ddiv_rn((double)t, 1e6);
-      const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : pow(tau_d, p.alpha));
-      double wt = __dmul_rn(ta, w.g.eta_beta[s]);
-      int64_t cost = w.g.len[s];
-      if (alg == 4 && p.congestion) {
-        const int32_t b = w.g.bind[s];
-        const int32_t load = occ + (b >= 0 ? w.s.qlen[b] : 0);
-        wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
-        cost = cost + cost * (int64_t)load;
-      }
-      w.weight[s] = wt;
-      w.ecost[s] = cost;
-    }
-  }
-  // block max of occupancy
-  int32_t m = occ;
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
-  __syncthreads();
+  const int32_t occ = (s < w.g.M && w.g.slot_edge[s] >= 0) ? slot_fg(w, s) : 0;
+  const int32_t m = block_max(occ, smax);
   if (threadIdx.x == 0) {
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, smax[i]);
     if (m > 0) atomicMax(&w.ctl->max_occ, m);
     __threadfence();
     const unsigned prev = atomicAdd(&w.ctl->blocks_done, 1u);
     is_last = prev == gridDim.x - 1;
   }
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {  // step finalize (engine.cpp:399, 146-152)
+  if (is_last && threadIdx.x == 0) {
     __threadfence();
-    DevCtl* c = w.ctl;
-    c->blocks_done = 0;
-    c->qsamples += p.S;
-    c->n_t = c->n_next;
-    c->n_next = 0;
-    c->dcount = 0;
-    const int64_t step = c->step + 1;
-    c->step = step;
-    c->done = (step >= p.max_steps || c->unfinished == 0) ? 1 : 0;
-    c->unfinished = 0;
+    finalize_step(w);
     __threadfence();
   }
 }
@@ -1140,6 +1360,9 @@ __global__ void k_next_node(DevWorld w, int algorithm, int count, const int32_t*
 // launch plumbing
 // ---------------------------------------------------------------------------
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+// stages C..G: latency-bound per-entity chains, so small blocks spread them
+// over as many SMs as possible
+constexpr int kTail = 64;
 
 void colony_shape(int ants, int* threads, int* vpb) {
   int t = ants <= 256 ? 256 : ((ants + 31) / 32) * 32;
@@ -1152,8 +1375,13 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   const int V = w.p.V, S = w.p.S, m = w.g.m, n = w.g.n;
   if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 2) goto tail;
-  if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
-    const int threads = 256, vpb = 256 / w.p.ants;
+  if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
+    const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
+    k_colony_grid<<<blocks_for(V, vpb), threads, 0, st>>>(w);
+  } else if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
+    // one vehicle's colony per block when it fills whole warps (no block
+    // barrier couples different vehicles' walk lengths), else packed
+    const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
     if (w.d.kind == 1)
       k_colony_ell4<1><<<blocks_for(V, vpb), threads, 0, st>>>(w);
     else
@@ -1182,19 +1410,19 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 1) return cudaGetLastError();
 tail:
-  if (S > 0) k_signals<<<blocks_for(S, 256), 256, 0, st>>>(w);
-  k_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
-  if (S > 0) k_e3<<<blocks_for(S, 256), 256, 0, st>>>(w);
+  if (S > 0) k_signals<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
+  k_move<<<blocks_for(V, kTail), kTail, 0, st>>>(w);
+  if (S > 0) k_e3<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
   if (w.p.algorithm == 2 || w.p.algorithm == 3) {
     if (w.p.siblings_only) {
-      k_scoped<<<blocks_for(n, 256), 256, 0, st>>>(w);
+      k_scoped<<<blocks_for(n, kTail), kTail, 0, st>>>(w);
     } else {
       size_t bytes = r.scan_temp_bytes;
       cudaError_t e = cub::DeviceScan::ExclusiveSum(r.scan_temp, bytes, w.v.dflag, w.v.pos, V, st);
       if (e != cudaSuccess) return e;
     }
   }
-  k_edges<<<blocks_for(w.g.M, 256), 256, 0, st>>>(w);
+  k_edges<<<blocks_for(w.g.M, kTail), kTail, 0, st>>>(w);
   return cudaGetLastError();
 }
 
