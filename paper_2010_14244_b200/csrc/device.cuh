@@ -23,7 +23,8 @@ struct DevGraph {
   int32_t n, m;
   int32_t ell;              // ELL row width (4 or 8; slot = x*ell + i) or 0 for plain CSR
   int32_t M;                // slot-space size (n*ell for ELL, m for CSR); padding slots have slot_edge = -1
-  const int2* row;          // [n] {first slot, out-degree}
+  const int2* row;          // [n] {first slot, row span} (span = ELL width, or out-degree for CSR)
+  const int32_t* deg;       // [n] out-degree
   const int32_t* key;       // [M] colony fast path: packed grid (row<<16|col) of the neighbour, or
                             //     the neighbour id for table distances; -1 on padding
   const int32_t* col;       // [m] neighbour (edge.to) per slot
@@ -68,6 +69,7 @@ struct DevParams {
   int32_t scratch_mode;     // 1: every ant's tour kept in scratch, the plan is the winner's row
   int32_t need_positions;  // MACO network-wide fold
   int32_t prefetch;        // bulk-prefetch the step's state into L2 at the start of stage B
+  uint32_t rk[20];         // Philox4x32-10 round keys of `seed` (host key schedule)
   int32_t record_paths;
 };
 
@@ -84,6 +86,12 @@ struct DevCtl {
   int32_t max_occ;
   uint32_t blocks_done;
   int32_t error;  // device-side overflow flag (path buffer)
+  // stage trace of the current step (%globaltimer ns; written when trace is on):
+  // [0] walk start (min), [1] walk staging done (max), [2] walk end (max),
+  // [3] tail start (min), [4] E1||E2 done, [5] E3 done, [6] F+G done
+  unsigned long long trace[8];
+  int32_t trace_on;
+  int32_t _pad2;
 };
 
 struct DevVehicles {

@@ -468,6 +468,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
   CK(cudaSetDevice(h->device));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CK(configure_kernels());
   DevBuffers& B = h->buf;
   DevWorld& w = h->w;
 
@@ -550,16 +551,27 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // (one aligned vector load per row), plain CSR otherwise ------------------
   int32_t maxdeg = 0;
   for (int32_t u = 0; u < n; ++u) maxdeg = std::max(maxdeg, g.out_ptr[u + 1] - g.out_ptr[u]);
-  const int32_t ell = maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 0);
+  const bool lattice = dd->kind == GMACO_DIST_GRID;  // lattice shape validated above
+  const int32_t ell = lattice || maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 0);
   const int32_t M = ell ? n * ell : m;
   h->ell = ell;
   h->M = M;
   h->slot_edge.assign(M, -1);
   std::vector<int2> row(n);
+  std::vector<int32_t> deg(n);
   for (int32_t u = 0; u < n; ++u) {
     const int32_t first = ell ? u * ell : g.out_ptr[u];
-    row[u] = make_int2(first, g.out_ptr[u + 1] - g.out_ptr[u]);
-    for (int32_t i = 0; i < row[u].y; ++i) h->slot_edge[first + i] = g.out_edge[g.out_ptr[u] + i];
+    deg[u] = g.out_ptr[u + 1] - g.out_ptr[u];
+    row[u] = make_int2(first, ell ? ell : deg[u]);
+    for (int32_t i = 0; i < deg[u]; ++i) {
+      const int32_t e = g.out_edge[g.out_ptr[u] + i];
+      int32_t slot = first + i;
+      if (lattice) {  // direction-slotted rows {up, left, right, down} = ascending neighbour id
+        const int32_t Cc = dd->grid_cols, v = g.to[e];
+        slot = first + (v == u - Cc ? 0 : v == u - 1 ? 1 : v == u + 1 ? 2 : 3);
+      }
+      h->slot_edge[slot] = e;
+    }
   }
   for (int32_t s = 0; s < M; ++s)
     if (h->slot_edge[s] >= 0) g.edge_slot[h->slot_edge[s]] = s;
@@ -602,6 +614,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.g.ell = ell;
   w.g.M = M;
   w.g.row = B.upload(row);
+  w.g.deg = B.upload(deg);
   w.g.key = B.upload(key);
   w.g.col = B.upload(col);
   w.g.len = B.upload(slen);
@@ -648,6 +661,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
   p.prefetch = 1;
+  for (int r = 0; r < 10; ++r) {  // Philox4x32-10 key schedule of the seed
+    p.rk[2 * r] = (uint32_t)c.seed + (uint32_t)r * 0x9E3779B9u;
+    p.rk[2 * r + 1] = (uint32_t)(c.seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+  }
   // realized-path storage: needed for completion deposits; paths are bounded by
   // the decision count (<= max_steps) and, with the progress filter, by n-1.
   p.path_cap = (int32_t)std::max<int64_t>(
@@ -769,6 +786,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     h->res.scan_temp_bytes = scan_temp_bytes(V);
     h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
   }
+  h->res.coop_blocks = coop_tail_blocks(w, h->device);
   CK(cudaEventCreate(&h->ev_a));
   CK(cudaEventCreate(&h->ev_b));
   CK(cudaDeviceSynchronize());
@@ -1208,6 +1226,27 @@ int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, doubl
     }
     for (auto& e : ev) cudaEventDestroy(e);
     refresh_ctl(h);
+  });
+}
+
+// Profiling hook: stage timestamps (%globaltimer ns) of the next `steps`
+// steps' LAST step; see DevCtl::trace.  Not part of the reference surface.
+int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out8) {
+  if (!h || !out8) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    for (int32_t i = 0; i < steps; ++i) {
+      DevCtl t;
+      CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
+      t.trace_on = 1;
+      for (int k = 0; k < 8; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
+      CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
+      run_steps(h, 1);
+    }
+    DevCtl t;
+    CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 8; ++k) out8[k] = t.trace[k];
+    t.trace_on = 0;
+    CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
   });
 }
 

@@ -14,15 +14,20 @@
 // built with -fmad=false) so they round exactly like the reference's
 // FMA-free x86-64 build.
 
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device.cuh"
 #include "kernels.h"
 
 namespace gmaco {
+
+namespace cg = cooperative_groups;
+constexpr int kTailCoop = 128;
 
 // ---------------------------------------------------------------------------
 // counter-based RNG (rng.hpp:21-56) and Philox4x32-10
@@ -52,6 +57,17 @@ __device__ __forceinline__ uint4 philox4(uint4 c, uint32_t k0, uint32_t k1) {
     c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+// Same function with the key schedule precomputed on the host:
+// rk[2r], rk[2r+1] = key words of round r (kernel-parameter constants).
+__device__ __forceinline__ uint4 philox4_rk(uint4 c, const uint32_t* rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0);
   }
   return c;
 }
@@ -115,11 +131,13 @@ __device__ __forceinline__ Row scan_row(const DevGraph& g, const Target<DK>& t, 
   Row r;
   const int2 ri = __ldg(g.row + x);
   r.first = ri.x;
-  r.deg = ri.y;
+  r.deg = 0;
   r.dx = t.dist(x);
   r.reach = r.closer = r.sp = 0u;
-  for (int i = 0; i < r.deg; ++i) {
+  for (int i = 0; i < ri.y; ++i) {  // ri.y = row span; ELL rows may hold holes (col -1)
     const int32_t nb = __ldg(g.col + r.first + i);
+    if (nb < 0) continue;
+    ++r.deg;
     const int64_t dn = t.dist(nb);
     if (dn == kInf) continue;
     r.reach |= 1u << i;
@@ -137,7 +155,9 @@ __device__ __forceinline__ int32_t dijkstra_pick(const DevGraph& g, const Target
   const int2 ri = __ldg(g.row + x);
   for (int i = 0; i < ri.y; ++i) {
     const int32_t s = ri.x + i;
-    const int64_t dn = t.dist(__ldg(g.col + s));
+    const int32_t nb = __ldg(g.col + s);
+    if (nb < 0) continue;
+    const int64_t dn = t.dist(nb);
     if (dn == kInf) continue;
     if (__ldg(g.len + s) + dn == dx) return s;
   }
@@ -212,6 +232,18 @@ __device__ __forceinline__ int32_t maco_pick(const DevWorld& w, int32_t first, u
     }
   }
   return second;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_min(DevCtl* c, int i) {
+  if (c->trace_on) atomicMin(&c->trace[i], gtimer());
+}
+__device__ __forceinline__ void trace_max(DevCtl* c, int i) {
+  if (c->trace_on) atomicMax(&c->trace[i], gtimer());
 }
 
 __device__ __forceinline__ bool skip_step(const DevCtl* ctl) {
@@ -800,14 +832,18 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 // sequential roulette and one tour-cost load — identical decisions to
 // k_colony / k_colony_ell4 (same candidate order, same arithmetic).
 // ---------------------------------------------------------------------------
+template <bool kSmem, bool kScratch>
 __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  if (threadIdx.x == 0) trace_min(w.ctl, 0);
   if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   constexpr int kMaxVpb = 256;
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
+  __shared__ int32_t done_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
   __shared__ long long red5[5][32];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
@@ -816,7 +852,32 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   const bool live = lv < vpb && vid < w.p.V;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
-
+  const double* __restrict__ W = w.weight;
+  const int64_t* __restrict__ Cst = w.ecost;
+  const int32_t* sdeg = nullptr;
+  __shared__ __align__(8) uint64_t stage_bar;
+  if (kSmem) {
+    // Stage this step's weight / tour-cost tables and the degree table in
+    // shared memory with three TMA bulk copies (cp.async.bulk) completing on
+    // one mbarrier; the other threads overlap the vehicle prologue below.
+    const uint32_t bW = 8u * (uint32_t)w.g.M, bD = 4u * (uint32_t)w.g.n;
+    if (threadIdx.x == 0) {
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dyn_smem);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bW + bD) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(w.weight), "r"(bW), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst + bW), "l"(w.ecost), "r"(bW), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst + 2 * bW), "l"(w.g.deg), "r"(bD), "r"(bar) : "memory");
+    }
+    W = reinterpret_cast<const double*>(dyn_smem);
+    Cst = reinterpret_cast<const int64_t*>(dyn_smem + bW);
+    sdeg = reinterpret_cast<const int32_t*>(dyn_smem + 2 * bW);
+  }
   if (live && ant == 0) {
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
@@ -840,9 +901,17 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     }
     start_s[lv] = start;
     deciding_s[lv] = deciding;
+    done_s[lv] = 0;
     best[lv] = ~0ull;
   }
   __syncthreads();
+  if (kSmem) {  // TMA tables landed (phase 0 of the staging mbarrier)
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
+        : "memory");
+  }
+  if (threadIdx.x == 0) trace_max(w.ctl, 1);
   long long steps = 0, cands = 0, degs = 0, routes = 0, decided = 0;
   int32_t start = -1, hops = 0;
   int64_t cost = 0;
@@ -853,91 +922,103 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     const int32_t cols = w.d.cols, rows = w.d.rows;
     const int32_t rd = dest / cols, cd = dest - rd * cols;
     int32_t rx = start / cols, cx = start - rx * cols;
-    const int32_t hop_limit = w.p.hop_limit;
-    const uint32_t k0 = (uint32_t)w.p.seed, k1 = (uint32_t)(w.p.seed >> 32);
-    const bool ref_rng = w.p.rng == 1;
-    const double* __restrict__ W = w.weight;
-    const int64_t* __restrict__ Cst = w.ecost;
-    if (w.p.scratch_mode) tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
-    uint4 rnd = ref_rng ? make_uint4(0, 0, 0, 0)
-                        : philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, 0u), k0, k1);
-    const int32_t max_hops = w.p.max_hops;
-    while ((rx != rd || cx != cd) && (hop_limit == 0 || hops < hop_limit)) {
-      if (hops >= max_hops) {
-        cost = kInf;
-        break;
-      }
-      const int32_t x = rx * cols + cx;
-      const int up = rx > 0, left = cx > 0, right = cx < cols - 1, down = rx < rows - 1;
-      const int dc = cd > cx ? 1 : (cd < cx ? -1 : 0);
-      const int dr = rd > rx ? 1 : (rd < rx ? -1 : 0);
-      // ELL offsets of the (at most two) candidates, in ascending neighbour id
-      const int off_h = dc > 0 ? up + left : up;  // right : left
-      const int off_v = dr > 0 ? up + left + right : 0;  // down : up
-      int oa, ob;  // first / second candidate offsets (ob < 0: single candidate)
-      int32_t na_r, na_c, nb_r, nb_c;
-      if (dr == 0) {
-        oa = off_h; ob = -1; na_r = rx; na_c = cx + dc; nb_r = 0; nb_c = 0;
-      } else if (dc == 0) {
-        oa = off_v; ob = -1; na_r = rx + dr; na_c = cx; nb_r = 0; nb_c = 0;
-      } else if (dr < 0) {  // up (x-cols) precedes the horizontal move
-        oa = off_v; ob = off_h; na_r = rx - 1; na_c = cx; nb_r = rx; nb_c = cx + dc;
-      } else {  // horizontal move precedes down (x+cols)
-        oa = off_h; ob = off_v; na_r = rx; na_c = cx + dc; nb_r = rx + 1; nb_c = cx;
-      }
-      const double wa = W[4 * x + oa];
-      const double wb = ob >= 0 ? W[4 * x + ob] : 0.0;
-      // this hop's uniform (Philox block shared by hops 2k, 2k+1)
-      double u;
-      if (ref_rng) {
-        u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
-                         (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
-      } else {
-        u = to_unit(philox_half(rnd, hops));
-        if (hops & 1)  // next block for hops+1, +2: off the load/decision chain
-          rnd = philox4(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)(hops + 1) >> 1), k0, k1);
-      }
-      const int c = ob >= 0 ? 2 : 1;
-      const double total = ob >= 0 ? __dadd_rn(wa, wb) : wa;
-      bool take_b;
-      if (total <= 0.0 || !isfinite(total)) {
-        const int p = (int)__dmul_rn(u, (double)c);
-        take_b = ob >= 0 && p >= 1;
-      } else {
-        // cumulative: first candidate with point < cum, default the last one
-        take_b = ob >= 0 && !(__dmul_rn(u, total) < wa);
-      }
-      const int off = take_b ? ob : oa;
-      const int32_t s = 4 * x + off;
+    // The walk is monotone: the signs of (rd - rx, cd - cx) never flip and
+    // every hop removes one unit of Manhattan distance, so the hop count is
+    // known up front (the generic loop's x != dest / hop_limit / max_hops
+    // tests collapse to this count and a failure flag).
+    const int dc = cd > cx ? 1 : -1, dr = rd > rx ? 1 : -1;
+    int32_t rem_h = abs(cd - cx), rem_v = abs(rd - rx);
+    int32_t n = rem_h + rem_v;
+    if (w.p.hop_limit && n > w.p.hop_limit) n = w.p.hop_limit;
+    const bool capped = n > w.p.max_hops;  // generic walker fails at hop max_hops
+    if (capped) n = w.p.max_hops;
+    int32_t* tp = kScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
+    tour = tp;
+    int32_t idegs = 0, icands = 0;
+    // Direction-slotted lattice rows: slot 4x+{0,1,2,3} = {up, left, right,
+    // down} (holes at the border), i.e. ascending neighbour id.  With the
+    // walk direction fixed, the candidate slots are per-walk constants: when
+    // both moves remain, the first candidate is "up" if moving up, else the
+    // horizontal move.
+    const int off_h = dc > 0 ? 2 : 1, off_v = dr > 0 ? 3 : 0;
+    const int step_h = dc, step_v = dr * cols;
+    const bool v_first = dr < 0;
+    int32_t x = start;
+    auto hop = [&](uint64_t bits) {
+      const double u = to_unit(bits);
+      const bool two = rem_h > 0 && rem_v > 0;
+      const bool a_is_v = two ? v_first : rem_h == 0;
+      const int oa = a_is_v ? off_v : off_h, ob = a_is_v ? off_h : off_v;
+      const int xa = 4 * x + oa, xb = 4 * x + (two ? ob : oa);
+      const double wa = W[xa];
+      const double wb = two ? W[xb] : 0.0;
+      const double total = __dadd_rn(wa, wb);  // + exact 0.0 for a single candidate
+      // routing.cpp:100-113 without branches: total <= 0 or non-finite picks
+      // uniformly (floor(u*2) >= 1 takes the second), else the first
+      // candidate iff u*total < wa
+      const bool bad = !(total > 0.0) || __double_as_longlong(fabs(total)) >= 0x7ff0000000000000ll;
+      const bool take_b = two && (bad ? __dmul_rn(u, 2.0) >= 1.0 : !(__dmul_rn(u, total) < wa));
+      const bool move_v = take_b ? !a_is_v : a_is_v;
+      const int32_t s = take_b ? xb : xa;
       cost += Cst[s];
-      if (tour) tour[hops] = s;
-      rx = take_b ? nb_r : na_r;
-      cx = take_b ? nb_c : na_c;
-      degs += up + left + right + down;
-      cands += c;
-      ++hops;
-      ++steps;
+      if (kScratch) *tp++ = s;
+      idegs += kSmem ? sdeg[x] : __ldg(w.g.deg + x);
+      icands += 1 + two;
+      x += move_v ? step_v : step_h;
+      rem_v -= move_v;
+      rem_h -= !move_v;
+    };
+    if (w.p.rng == 1) {
+      for (int32_t h = 0; h < n; ++h)
+        hop(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                 (uint64_t)step | ((uint64_t)(uint32_t)h << 40)));
+    } else {
+      // hop pair (2p, 2p+1) uses Philox block p; block p+1 is computed in the
+      // same basic block, so its independent chain fills the hops' latency
+      uint4 cur = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, 0u), w.p.rk);
+      const int32_t pairs = n >> 1;
+      for (int32_t p = 0; p < pairs; ++p) {
+        const uint4 nxt = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)p + 1u), w.p.rk);
+        hop(((uint64_t)cur.x << 32) | cur.y);
+        hop(((uint64_t)cur.z << 32) | cur.w);
+        cur = nxt;
+      }
+      if (n & 1) hop(((uint64_t)cur.x << 32) | cur.y);
     }
+    if (capped) cost = kInf;
+    hops = n;
+    steps = n;
+    degs = idegs;
+    cands = icands;
+    // best tour by (cost, ant); the vehicle's LAST ant to finish runs the
+    // epilogue, so no block barrier couples different vehicles' walk lengths
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
-  }
-  __syncthreads();
-  if (live && start >= 0 && ant == (int)(best[lv] & 1023u)) {
-    // every lattice node != dest has a closer neighbour, so hop 0 succeeds
-    const bool deciding = deciding_s[lv];
-    if (w.p.scratch_mode) {
-      v.plan_ant[vid] = ant;
-    } else {
-      tour = v.plan + (size_t)vid * w.p.plan_cap;
-      const Target<1> t(w.d, v.dest[vid]);
-      hops = ant_walk<1, true>(w, t, vid, ant, start, step, tour).hops;
+    __threadfence_block();
+    if (atomicAdd(&done_s[lv], 1) == K - 1) {
+      __threadfence_block();
+      const int winner = (int)(best[lv] & 1023u);
+      const bool deciding = deciding_s[lv];
+      int32_t wh;
+      if (kScratch) {
+        v.plan_ant[vid] = winner;
+        tour = v.scratch + ((size_t)vid * K + winner) * (size_t)w.p.plan_cap;
+        wh = hops;  // every ant of the vehicle walks the same (capped) hop count
+      } else {  // replay the winner to materialize its tour
+        tour = v.plan + (size_t)vid * w.p.plan_cap;
+        const Target<1> t(w.d, v.dest[vid]);
+        wh = ant_walk<1, true>(w, t, vid, winner, start, step, tour).hops;
+      }
+      finish_colony(w, vid, start, tour, wh, deciding, step);
+      routes = 1;
+      decided = deciding;
     }
-    finish_colony(w, vid, start, tour, hops, deciding, step);
-    routes = 1;
-    decided = deciding;
   }
   const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
-  if (threadIdx.x == 0) flush_counters(w.ctl, t);
+  if (threadIdx.x == 0) {
+    flush_counters(w.ctl, t);
+    trace_max(w.ctl, 2);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1145,6 +1226,7 @@ __device__ __forceinline__ void node_scoped(const DevWorld& w, int32_t u) {
     const int32_t chosen = w.v.on_edge[best];
     for (int i = 0; i < ri.y; ++i) {
       const int32_t s = ri.x + i;
+      if (w.g.col[s] < 0) continue;  // ELL hole
       const int64_t t = w.tau[s];
       w.tau[s] = s == chosen ? min(w.p.tau_hi, t + w.p.inc) : max(w.p.tau_lo, t - w.p.dec);
     }
@@ -1296,6 +1378,58 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
 }
 
 // ---------------------------------------------------------------------------
+// cooperative tail (one launch for stages C..G): E1 (signals) and E2 (motion)
+// touch disjoint vehicles — queued vs on-edge — and disjoint queue fields
+// (E1: qhead/qnext/qlen, E2: arrival stacks), so they run concurrently;
+// grid.sync() orders E3 after E2 and F+G after E3.  Launched with the
+// cooperative attribute, which guarantees co-residency of the grid.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
+  if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
+  cg::grid_group grid = cg::this_grid();
+  if (threadIdx.x == 0) trace_min(w.ctl, 3);
+  __shared__ long long red[32];
+  __shared__ int32_t smax[32];
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const DevParams& p = w.p;
+  // C, D, E1 (signals) || E2 (vehicles)
+  long long qt = 0, active = 0, unfinished = 0;
+  for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
+    if (i < p.S)
+      qt += sig_cde1(w, (int32_t)i);
+    else
+      veh_move(w, (int32_t)(i - p.S), active, unfinished);
+  }
+  qt = block_sum(qt, red);
+  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+  active = block_sum(active, red);
+  if (threadIdx.x == 0 && active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
+  unfinished = block_sum(unfinished, red);
+  if (threadIdx.x == 0 && unfinished)
+    atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
+  if (threadIdx.x == 0) trace_max(w.ctl, 4);
+  grid.sync();
+  // E3
+  for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
+  if (p.siblings_only && (p.algorithm == 2 || p.algorithm == 3)) {
+    grid.sync();
+    for (int64_t u = gtid; u < w.g.n; u += gstride) node_scoped(w, (int32_t)u);
+  }
+  if (threadIdx.x == 0) trace_max(w.ctl, 5);
+  grid.sync();
+  // F + G
+  int32_t m = 0;
+  for (int64_t s = gtid; s < w.g.M; s += gstride)
+    if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
+  m = block_max(m, smax);
+  if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ, m);
+  if (threadIdx.x == 0) trace_max(w.ctl, 6);
+  grid.sync();
+  if (gtid == 0) finalize_step(w);
+}
+
+// ---------------------------------------------------------------------------
 // Batched next-hop query (gmaco_next_node): next_node_{dijkstra,aco,maco}
 // over the current field, one thread per query.
 // ---------------------------------------------------------------------------
@@ -1364,6 +1498,32 @@ static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t -
 // over as many SMs as possible
 constexpr int kTail = 64;
 
+// Dynamic shared memory of the staged grid walker (0 = read from global):
+// weight + tour-cost tables, 16 B per slot, when they fit 96 KiB.
+size_t grid_smem_bytes(const DevWorld& w) {
+  // TMA bulk copies need 16-byte multiples: M is a multiple of 4 (ELL-4), n of 4
+  const size_t bytes = 16 * (size_t)w.g.M + 4 * (size_t)w.g.n;
+  return (w.g.n % 4 == 0 && bytes <= (96u << 10)) ? bytes : 0;
+}
+
+cudaError_t configure_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(k_colony_grid<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_colony_grid<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+}
+
+// Grid size of the cooperative tail: enough 128-thread blocks for the
+// largest stage, capped at what is co-resident on the device.
+int coop_tail_blocks(const DevWorld& w, int device) {
+  int per_sm = 0, sms = 0, coop = 0;
+  if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device) != cudaSuccess || !coop) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop, kTailCoop, 0) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M);
+  const int64_t want = (work + kTailCoop - 1) / kTailCoop;
+  return (int)std::min<int64_t>(want, (int64_t)per_sm * sms);
+}
+
 void colony_shape(int ants, int* threads, int* vpb) {
   int t = ants <= 256 ? 256 : ((ants + 31) / 32) * 32;
   *threads = t;
@@ -1376,8 +1536,20 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 2) goto tail;
   if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
-    const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
-    k_colony_grid<<<blocks_for(V, vpb), threads, 0, st>>>(w);
+    const size_t smem = grid_smem_bytes(w);
+    if (smem) {  // whole weight/cost tables staged per CTA: pack vehicles into 256-thread CTAs
+      const int vpb = 256 / w.p.ants;
+      if (w.p.scratch_mode)
+        k_colony_grid<true, true><<<blocks_for(V, vpb), vpb * w.p.ants, smem, st>>>(w);
+      else
+        k_colony_grid<true, false><<<blocks_for(V, vpb), vpb * w.p.ants, smem, st>>>(w);
+    } else {
+      const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
+      if (w.p.scratch_mode)
+        k_colony_grid<false, true><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+      else
+        k_colony_grid<false, false><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+    }
   } else if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
     // one vehicle's colony per block when it fills whole warps (no block
     // barrier couples different vehicles' walk lengths), else packed
@@ -1410,6 +1582,19 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 1) return cudaGetLastError();
 tail:
+  if (r.coop_blocks > 0 && !w.p.need_positions) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(r.coop_blocks);
+    lc.blockDim = dim3(kTailCoop);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, k_tail_coop, w);
+  }
   if (S > 0) k_signals<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
   k_move<<<blocks_for(V, kTail), kTail, 0, st>>>(w);
   if (S > 0) k_e3<<<blocks_for(S, kTail), kTail, 0, st>>>(w);

@@ -15,6 +15,7 @@ struct StepResources {
   size_t scan_temp_bytes = 0;
   bool capturing = false;
   int part = 0;  // 0 whole step, 1 stage-B walk only, 2 stages C..G only
+  int coop_blocks = 0;  // >0: stages C..G as one cooperative launch of this many blocks
 };
 
 // Enqueues one engine step (stages B..G) on `st`.  Optional events bracket
@@ -22,6 +23,8 @@ struct StepResources {
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end);
 size_t scan_temp_bytes(int V);
+cudaError_t configure_kernels();
+int coop_tail_blocks(const DevWorld& w, int device);
 void colony_shape(int ants, int* threads, int* vpb);
 cudaError_t launch_next_node(const DevWorld& w, int algorithm, int count, const int32_t* cur,
                              const int32_t* dst, const uint64_t* entity, const uint64_t* stepk, int64_t n_t,

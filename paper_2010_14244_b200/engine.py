@@ -45,6 +45,7 @@ SIGNATURES = {
     "gmaco_last_timing": (C.c_int, C.c_void_p, P(f64), P(f64), P(i64)),
     "gmaco_set_timing": (C.c_int, C.c_void_p, i32),
     "gmaco_bench_steps": (C.c_int, C.c_void_p, i32, i64, P(f64), P(f64)),
+    "gmaco_debug_trace": (C.c_int, C.c_void_p, i32, P(u64)),
     "gmaco_last_error": (C.c_char_p, C.c_void_p),
     "gmaco_destroy": (None, C.c_void_p),
 }
@@ -204,6 +205,12 @@ class Engine:
         step = np.zeros(steps, dtype=np.float64)
         self._check(self.L.gmaco_bench_steps(self.h, steps, flush_bytes, abi.ptr(walk, f64), abi.ptr(step, f64)))
         return walk, step
+
+    def debug_trace(self, steps: int = 1) -> np.ndarray:
+        """Stage timestamps (ns) of the last of `steps` steps (DevCtl::trace)."""
+        out = np.zeros(8, dtype=np.uint64)
+        self._check(self.L.gmaco_debug_trace(self.h, steps, abi.ptr(out, u64)))
+        return out
 
     def last_timing(self):
         a, b, n = f64(), f64(), i64()
