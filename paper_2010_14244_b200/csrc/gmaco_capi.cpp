@@ -463,12 +463,6 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     if (g.out_ptr[u + 1] - g.out_ptr[u] > kMaxDegree)
       throw ValidationError(fmt("node %d out-degree exceeds the engine bound of %d", u, kMaxDegree));
 
-  int dev_count = 0;
-  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
-    throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
-  CK(cudaSetDevice(h->device));
-  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  CK(configure_kernels());
   DevBuffers& B = h->buf;
   DevWorld& w = h->w;
 
@@ -540,12 +534,19 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   } else {
     throw ValidationError(fmt("unknown distance kind %d", dd->kind));
   }
-  if (!table.empty()) w.d.table = B.upload(table);
-  if (!slot_of.empty()) w.d.slot_of = B.upload(slot_of);
-
   // ---- spawn (host, engine.cpp:71-114) -------------------------------------
   Spawned sp = spawn(c, g, dh, targets);
   const int32_t V = c.vehicle_count;
+  // all host-side validation is done: from here on the device is required
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CK(configure_kernels());
+  if (!table.empty()) w.d.table = B.upload(table);
+  if (!slot_of.empty()) w.d.slot_of = B.upload(slot_of);
+
 
   // ---- graph in slot order: ELL rows of width 4/8 when the out-degree allows
   // (one aligned vector load per row), plain CSR otherwise ------------------
