@@ -21,6 +21,7 @@ from paper_2010_14244_b200 import abi
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "libgmaco_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libmacosim_ref.so")
+BRIDGE_SO = os.path.join(HERE, "_ref", "libmacosim_bridge.so")
 REFERENCE_SRC = "/root/reference/proj"
 
 P = C.POINTER
@@ -31,7 +32,7 @@ def build(force: bool = False) -> None:
     """Builds the port, and the reference library when its sources exist."""
     targets = ["port"]
     if os.path.isdir(REFERENCE_SRC):
-        targets.append("ref")
+        targets += ["ref", "bridge"]
     if force or not os.path.exists(PORT_SO) or "ref" in targets:
         subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
