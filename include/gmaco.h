@@ -211,6 +211,19 @@ int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist,
 int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id);
 int gmaco_nccl_unique_id(void* out128);
 
+/* Host-mediated sharding (tests, or a caller with its own transport): this
+ * engine plans vehicles [lo, hi) only.  Per step: gmaco_step_split(h, 1)
+ * (stage B over the shard); gmaco_exchange_export (the shard's decision
+ * records [hi-lo] — edge id taken, -1 none, -2 retired — and its best-tour
+ * deposits per edge id [edge_count]); combine across shards (concatenate
+ * the records in vehicle order, sum the deposits); gmaco_exchange_import
+ * ([vehicle_count] records, [edge_count] deposit sums); then
+ * gmaco_step_split(h, 2) (apply the remote decisions, stages C..G). */
+int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi);
+int gmaco_step_split(gmaco_engine* h, int32_t part);
+int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits);
+int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64_t* deposits);
+
 /* Executes up to `steps` engine steps (sequential_step, engine.cpp:352-400),
  * stopping early once finished() (engine.cpp:146-152) holds.  `executed`
  * (may be NULL) receives the number of steps run. */

@@ -460,7 +460,8 @@ struct og_world {
   /* step scratch */
   ivec dec_vid, dec_edge, completions, enq_vid;
   gmaco_counters ctr;
-  int32_t vlo, vhi; /* planning range (sharded emulation) */
+  int32_t vlo, vhi; /* planning range (sharded protocol) */
+  int32_t* dec_rec; /* this step's decision per vehicle: edge, -1 none, -2 retired */
 };
 
 /* ---- distance service (routing.cpp reads dist.reachable / dist.dist_mm) -- */
@@ -876,6 +877,7 @@ void og_world_destroy(og_world* w) {
   if (w->path) for (int32_t i = 0; i < w->V; ++i) free(w->path[i].a);
   if (w->plan) for (int32_t i = 0; i < w->V; ++i) free(w->plan[i].a);
   free(w->path); free(w->plan); free(w->plan_step); free(w->plan_done); free(w->dep); free(w->occ);
+  free(w->dec_rec);
   free(w->dec_vid.a); free(w->dec_edge.a); free(w->completions.a); free(w->enq_vid.a);
   free(w);
 }
@@ -982,6 +984,7 @@ og_world* og_world_create(const gmaco_graph_desc* gd, const gmaco_distance_desc*
   ALLOC(w->depart, V); ALLOC(w->arrive, V); ALLOC(w->latency_debt, V); ALLOC(w->driving, V);
   ALLOC(w->queued, V); ALLOC(w->lat_steps, V); ALLOC(w->path_len_mm, V); ALLOC(w->state, V);
   ALLOC(w->path, V); ALLOC(w->plan, V); ALLOC(w->plan_step, V); ALLOC(w->plan_done, V);
+  ALLOC(w->dec_rec, V);
   for (int32_t i = 0; i < V; ++i) {
     w->at_node[i] = -1; w->on_edge[i] = -1; w->queued_phase[i] = -1; w->arrive[i] = -1;
     w->state[i] = GMACO_PENDING;
@@ -1045,6 +1048,7 @@ static void decide(og_world* w, int32_t vid) { /* engine.cpp:175-217 */
 static void colony_plan(og_world* w, int32_t vid) {
   activate(w, vid);
   if (vid < w->vlo || vid >= w->vhi) return;
+  w->dec_rec[vid] = -1;
   const gmaco_colony_params* cp = &w->cfg.colony;
   int32_t start = -1;
   const int deciding = w->state[vid] == GMACO_AT_NODE;
@@ -1067,7 +1071,10 @@ static void colony_plan(og_world* w, int32_t vid) {
     w->plan[vid].n = 0;
     w->plan_step[vid] = w->step;
     w->plan_done[vid] = 0;
-    if (deciding) w->state[vid] = GMACO_RETIRED;
+    if (deciding) {
+      w->state[vid] = GMACO_RETIRED;
+      w->dec_rec[vid] = -2;
+    }
     return;
   }
   const int32_t max_hops = cp->max_hops > 0 ? cp->max_hops : w->g.n - 1;
@@ -1079,7 +1086,18 @@ static void colony_plan(og_world* w, int32_t vid) {
   w->plan_step[vid] = w->step;
   w->plan_done[vid] = pl->n > 0 && w->g.to[pl->a[pl->n - 1]] == w->dest[vid];
   w->ctr.vehicle_routes++;
-  if (deciding) take_edge(w, vid, pl->a[0], 0);
+  if (w->plan_done[vid] && w->cfg.colony.deposit == GMACO_DEPOSIT_BEST_TOUR) {
+    /* best-tour deposit: deposit_amount(tour length) per tour edge, summed
+     * exactly per edge; applied (sum-then-clamp) in stage F */
+    int64_t len = 0;
+    for (int32_t i = 0; i < pl->n; ++i) len += w->g.len[pl->a[i]];
+    const int64_t amount = og_deposit_amount(len, &w->cfg.pheromone);
+    for (int32_t i = 0; i < pl->n; ++i) w->dep[pl->a[i]] += amount;
+  }
+  if (deciding) {
+    take_edge(w, vid, pl->a[0], 0);
+    w->dec_rec[vid] = pl->a[0];
+  }
 }
 
 static void assign(og_world* w, int32_t s) { /* engine.cpp:223-239 */
@@ -1207,14 +1225,6 @@ static void pheromone_commit(og_world* w) { /* engine.cpp:326-350, parallel.cpp:
     /* best-tour deposit: every planned tour that reaches its destination adds
      * deposit_amount(tour length) to its edges; sum-then-clamp is exact. */
     const int64_t hi = max_u(p);
-    for (int32_t vid = w->vlo; vid < w->vhi; ++vid) {
-      const ivec* pl = &w->plan[vid];
-      if (w->plan_step[vid] != w->step || !w->plan_done[vid] || pl->n == 0) continue;
-      int64_t len = 0;
-      for (int32_t i = 0; i < pl->n; ++i) len += w->g.len[pl->a[i]];
-      const int64_t amount = og_deposit_amount(len, p);
-      for (int32_t i = 0; i < pl->n; ++i) w->dep[pl->a[i]] += amount;
-    }
     for (int32_t e = 0; e < w->g.m; ++e) {
       if (w->dep[e]) w->tau[e] = i64min(w->tau[e] + w->dep[e], hi);
       w->dep[e] = 0;
@@ -1247,7 +1257,7 @@ static void evaporate(og_world* w) {
  * (the reference refreshes after G); neither F nor G reads it and the
  * refresh reads no pheromone, so the order is immaterial except that the
  * colony congestion term sees this step's occupancy. */
-static void step(og_world* w) {
+static void step_part1(og_world* w) {
   w->dec_vid.n = 0; w->dec_edge.n = 0; w->completions.n = 0; w->enq_vid.n = 0;
   w->active = count_active(w);
   /* B */
@@ -1255,6 +1265,21 @@ static void step(og_world* w) {
     for (int32_t vid = 0; vid < w->V; ++vid) colony_plan(w, vid);
   else
     for (int32_t vid = 0; vid < w->V; ++vid) decide(w, vid);
+}
+
+/* Sharded protocol: apply the other shards' decision records. */
+static void apply_remote(og_world* w) {
+  if (w->vlo == 0 && w->vhi == w->V) return;
+  for (int32_t vid = 0; vid < w->V; ++vid) {
+    if (vid >= w->vlo && vid < w->vhi) continue;
+    const int32_t rec = w->dec_rec[vid];
+    if (rec >= 0) take_edge(w, vid, rec, 0);
+    else if (rec == -2) w->state[vid] = GMACO_RETIRED;
+  }
+}
+
+static void step_part2(og_world* w) {
+  apply_remote(w);
   /* C */
   int64_t qt = 0;
   for (int64_t k = 0; k < (int64_t)w->S * GMACO_PHASES; ++k) qt += w->q[k].size;
@@ -1278,6 +1303,11 @@ static void step(og_world* w) {
   evaporate(w);
   refresh_edge_terms(w);
   w->step++;
+}
+
+static void step(og_world* w) {
+  step_part1(w);
+  step_part2(w);
 }
 
 int og_world_finished(og_world* w) { /* engine.cpp:146-152 */
@@ -1429,5 +1459,26 @@ int og_world_set_vehicle_range(og_world* w, int32_t lo, int32_t hi) {
   if (lo < 0 || hi > w->V || lo > hi) return 1;
   w->vlo = lo;
   w->vhi = hi;
+  return 0;
+}
+
+/* ---- sharded protocol (multi-GPU exchange, host-mediated) ---------------- */
+int og_world_step_part(og_world* w, int32_t part) {
+  if (og_world_finished(w)) return 0;
+  if (part == 1) step_part1(w);
+  else step_part2(w);
+  return 1;
+}
+
+int og_world_exchange_export(og_world* w, int32_t* decisions, int64_t* deposits) {
+  if (decisions)
+    for (int32_t vid = w->vlo; vid < w->vhi; ++vid) decisions[vid - w->vlo] = w->dec_rec[vid];
+  if (deposits) memcpy(deposits, w->dep, sizeof(int64_t) * (size_t)w->g.m);
+  return 0;
+}
+
+int og_world_exchange_import(og_world* w, const int32_t* decisions, const int64_t* deposits) {
+  if (decisions) memcpy(w->dec_rec, decisions, sizeof(int32_t) * (size_t)w->V);
+  if (deposits) memcpy(w->dep, deposits, sizeof(int64_t) * (size_t)w->g.m);
   return 0;
 }

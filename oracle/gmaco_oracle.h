@@ -67,9 +67,14 @@ int og_world_counters(og_world* w, gmaco_counters* c);
 int og_world_next_node(og_world* w, int algorithm, int32_t count, const int32_t* current,
                        const int32_t* dest, const uint64_t* entity, const uint64_t* step, int64_t n_t,
                        int32_t* out_next, int32_t* out_via, uint8_t* out_dev);
-/* Sharded-execution hooks (multi-rank protocol tests): restrict colony
- * planning / decisions to vehicles [lo, hi). */
+/* Sharded protocol (the multi-GPU exchange, host-mediated): plan only
+ * vehicles [lo, hi); per step part 1 (stage B over the shard), export the
+ * shard's decision records (edge, -1, -2) and deposits, import everyone's,
+ * part 2 (apply remote decisions, stages C..G). */
 int og_world_set_vehicle_range(og_world* w, int32_t lo, int32_t hi);
+int og_world_step_part(og_world* w, int32_t part);
+int og_world_exchange_export(og_world* w, int32_t* decisions, int64_t* deposits);
+int og_world_exchange_import(og_world* w, const int32_t* decisions, const int64_t* deposits);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,9 @@ def port_lib():
         _sig(L, "og_world_next_node", C.c_int, C.c_void_p, C.c_int, i32, P(i32), P(i32), P(u64),
              P(u64), i64, P(i32), P(i32), P(u8))
         _sig(L, "og_world_set_vehicle_range", C.c_int, C.c_void_p, i32, i32)
+        _sig(L, "og_world_step_part", C.c_int, C.c_void_p, i32)
+        _sig(L, "og_world_exchange_export", C.c_int, C.c_void_p, P(i32), P(i64))
+        _sig(L, "og_world_exchange_import", C.c_int, C.c_void_p, P(i32), P(i64))
         _port = L
     return _port
 
@@ -275,8 +278,24 @@ class PortWorld(_WorldBase):
         self.L.og_world_counters(self.h, C.byref(c))
         return c
 
-    def set_vehicle_range(self, lo, hi):
-        self.L.og_world_set_vehicle_range(self.h, lo, hi)
+    def set_shard(self, lo, hi):
+        self.shard = (lo, hi)
+        assert self.L.og_world_set_vehicle_range(self.h, lo, hi) == 0
+
+    def step_split(self, part):
+        return self.L.og_world_step_part(self.h, part)
+
+    def exchange_export(self):
+        lo, hi = self.shard
+        dec = np.zeros(max(hi - lo, 1), dtype=np.int32)
+        dep = np.zeros(self.m, dtype=np.int64)
+        self.L.og_world_exchange_export(self.h, abi.ptr(dec, i32), abi.ptr(dep, i64))
+        return dec[: hi - lo], dep
+
+    def exchange_import(self, decisions, deposits):
+        d = np.ascontiguousarray(decisions, dtype=np.int32)
+        p = np.ascontiguousarray(deposits, dtype=np.int64)
+        self.L.og_world_exchange_import(self.h, abi.ptr(d, i32), abi.ptr(p, i64))
 
 
 class RefWorld(_WorldBase):

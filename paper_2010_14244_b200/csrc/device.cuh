@@ -70,6 +70,9 @@ struct DevParams {
   int32_t need_positions;  // MACO network-wide fold
   int32_t prefetch;        // bulk-prefetch the step's state into L2 at the start of stage B
   uint32_t rk[20];         // Philox4x32-10 round keys of `seed` (host key schedule)
+  // vehicle sharding (multi-GPU): this rank plans vehicles [shard_lo, shard_hi);
+  // the others' decisions arrive through the exchange (k_apply_remote)
+  int32_t shard_lo, shard_hi, sharded;
   int32_t record_paths;
 };
 
@@ -113,6 +116,7 @@ struct DevVehicles {
   int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
   int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)
   int32_t* plan_ant;            // winning ant per vehicle (scratch mode)
+  int32_t* dec_rec;             // [V_pad] this step's decision per vehicle: slot, -1 none, -2 retired
   int64_t* plan_step;
   uint8_t* plan_done;
 };

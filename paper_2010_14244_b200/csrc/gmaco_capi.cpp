@@ -27,6 +27,7 @@
 #include "device.cuh"
 #include "gmaco.h"
 #include "kernels.h"
+#include "nccl.h"
 
 namespace gmaco {
 namespace {
@@ -282,6 +283,9 @@ struct gmaco_engine {
   int64_t last_walk_launches = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   int64_t wall_ms = 0;
+  // multi-GPU
+  int32_t rank = 0, world = 1, shard_pad = 0;
+  ncclComm_t comm = nullptr;
 
   ~gmaco_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -295,6 +299,15 @@ struct gmaco_engine {
     if (ctl_host) cudaFreeHost(ctl_host);
     if (stop_host) cudaFreeHost(stop_host);
     if (stream) cudaStreamDestroy(stream);
+    destroy_comm();
+  }
+  void destroy_comm();
+  void reset_graphs() {
+    for (auto* ge : {&graph_big, &graph_one, &tgraph_big, &tgraph_one, &graph_walk, &graph_tail})
+      if (*ge) {
+        cudaGraphExecDestroy(*ge);
+        *ge = nullptr;
+      }
   }
 };
 
@@ -662,6 +675,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
   p.prefetch = 1;
+  p.shard_lo = 0;
+  p.shard_hi = V;
+  p.sharded = 0;
   for (int r = 0; r < 10; ++r) {  // Philox4x32-10 key schedule of the seed
     p.rk[2 * r] = (uint32_t)c.seed + (uint32_t)r * 0x9E3779B9u;
     p.rk[2 * r + 1] = (uint32_t)(c.seed >> 32) + (uint32_t)r * 0xBB67AE85u;
@@ -765,6 +781,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
   dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
   dv.plan_ant = B.filled<int32_t>(V, 0);
+  dv.dec_rec = B.filled<int32_t>(V, -1);
   dv.plan_n = B.filled<int32_t>(V, 0);
   dv.plan_step = B.filled<int64_t>(V, -1);
   dv.plan_done = B.filled<uint8_t>(V, 0);
@@ -935,7 +952,80 @@ void scatter_slots(const gmaco_engine* h, const std::vector<T>& by_slot, T* by_e
     if (h->slot_edge[s] >= 0) by_edge[h->slot_edge[s]] = by_slot[s];
 }
 
+// ---- NCCL (dlopen'ed: the library has no hard NCCL dependency) -------------
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.lib) {
+    void* l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) l = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) throw std::runtime_error("NCCL runtime (libnccl.so.2) not found");
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(l, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(l, "ncclCommInitRank"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(l, "ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(l, "ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(l, "ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(l, "ncclGetErrorString"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.CommDestroy)
+      throw std::runtime_error("NCCL runtime lacks required symbols");
+    api.lib = l;
+  }
+  return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string("NCCL error in ") + what + ": " +
+                             (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
+}
+
+// Exchange of one step (enqueued between stage B and the rest, captured in
+// the step graph): every rank's decision records -> all ranks (allgather of
+// the padded shards), best-tour deposits summed (exact int64 allreduce).
+cudaError_t nccl_exchange(void* ctx, cudaStream_t st) {
+  auto* h = static_cast<gmaco_engine*>(ctx);
+  const DevWorld& w = h->w;
+  const size_t P = h->shard_pad;
+  if (nccl().AllGather(w.v.dec_rec + (size_t)h->rank * P, w.v.dec_rec, P, ncclInt32, h->comm, st) != ncclSuccess)
+    return cudaErrorUnknown;
+  if (w.p.deposit == GMACO_DEPOSIT_BEST_TOUR &&
+      nccl().AllReduce(w.dep, w.dep, (size_t)w.g.M, ncclInt64, ncclSum, h->comm, st) != ncclSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+
+void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
+  DevWorld& w = h->w;
+  if (w.p.algorithm != GMACO_COLONY) throw ValidationError("sharding: only the colony algorithm shards vehicles");
+  if (lo < 0 || hi > w.p.V || lo > hi) throw ValidationError("sharding: invalid vehicle range");
+  if (pad_total > w.p.V) {  // allgather layout: world * shard_pad records
+    int32_t* d = h->buf.filled<int32_t>(pad_total, -1);
+    w.v.dec_rec = d;
+  }
+  w.p.shard_lo = lo;
+  w.p.shard_hi = hi;
+  w.p.sharded = 1;
+  h->reset_graphs();
+}
+
 }  // namespace
+
+void gmaco_engine::destroy_comm() {
+  if (comm) {
+    nccl().CommDestroy(comm);
+    comm = nullptr;
+  }
+}
 
 // ============================================================================
 // C ABI
@@ -943,6 +1033,97 @@ void scatter_slots(const gmaco_engine* h, const std::vector<T>& by_slot, T* by_e
 extern "C" {
 
 int32_t gmaco_abi_version(void) { return GMACO_ABI_VERSION; }
+
+int gmaco_nccl_unique_id(void* out128) {
+  if (!out128) return GMACO_EVALIDATION;
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    nck(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id) {
+  if (!h || !nccl_id || world < 1 || rank < 0 || rank >= world) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const int32_t V = h->w.p.V;
+    const int32_t P = (V + world - 1) / world;  // padded contiguous shards (allgather layout)
+    const int32_t lo = std::min(V, rank * P), hi = std::min(V, (rank + 1) * P);
+    set_shard(h, lo, hi, world * P);
+    h->rank = rank;
+    h->world = world;
+    h->shard_pad = P;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    h->destroy_comm();
+    nck(nccl().CommInitRank(&h->comm, world, id, rank), "ncclCommInitRank");
+    h->res.exchange = nccl_exchange;
+    h->res.exchange_ctx = h;
+  });
+}
+
+int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    set_shard(h, lo, hi, 0);
+    h->res.exchange = nullptr;
+  });
+}
+
+int gmaco_step_split(gmaco_engine* h, int32_t part) {
+  if (!h || (part != 1 && part != 2)) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    if (part == 1) {
+      refresh_ctl(h);
+      *h->stop_host = h->ctl_host->step + 1;
+      CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+      if (!h->graph_walk) h->graph_walk = capture_part(h, 1);
+      CK(cudaGraphLaunch(h->graph_walk, h->stream));
+    } else {
+      if (!h->graph_tail) h->graph_tail = capture_part(h, 2);
+      CK(cudaGraphLaunch(h->graph_tail, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    refresh_ctl(h);
+  });
+}
+
+int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits) {
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevWorld& w = h->w;
+    const int32_t lo = w.p.shard_lo, hi = w.p.shard_hi;
+    if (decisions && hi > lo) {  // records at the boundary: edge id, -1 none, -2 retired
+      CK(cudaMemcpy(decisions, w.v.dec_rec + lo, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost));
+      for (int32_t i = 0; i < hi - lo; ++i)
+        if (decisions[i] >= 0) decisions[i] = h->slot_edge[decisions[i]];
+    }
+    if (deposits) scatter_slots(h, download(w.dep, h->M), deposits);
+  });
+}
+
+int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64_t* deposits) {
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevWorld& w = h->w;
+    if (decisions) {
+      std::vector<int32_t> d(decisions, decisions + w.p.V);
+      for (auto& x : d)
+        if (x >= 0) {
+          if (x >= h->g.m) throw ValidationError("exchange_import: invalid edge id");
+          x = h->g.edge_slot[x];
+        }
+      CK(cudaMemcpy(w.v.dec_rec, d.data(), d.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (deposits) {
+      std::vector<int64_t> d(h->M, 0);
+      for (int32_t s = 0; s < h->M; ++s)
+        if (h->slot_edge[s] >= 0) d[s] = deposits[h->slot_edge[s]];
+      CK(cudaMemcpy(w.dep, d.data(), d.size() * 8, cudaMemcpyHostToDevice));
+    }
+  });
+}
 
 int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist, const gmaco_sim_config* cfg,
                  int32_t device, gmaco_engine** out) {

@@ -349,6 +349,7 @@ __device__ __forceinline__ void flush_counters(DevCtl* c, const Sum5& t) {
 __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_t slot, bool deviated,
                                           int32_t from) {
   const DevVehicles& v = w.v;
+  if (w.p.sharded) v.dec_rec[vid] = slot;
   v.state[vid] = kOnEdge;
   v.on_edge[vid] = slot;
   v.progress[vid] = v.overshoot[vid];
@@ -539,8 +540,8 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
   const int ant = threadIdx.x - lv * K;
-  const int32_t vid = blockIdx.x * vpb + lv;
-  const bool live = lv < vpb && vid < w.p.V;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.shard_hi;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
 
@@ -567,6 +568,7 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
     }
     start_s[lv] = start;
     deciding_s[lv] = deciding;
+    if (w.p.sharded) v.dec_rec[vid] = -1;
     best[lv] = ~0ull;
   }
   __syncthreads();
@@ -595,7 +597,10 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
-      if (deciding) v.state[vid] = kRetired;
+      if (deciding) {
+        v.state[vid] = kRetired;
+        if (w.p.sharded) v.dec_rec[vid] = -2;
+      }
     } else {
       int32_t* tour;
       int32_t hops;
@@ -639,8 +644,8 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
   const int ant = threadIdx.x - lv * K;
-  const int32_t vid = blockIdx.x * vpb + lv;
-  const bool live = lv < vpb && vid < w.p.V;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.shard_hi;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
 
@@ -667,6 +672,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
     }
     start_s[lv] = start;
     deciding_s[lv] = deciding;
+    if (w.p.sharded) v.dec_rec[vid] = -1;
     best[lv] = ~0ull;
   }
   __syncthreads();
@@ -804,7 +810,10 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
-      if (deciding) v.state[vid] = kRetired;
+      if (deciding) {
+        v.state[vid] = kRetired;
+        if (w.p.sharded) v.dec_rec[vid] = -2;
+      }
     } else {
       if (w.p.scratch_mode) {
         v.plan_ant[vid] = ant;
@@ -848,8 +857,8 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
   const int ant = threadIdx.x - lv * K;
-  const int32_t vid = blockIdx.x * vpb + lv;
-  const bool live = lv < vpb && vid < w.p.V;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.shard_hi;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
   const double* __restrict__ W = w.weight;
@@ -901,6 +910,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     }
     start_s[lv] = start;
     deciding_s[lv] = deciding;
+    if (w.p.sharded) v.dec_rec[vid] = -1;
     done_s[lv] = 0;
     best[lv] = ~0ull;
   }
@@ -1378,6 +1388,28 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
 }
 
 // ---------------------------------------------------------------------------
+// Sharded runs: apply the other ranks' decisions (after the exchange) to the
+// replicated vehicle state — activation (engine.cpp:177-180), then the
+// decision's bookkeeping (engine.cpp:202-216) or retirement.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vid >= w.p.V || (vid >= w.p.shard_lo && vid < w.p.shard_hi)) return;
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  if (v.state[vid] == kPending && v.depart[vid] == step) {
+    v.state[vid] = kAtNode;
+    v.at_node[vid] = v.origin[vid];
+  }
+  const int32_t rec = v.dec_rec[vid];
+  if (rec >= 0)
+    take_edge(w, vid, rec, false, v.at_node[vid]);
+  else if (rec == -2)
+    v.state[vid] = kRetired;
+}
+
+// ---------------------------------------------------------------------------
 // cooperative tail (one launch for stages C..G): E1 (signals) and E2 (motion)
 // touch disjoint vehicles — queued vs on-edge — and disjoint queue fields
 // (E1: qhead/qnext/qlen, E2: arrival stacks), so they run concurrently;
@@ -1532,7 +1564,8 @@ void colony_shape(int ants, int* threads, int* vpb) {
 
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end) {
-  const int V = w.p.V, S = w.p.S, m = w.g.m, n = w.g.n;
+  const int V = w.p.V, S = w.p.S, n = w.g.n;
+  const int VS = w.p.shard_hi - w.p.shard_lo;  // vehicles planned on this rank
   if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 2) goto tail;
   if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
@@ -1540,28 +1573,28 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
     if (smem) {  // whole weight/cost tables staged per CTA: pack vehicles into 256-thread CTAs
       const int vpb = 256 / w.p.ants;
       if (w.p.scratch_mode)
-        k_colony_grid<true, true><<<blocks_for(V, vpb), vpb * w.p.ants, smem, st>>>(w);
+        k_colony_grid<true, true><<<blocks_for(VS, vpb), vpb * w.p.ants, smem, st>>>(w);
       else
-        k_colony_grid<true, false><<<blocks_for(V, vpb), vpb * w.p.ants, smem, st>>>(w);
+        k_colony_grid<true, false><<<blocks_for(VS, vpb), vpb * w.p.ants, smem, st>>>(w);
     } else {
       const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
       if (w.p.scratch_mode)
-        k_colony_grid<false, true><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+        k_colony_grid<false, true><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
       else
-        k_colony_grid<false, false><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+        k_colony_grid<false, false><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
     }
   } else if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
     // one vehicle's colony per block when it fills whole warps (no block
     // barrier couples different vehicles' walk lengths), else packed
     const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
     if (w.d.kind == 1)
-      k_colony_ell4<1><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+      k_colony_ell4<1><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
     else
-      k_colony_ell4<0><<<blocks_for(V, vpb), threads, 0, st>>>(w);
+      k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
   } else if (w.p.algorithm == 4) {
     int threads, vpb;
     colony_shape(w.p.ants, &threads, &vpb);
-    const unsigned grid = blocks_for(V, vpb);
+    const unsigned grid = blocks_for(VS, vpb);
     if (w.d.kind == 1) {
       if (w.p.progress_filter)
         k_colony<1, true><<<grid, threads, 0, st>>>(w);
@@ -1582,6 +1615,13 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 1) return cudaGetLastError();
 tail:
+  if (w.p.sharded) {
+    if (r.exchange) {  // NCCL: decisions allgather + deposit allreduce (captured with the step)
+      cudaError_t e = r.exchange(r.exchange_ctx, st);
+      if (e != cudaSuccess) return e;
+    }
+    k_apply_remote<<<blocks_for(V, 256), 256, 0, st>>>(w);
+  }
   if (r.coop_blocks > 0 && !w.p.need_positions) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(r.coop_blocks);

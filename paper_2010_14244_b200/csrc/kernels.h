@@ -16,6 +16,10 @@ struct StepResources {
   bool capturing = false;
   int part = 0;  // 0 whole step, 1 stage-B walk only, 2 stages C..G only
   int coop_blocks = 0;  // >0: stages C..G as one cooperative launch of this many blocks
+  // sharded runs: enqueues the decision / deposit exchange between stage B
+  // and the rest of the step (NCCL); null for host-mediated exchange
+  cudaError_t (*exchange)(void* ctx, cudaStream_t st) = nullptr;
+  void* exchange_ctx = nullptr;
 };
 
 // Enqueues one engine step (stages B..G) on `st`.  Optional events bracket

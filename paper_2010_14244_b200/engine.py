@@ -46,6 +46,10 @@ SIGNATURES = {
     "gmaco_set_timing": (C.c_int, C.c_void_p, i32),
     "gmaco_bench_steps": (C.c_int, C.c_void_p, i32, i64, P(f64), P(f64)),
     "gmaco_debug_trace": (C.c_int, C.c_void_p, i32, P(u64)),
+    "gmaco_set_shard": (C.c_int, C.c_void_p, i32, i32),
+    "gmaco_step_split": (C.c_int, C.c_void_p, i32),
+    "gmaco_exchange_export": (C.c_int, C.c_void_p, P(i32), P(i64)),
+    "gmaco_exchange_import": (C.c_int, C.c_void_p, P(i32), P(i64)),
     "gmaco_last_error": (C.c_char_p, C.c_void_p),
     "gmaco_destroy": (None, C.c_void_p),
 }
@@ -211,6 +215,30 @@ class Engine:
         out = np.zeros(8, dtype=np.uint64)
         self._check(self.L.gmaco_debug_trace(self.h, steps, abi.ptr(out, u64)))
         return out
+
+    # -- sharding (multi-GPU) -----------------------------------------------------
+    def attach_comm(self, rank: int, world: int, nccl_id: bytes):
+        buf = C.create_string_buffer(nccl_id, 128)
+        self._check(self.L.gmaco_attach_comm(self.h, rank, world, buf))
+
+    def set_shard(self, lo: int, hi: int):
+        self.shard = (lo, hi)
+        self._check(self.L.gmaco_set_shard(self.h, lo, hi))
+
+    def step_split(self, part: int):
+        self._check(self.L.gmaco_step_split(self.h, part))
+
+    def exchange_export(self):
+        lo, hi = self.shard
+        dec = np.zeros(max(hi - lo, 1), dtype=np.int32)
+        dep = np.zeros(self.m, dtype=np.int64)
+        self._check(self.L.gmaco_exchange_export(self.h, abi.ptr(dec, i32), abi.ptr(dep, i64)))
+        return dec[: hi - lo], dep
+
+    def exchange_import(self, decisions, deposits):
+        d = np.ascontiguousarray(decisions, dtype=np.int32)
+        p = np.ascontiguousarray(deposits, dtype=np.int64)
+        self._check(self.L.gmaco_exchange_import(self.h, abi.ptr(d, i32), abi.ptr(p, i64)))
 
     def last_timing(self):
         a, b, n = f64(), f64(), i64()

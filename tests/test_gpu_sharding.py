@@ -1,0 +1,86 @@
+"""Sharded colonies on the device: engines that each plan one vehicle shard
+and exchange decision records + deposits must reproduce the unsharded
+world bit for bit — through the host-mediated exchange (several engines on
+one GPU, stepping in lockstep, so no kernel waits on another) and through
+the engine's own NCCL exchange (world size 1 on the single available GPU)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2010_14244_b200 import abi, networks, sharding
+from paper_2010_14244_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+
+def world(V=301, ants=16, rows=12):
+    net = networks.grid(rows, rows, signals="all")
+    cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive",
+                                                   vehicle_count=V, seed=5, max_steps=80), ants=ants)
+    return net, cfg
+
+
+def same(a, b):
+    va, vb = a.vehicles(), b.vehicles()
+    for f in abi.VEHICLE_FIELDS:
+        if not np.array_equal(va[f], vb[f]):
+            return f
+    sa, sb = a.signals(), b.signals()
+    for f in sa:
+        if not np.array_equal(sa[f], sb[f]):
+            return f
+    if not np.array_equal(a.pheromone(), b.pheromone()):
+        return "pheromone"
+    if not np.array_equal(a.occupancy(), b.occupancy()):
+        return "occupancy"
+    return None
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_host_mediated_shards_equal_unsharded(nshards):
+    net, cfg = world()
+    single = Engine(net, cfg, net.grid_distance())
+    shards = []
+    for r in range(nshards):
+        e = Engine(net, cfg, net.grid_distance())
+        e.set_shard(*sharding.shard_bounds(cfg.vehicle_count, nshards, r))
+        shards.append(e)
+    step = sharding.local_transport(shards)
+    for k in range(10):
+        step()
+        single.step(1)
+        for e in shards:
+            assert same(e, single) is None, (k, same(e, single))
+    assert sum(e.counters().ant_steps for e in shards) == single.counters().ant_steps
+
+
+def test_mixed_engine_and_oracle_shards():
+    """A GPU shard and an oracle shard exchanging records (edge ids at the
+    boundary) still equal the unsharded oracle world."""
+    net, cfg = world(V=200)
+    cpu_single = O.PortWorld(net, cfg, net.grid_distance())
+    g = Engine(net, cfg, net.grid_distance())
+    g.set_shard(*sharding.shard_bounds(200, 2, 0))
+    c = O.PortWorld(net, cfg, net.grid_distance())
+    c.set_shard(*sharding.shard_bounds(200, 2, 1))
+    step = sharding.local_transport([g, c])
+    for _ in range(8):
+        step()
+        cpu_single.step(1)
+    assert same(g, cpu_single) is None
+    assert same(c, cpu_single) is None
+
+
+def test_nccl_exchange_world1_equals_unsharded():
+    from paper_2010_14244_b200 import engine
+    import ctypes as C
+    net, cfg = world(V=1000, ants=64, rows=32)
+    uid = C.create_string_buffer(128)
+    assert engine.load().gmaco_nccl_unique_id(uid) == 0
+    e = Engine(net, cfg, net.grid_distance())
+    e.attach_comm(0, 1, uid.raw)
+    single = Engine(net, cfg, net.grid_distance())
+    e.step(6)
+    single.step(6)
+    assert same(e, single) is None
+    assert e.counters().ant_steps == single.counters().ant_steps
