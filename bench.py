@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--force-comm", action="store_true",
+                    help="attach the NCCL exchange even at one rank (exercises the multi-GPU path)")
     return ap.parse_args()
 
 
@@ -66,14 +68,15 @@ def workload_config(seed: int, max_steps: int, vehicles: int = VEHICLES):
 
 def config_block(args, world):
     return {
-        "workload": "C2: 32x32 grid, signals at every intersection, 1000 vehicles/GPU, 64 ants/colony, "
+        "workload": "C2: 32x32 grid, signals at every intersection, 1000 vehicles per GPU, 64 ants/colony, "
                     "preemptive signals, congestion-modified pheromone, one colony iteration per step",
         "network": f"grid {GRID}x{GRID}, 200 m edges, 3 lanes, {GRID * GRID} signals",
         "vehicles_per_gpu": VEHICLES,
         "ants_per_colony": ANTS,
         "iterations_timed": args.steps,
         "l2": "flushed (512 MiB write) between timed iterations; working set ~1 MB is L2-resident",
-        "parallelism": f"vehicle-sharded replicas x{world}" if world > 1 else "1 GPU",
+        "parallelism": (f"one world of {VEHICLES * world} vehicles sharded over {world} GPUs (NCCL allgather of "
+                        "decisions + int64 allreduce of deposits per step)") if world > 1 else "1 GPU",
     }
 
 
@@ -131,15 +134,6 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback (B200_PROFILING.md)"
-
-
-def algorithmic_bytes(c, grid_closed_form=True):
-    """Algorithmic bytes of the walk kernel: per ant-step
-    8 B row descriptor + 4 B per scanned out-edge (column) + 8 B per dense
-    distance lookup (0 with the grid closed form) + 8 B weight per candidate
-    + 8 B tour cost of the chosen edge."""
-    dist = 0 if grid_closed_form else 8 * c.degree_sum
-    return 8 * c.ant_steps + 4 * c.degree_sum + dist + 8 * c.candidates + 8 * c.ant_steps
 
 
 # ----------------------------------------------------------------------------
@@ -238,64 +232,83 @@ def cpu_baseline(seconds):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
-def run_ours(args, rank, world, local):
-    import torch
-    from paper_2010_14244_b200 import networks
+def make_engine(net, vehicles, seed, max_steps, local, rank, world, uid):
     from paper_2010_14244_b200.engine import Engine
+    eng = Engine(net, workload_config(seed, max_steps, vehicles), net.grid_distance(), device=local)
+    if uid:  # one world, vehicles sharded over the ranks; NCCL exchange inside the step graph
+        eng.attach_comm(rank, world, uid)
+    return eng
+
+
+def run_ours(args, rank, world, local):
+    import ctypes as C
+
+    import torch
+    from paper_2010_14244_b200 import abi, engine, networks
 
     torch.cuda.set_device(local)
-    pg = None
+    dist = None
+    uid = b""
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        pg = dist
+    if world > 1 or args.force_comm:
+        box = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            rc = engine.load().gmaco_nccl_unique_id(buf)
+            assert rc == 0, "ncclGetUniqueId failed"
+            box[0] = buf.raw
+        if dist:
+            dist.broadcast_object_list(box, src=0)
+        uid = box[0]
     net = networks.grid(GRID, GRID, signals="all")
+    vehicles = VEHICLES * world  # weak scaling: 1,000 vehicles' colonies per GPU
     max_steps = args.warmup + args.steps + 1
 
     # ---- device-resident throughput (value) ---------------------------------
     # K back-to-back iterations enqueued without host sync, each bracketed by
     # CUDA events on the engine stream; a 512 MiB memset flushes L2 between
     # iterations outside the events.
-    eng = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
+    eng = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)
     eng.step(args.warmup)
     c0 = eng.counters()
     torch.cuda.synchronize()
-    if pg:
-        pg.barrier()
+    if dist:
+        dist.barrier()
     with ClockSampler(local) as clk:
         walk, stepms = eng.bench_steps(args.steps, L2_FLUSH_BYTES)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     c1 = eng.counters()
-    walk_ms, step_ms, launches = float(walk.sum()), float(stepms.sum()), args.steps
+    walk_ms, step_ms = float(walk.sum()), float(stepms.sum())
     ant_steps = c1.ant_steps - c0.ant_steps
     routes = c1.vehicle_routes - c0.vehicle_routes
+    alg_bytes = c1.walk_bytes - c0.walk_bytes
+    kernels = c1.kernels_per_step
 
-    class D:  # counter deltas
-        pass
-    d = D()
-    d.ant_steps = ant_steps
-    d.degree_sum = c1.degree_sum - c0.degree_sum
-    d.candidates = c1.candidates - c0.candidates
-    alg_bytes = algorithmic_bytes(d)
-
-    # chained (no flush, multi-step CUDA graphs) on a fresh world, for reference
-    eng2 = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
+    # chained (no flush, multi-step CUDA graphs), for reference
+    eng2 = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)
     eng2.step(args.warmup)
     s0 = eng2.counters().ant_steps
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     eng2.step(args.steps)
     chained_s = time.perf_counter() - t0
-    chained = (eng2.counters().ant_steps - s0) / chained_s
+    chained_steps = eng2.counters().ant_steps - s0
     eng2.close()
 
     # ---- end to end through the C ABI from host buffers (e2e) ---------------
-    import ctypes as C
-    from paper_2010_14244_b200 import abi
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
-    e = Engine(net, workload_config(1 + rank, max_steps), net.grid_distance(), device=local)
-    h2d = (net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1)  # graph SoA uploaded from host
-    st = np.zeros(VEHICLES, dtype=np.uint8)
-    oe = np.zeros(VEHICLES, dtype=np.int32)
+    e = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)  # H2D of all inputs
+    h2d = net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1 + 0
+    st = np.zeros(vehicles, dtype=np.uint8)
+    oe = np.zeros(vehicles, dtype=np.int32)
     view = abi.VehicleView(state=abi.ptr(st, C.c_uint8), on_edge=abi.ptr(oe, C.c_int32))
     e.step(args.warmup)
     for _ in range(args.steps):
@@ -305,24 +318,25 @@ def run_ours(args, rank, world, local):
     e2e_dt = time.perf_counter() - t0
     e2e_steps = e.counters().ant_steps
     e.close()
-    d2h = VEHICLES * 5
+    d2h = vehicles * 5
 
-    # ---- reduce over ranks ------------------------------------------------------
-    t_dev = step_ms / 1e3
-    vals = torch.tensor([t_dev, e2e_dt, walk_ms], dtype=torch.float64, device="cuda")
-    tot = torch.tensor([ant_steps, routes, e2e_steps], dtype=torch.float64, device="cuda")
-    if pg:
-        pg.all_reduce(vals, op=pg.ReduceOp.MAX)
-        pg.all_reduce(tot, op=pg.ReduceOp.SUM)
-    t_dev, e2e_dt, walk_ms_max = vals.tolist()
-    tot_steps, tot_routes, tot_e2e = tot.tolist()
+    # ---- reduce over ranks (time: max; work: sum) ------------------------------
+    vals = torch.tensor([step_ms / 1e3, e2e_dt, chained_s, walk_ms], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([ant_steps, routes, e2e_steps, chained_steps], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    t_dev, e2e_dt, chained_s, _ = vals.tolist()
+    tot_steps, tot_routes, tot_e2e, tot_chained = tot.tolist()
     if rank != 0:
-        if pg:
-            pg.destroy_process_group()
+        eng.close()
+        if dist:
+            dist.destroy_process_group()
         return
     peak, peak_src = measured_peak()
-    walk_avg_s = (walk_ms / 1e3) / max(launches, 1)
-    achieved = (alg_bytes / max(launches, 1)) / walk_avg_s / 1e9 if walk_avg_s > 0 else 0.0
+    launches = args.steps
+    walk_avg_s = (walk_ms / 1e3) / launches
+    achieved = (alg_bytes / launches) / walk_avg_s / 1e9 if walk_avg_s > 0 else 0.0
     line = {
         "metric": "ant-steps/sec",
         "value": tot_steps / t_dev,
@@ -338,17 +352,19 @@ def run_ours(args, rank, world, local):
         "data": "synthetic",
         "config": config_block(args, world),
         "vehicle_routes_per_sec": tot_routes / t_dev,
-        "ant_steps_per_iteration": tot_steps / args.steps / world,
+        "ant_steps_per_iteration": tot_steps / args.steps,
         "walk_kernel_share": (walk_ms / step_ms) if step_ms else None,
-        "chained_graph_value": chained,
+        "chained_graph_value": tot_chained / chained_s,
         "ms_per_step_p50": float(np.median(stepms)),
         "walk_ms_per_step_p50": float(np.median(walk)),
-        "gpu_launches": int(args.steps * launches_per_step(eng)),
+        "gpu_launches": int(args.steps * kernels),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "k_colony (walk)",
-                     "algorithmic_bytes_per_launch": alg_bytes / max(launches, 1),
-                     "avg_launch_us": walk_avg_s * 1e6},
+                     "kernel": "k_colony_grid (stage-B colony walk)",
+                     "algorithmic_bytes_per_launch": alg_bytes / launches,
+                     "avg_launch_us": walk_avg_s * 1e6,
+                     "note": "C2 is latency-bound (longest dependent walk; L2/SMEM-resident ~1 MB state), "
+                             "see DESIGN.md §7"},
         "e2e": {"value": tot_e2e / e2e_dt, "unit": "ant-steps/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h,
@@ -361,14 +377,8 @@ def run_ours(args, rank, world, local):
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     eng.close()
     print(json.dumps(line))
-    if pg:
-        pg.destroy_process_group()
-
-
-def launches_per_step(eng) -> int:
-    """Kernels enqueued per engine step for this world (kernels.cu launch_step)."""
-    S = eng.signal_count()
-    return 1 + (2 if S > 0 else 0) + 1 + 1
+    if dist:
+        dist.destroy_process_group()
 
 
 def main():

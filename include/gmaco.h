@@ -191,6 +191,8 @@ typedef struct {
   int64_t decisions;       /* engine routing decisions (StepDecision count) */
   int64_t candidates;      /* filtered candidates visited (sum of c) */
   int64_t degree_sum;      /* out-edges scanned (sum of d) */
+  int64_t kernels_per_step; /* engine kernels launched per step (this configuration) */
+  int64_t walk_bytes;      /* algorithmic bytes read by the stage-B walks so far */
 } gmaco_counters;
 
 typedef struct gmaco_engine gmaco_engine;

@@ -137,7 +137,8 @@ class SignalView(C.Structure):
 class Counters(C.Structure):
     _fields_ = [
         ("ant_steps", C.c_int64), ("vehicle_routes", C.c_int64), ("decisions", C.c_int64),
-        ("candidates", C.c_int64), ("degree_sum", C.c_int64),
+        ("candidates", C.c_int64), ("degree_sum", C.c_int64), ("kernels_per_step", C.c_int64),
+        ("walk_bytes", C.c_int64),
     ]
 
 

@@ -1303,6 +1303,17 @@ int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out) {
     out->decisions = c.decisions;
     out->candidates = c.candidates;
     out->degree_sum = c.degree_sum;
+    out->kernels_per_step = kernels_per_step(h->w, h->res);
+    // algorithmic bytes of the walks: the lattice walker reads
+    // the candidate weights and the chosen edge's tour cost; the generic
+    // walkers also read the row descriptor, the columns and (table kinds) one
+    // distance per scanned neighbour
+    const DevWorld& w = h->w;
+    if (w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.algorithm == GMACO_COLONY)
+      out->walk_bytes = 8 * c.candidates + 8 * c.ant_steps;
+    else
+      out->walk_bytes = 8 * c.ant_steps + 4 * c.degree_sum + (w.d.kind == 1 ? 0 : 8 * c.degree_sum) +
+                        8 * c.candidates + 8 * c.ant_steps;
   });
 }
 

@@ -1651,6 +1651,18 @@ tail:
   return cudaGetLastError();
 }
 
+// Engine kernels enqueued per step by launch_step (library kernels such as
+// the CUB scan and NCCL collectives are not counted).
+int kernels_per_step(const DevWorld& w, const StepResources& r) {
+  int k = 1;                 // stage-B walk / decide
+  if (w.p.sharded) k += 1;   // k_apply_remote
+  if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
+  if (w.p.S > 0) k += 2;     // k_signals, k_e3
+  k += 1;                    // k_move
+  if ((w.p.algorithm == 2 || w.p.algorithm == 3) && w.p.siblings_only) k += 1;  // k_scoped
+  return k + 1;              // k_edges
+}
+
 size_t scan_temp_bytes(int V) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int32_t*)nullptr, (int32_t*)nullptr, V);

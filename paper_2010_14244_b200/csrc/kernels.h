@@ -27,6 +27,7 @@ struct StepResources {
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end);
 size_t scan_temp_bytes(int V);
+int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 void colony_shape(int ants, int* threads, int* vpb);
