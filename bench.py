@@ -29,6 +29,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's banner / warnings go to stderr: stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import numpy as np  # noqa: E402
 
@@ -232,7 +235,7 @@ def cpu_baseline(seconds):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
-def make_engine(net, vehicles, seed, max_steps, local, rank, world, uid):
+def make_engine(net, vehicles, seed, max_steps, local, rank, world, uid: bytes):
     from paper_2010_14244_b200.engine import Engine
     eng = Engine(net, workload_config(seed, max_steps, vehicles), net.grid_distance(), device=local)
     if uid:  # one world, vehicles sharded over the ranks; NCCL exchange inside the step graph
@@ -248,11 +251,13 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dist = None
-    uid = b""
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if world > 1 or args.force_comm:
+    def fresh_uid():
+        """A new NCCL unique id from rank 0 (one per communicator: ids are single-use)."""
+        if world == 1 and not args.force_comm:
+            return b""
         box = [None]
         if rank == 0:
             buf = C.create_string_buffer(128)
@@ -261,7 +266,7 @@ def run_ours(args, rank, world, local):
             box[0] = buf.raw
         if dist:
             dist.broadcast_object_list(box, src=0)
-        uid = box[0]
+        return box[0]
     net = networks.grid(GRID, GRID, signals="all")
     vehicles = VEHICLES * world  # weak scaling: 1,000 vehicles' colonies per GPU
     max_steps = args.warmup + args.steps + 1
@@ -270,7 +275,7 @@ def run_ours(args, rank, world, local):
     # K back-to-back iterations enqueued without host sync, each bracketed by
     # CUDA events on the engine stream; a 512 MiB memset flushes L2 between
     # iterations outside the events.
-    eng = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)
+    eng = make_engine(net, vehicles, 1, max_steps, local, rank, world, fresh_uid())
     eng.step(args.warmup)
     c0 = eng.counters()
     torch.cuda.synchronize()
@@ -289,7 +294,7 @@ def run_ours(args, rank, world, local):
     kernels = c1.kernels_per_step
 
     # chained (no flush, multi-step CUDA graphs), for reference
-    eng2 = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)
+    eng2 = make_engine(net, vehicles, 1, max_steps, local, rank, world, fresh_uid())
     eng2.step(args.warmup)
     s0 = eng2.counters().ant_steps
     torch.cuda.synchronize()
@@ -302,6 +307,7 @@ def run_ours(args, rank, world, local):
     eng2.close()
 
     # ---- end to end through the C ABI from host buffers (e2e) ---------------
+    uid = fresh_uid()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()

@@ -73,6 +73,7 @@ struct DevParams {
   // vehicle sharding (multi-GPU): this rank plans vehicles [shard_lo, shard_hi);
   // the others' decisions arrive through the exchange (k_apply_remote)
   int32_t shard_lo, shard_hi, sharded;
+  int32_t no_smem;          // A/B switch: read the walk tables from global memory
   int32_t record_paths;
 };
 

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <queue>
@@ -674,7 +675,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.cong_evap = alg == GMACO_COLONY ? k.congestion_evaporation : 0;
   p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
-  p.prefetch = 1;
+  // debugging / A-B switches (defaults are the production configuration)
+  p.prefetch = std::getenv("GMACO_NO_PREFETCH") ? 0 : 1;
+  p.no_smem = std::getenv("GMACO_NO_SMEM") ? 1 : 0;
   p.shard_lo = 0;
   p.shard_hi = V;
   p.sharded = 0;

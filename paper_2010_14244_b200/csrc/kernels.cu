@@ -316,12 +316,12 @@ __device__ void prefetch_tail_state(const DevWorld& w) {
 
 // Five block-wide sums with a single barrier; valid in thread 0.
 struct Sum5 {
-  long long v[5];
+  long long v[7];  // ant_steps, candidates, degree_sum, routes, decisions, active(next), unfinished
 };
 __device__ __forceinline__ Sum5 block_sum5(Sum5 x, long long (*smem)[32]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < 7; ++k) {
     long long a = x.v[k];
     for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
     if (lane == 0) smem[k][wid] = a;
@@ -329,7 +329,7 @@ __device__ __forceinline__ Sum5 block_sum5(Sum5 x, long long (*smem)[32]) {
   __syncthreads();
   Sum5 r{};
   if (threadIdx.x == 0)
-    for (int k = 0; k < 5; ++k)
+    for (int k = 0; k < 7; ++k)
       for (int i = 0; i < (int)((blockDim.x + 31) >> 5); ++i) r.v[k] += smem[k][i];
   return r;
 }
@@ -343,6 +343,8 @@ __device__ __forceinline__ void flush_counters(DevCtl* c, const Sum5& t) {
     atomicAdd((unsigned long long*)&c->decisions, (unsigned long long)t.v[4]);
     atomicAdd((unsigned long long*)&c->dcount, (unsigned long long)t.v[4]);
   }
+  if (t.v[5]) atomicAdd((unsigned long long*)&c->n_next, (unsigned long long)t.v[5]);
+  if (t.v[6]) atomicAdd((unsigned long long*)&c->unfinished, (unsigned long long)t.v[6]);
 }
 
 // Vehicle takes edge `slot` (engine.cpp:207-216).
@@ -508,6 +510,10 @@ __device__ __forceinline__ WalkOut ant_walk(const DevWorld& w, const Target<DK>&
   return o;
 }
 
+// E2 (motion) of one vehicle; defined with the other per-entity stage bodies.
+// Colony walks run it for each vehicle right after that vehicle's stage B.
+__device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished);
+
 // Winner epilogue: plan bookkeeping, best-tour deposit (exact int64 sums,
 // deposit_amount pheromone.cpp:73-78) and, at a node, the first hop.
 __device__ __forceinline__ void finish_colony(const DevWorld& w, int32_t vid, int32_t start,
@@ -535,7 +541,7 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
-  __shared__ long long red5[5][32];
+  __shared__ long long red5[7][32];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
@@ -545,6 +551,7 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
 
+  long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
@@ -569,6 +576,7 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
     start_s[lv] = start;
     deciding_s[lv] = deciding;
     if (w.p.sharded) v.dec_rec[vid] = -1;
+    if (start < 0) veh_move(w, vid, act, unf);  // E2 now: stage B leaves this vehicle untouched
     best[lv] = ~0ull;
   }
   __syncthreads();
@@ -617,8 +625,9 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
       routes = 1;
       decided = deciding;
     }
+    veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
   }
-  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided, act, unf}}, red5);
   if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
-  __shared__ long long red5[5][32];
+  __shared__ long long red5[7][32];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
@@ -649,6 +658,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
 
+  long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
@@ -673,6 +683,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
     start_s[lv] = start;
     deciding_s[lv] = deciding;
     if (w.p.sharded) v.dec_rec[vid] = -1;
+    if (start < 0) veh_move(w, vid, act, unf);  // E2 now: stage B leaves this vehicle untouched
     best[lv] = ~0ull;
   }
   __syncthreads();
@@ -826,8 +837,9 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
       routes = 1;
       decided = deciding;
     }
+    veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
   }
-  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided, act, unf}}, red5);
   if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
@@ -844,14 +856,17 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 template <bool kSmem, bool kScratch>
 __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
+    if (w.p.prefetch) prefetch_tail_state(w);
+    return;
+  }
   if (threadIdx.x == 0) trace_min(w.ctl, 0);
-  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   constexpr int kMaxVpb = 256;
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
   __shared__ int32_t done_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
-  __shared__ long long red5[5][32];
+  __shared__ long long red5[7][32];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
@@ -887,6 +902,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     Cst = reinterpret_cast<const int64_t*>(dyn_smem + bW);
     sdeg = reinterpret_cast<const int32_t*>(dyn_smem + 2 * bW);
   }
+  long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
@@ -911,6 +927,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     start_s[lv] = start;
     deciding_s[lv] = deciding;
     if (w.p.sharded) v.dec_rec[vid] = -1;
+    if (start < 0) veh_move(w, vid, act, unf);  // E2 now: stage B leaves this vehicle untouched
     done_s[lv] = 0;
     best[lv] = ~0ull;
   }
@@ -1022,9 +1039,10 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       finish_colony(w, vid, start, tour, wh, deciding, step);
       routes = 1;
       decided = deciding;
+      veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
     }
   }
-  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided}}, red5);
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided, act, unf}}, red5);
   if (threadIdx.x == 0) {
     flush_counters(w.ctl, t);
     trace_max(w.ctl, 2);
@@ -1185,35 +1203,50 @@ __device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long lo
 __device__ __forceinline__ void sig_e3(const DevWorld& w, int32_t s) {
   const DevSignals& S = w.s;
   const int64_t now = w.ctl->step + 1;
+  const int k0 = s * kPhases;
+  // one round of independent loads for all 8 queues, then the (rare)
+  // arrival chains, then one round of head lookups for head_wait
+  int32_t chain[kPhases], len[kPhases], head[kPhases];
+#pragma unroll
   for (int ph = 0; ph < kPhases; ++ph) {
-    const int k = s * kPhases + ph;
-    const int32_t chain = S.arr_head[k];
-    int32_t len = S.qlen[k];
-    if (chain >= 0) {
-      S.arr_head[k] = -1;
-      int32_t tail = S.qtail[k];
-      int32_t head = S.qhead[k];
-      int32_t last = -1;
-      for (;;) {  // append chain members in ascending vid (selection; chains are short)
-        int32_t best = INT32_MAX;
-        for (int32_t c = chain; c >= 0; c = w.v.arr_next[c])
-          if (c > last && c < best) best = c;
-        if (best == INT32_MAX) break;
-        w.v.qnext[best] = -1;
-        if (tail < 0)
-          head = best;
-        else
-          w.v.qnext[tail] = best;
-        tail = best;
-        ++len;
-        last = best;
-      }
-      S.qhead[k] = head;
-      S.qtail[k] = tail;
-      S.qlen[k] = len;
-    }
-    S.head_wait[k] = len == 0 ? 0.0 : __dmul_rn((double)(now - w.v.joined[S.qhead[k]]), w.p.dt_s);
+    chain[ph] = S.arr_head[k0 + ph];
+    len[ph] = S.qlen[k0 + ph];
+    head[ph] = S.qhead[k0 + ph];
   }
+#pragma unroll
+  for (int ph = 0; ph < kPhases; ++ph) {
+    if (chain[ph] < 0) continue;
+    const int k = k0 + ph;
+    S.arr_head[k] = -1;
+    int32_t tail = S.qtail[k];
+    int32_t hd = head[ph], n = len[ph];
+    int32_t last = -1;
+    for (;;) {  // append chain members in ascending vid (selection; chains are short)
+      int32_t best = INT32_MAX;
+      for (int32_t c = chain[ph]; c >= 0; c = w.v.arr_next[c])
+        if (c > last && c < best) best = c;
+      if (best == INT32_MAX) break;
+      w.v.qnext[best] = -1;
+      if (tail < 0)
+        hd = best;
+      else
+        w.v.qnext[tail] = best;
+      tail = best;
+      ++n;
+      last = best;
+    }
+    S.qhead[k] = hd;
+    S.qtail[k] = tail;
+    S.qlen[k] = n;
+    head[ph] = hd;
+    len[ph] = n;
+  }
+  int64_t joined[kPhases];
+#pragma unroll
+  for (int ph = 0; ph < kPhases; ++ph) joined[ph] = len[ph] ? w.v.joined[head[ph]] : 0;
+#pragma unroll
+  for (int ph = 0; ph < kPhases; ++ph)
+    S.head_wait[k0 + ph] = len[ph] == 0 ? 0.0 : __dmul_rn((double)(now - joined[ph]), w.p.dt_s);
   const int64_t e = S.el_steps[s] + 1;
   S.el_steps[s] = e;
   S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
@@ -1409,6 +1442,35 @@ __global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
     v.state[vid] = kRetired;
 }
 
+// colony mode: remote vehicles' decisions, then their motion (E2) and the
+// next step's counts, exactly as the walk kernel does for its own shard
+__global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
+  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  long long act = 0, unf = 0;
+  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) {
+    const DevVehicles& v = w.v;
+    const int64_t step = w.ctl->step;
+    if (v.state[vid] == kPending && v.depart[vid] == step) {
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    const int32_t rec = v.dec_rec[vid];
+    if (rec >= 0)
+      take_edge(w, vid, rec, false, v.at_node[vid]);
+    else if (rec == -2)
+      v.state[vid] = kRetired;
+    veh_move(w, vid, act, unf);
+  }
+  act = block_sum(act, red);
+  unf = block_sum(unf, red);
+  if (threadIdx.x == 0) {
+    if (act) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)act);
+    if (unf) atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unf);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // cooperative tail (one launch for stages C..G): E1 (signals) and E2 (motion)
 // touch disjoint vehicles — queued vs on-edge — and disjoint queue fields
@@ -1416,6 +1478,7 @@ __global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
 // grid.sync() orders E3 after E2 and F+G after E3.  Launched with the
 // cooperative attribute, which guarantees co-residency of the grid.
 // ---------------------------------------------------------------------------
+template <bool kFusedMotion>
 __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
   cg::grid_group grid = cg::this_grid();
@@ -1425,6 +1488,31 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const DevParams& p = w.p;
+  if (kFusedMotion) {
+    // colony mode: E2 already ran inside the walk kernel, so one pass per
+    // signal does C, D, E1 (pops the FIFO head) and E3 (appends this step's
+    // arrivals after it) — the reference order for each queue
+    long long qt = 0;
+    for (int64_t s = gtid; s < p.S; s += gstride) {
+      qt += sig_cde1(w, (int32_t)s);
+      sig_e3(w, (int32_t)s);
+    }
+    qt = block_sum(qt, red);
+    if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+    if (threadIdx.x == 0) trace_max(w.ctl, 5);
+    grid.sync();
+    // every slot, ELL padding included: padding slots carry no decisions,
+    // deposits or occupancy and no walk reads them, so skipping the
+    // validity load only shortens the dependent chain
+    int32_t m = 0;
+    for (int64_t s = gtid; s < w.g.M; s += gstride) m = max(m, slot_fg(w, (int32_t)s));
+    m = block_max(m, smax);
+    if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ, m);
+    if (threadIdx.x == 0) trace_max(w.ctl, 6);
+    grid.sync();
+    if (gtid == 0) finalize_step(w);
+    return;
+  }
   // C, D, E1 (signals) || E2 (vehicles)
   long long qt = 0, active = 0, unfinished = 0;
   for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
@@ -1535,7 +1623,7 @@ constexpr int kTail = 64;
 size_t grid_smem_bytes(const DevWorld& w) {
   // TMA bulk copies need 16-byte multiples: M is a multiple of 4 (ELL-4), n of 4
   const size_t bytes = 16 * (size_t)w.g.M + 4 * (size_t)w.g.n;
-  return (w.g.n % 4 == 0 && bytes <= (96u << 10)) ? bytes : 0;
+  return (!w.p.no_smem && w.g.n % 4 == 0 && bytes <= (96u << 10)) ? bytes : 0;
 }
 
 cudaError_t configure_kernels() {
@@ -1549,7 +1637,7 @@ cudaError_t configure_kernels() {
 int coop_tail_blocks(const DevWorld& w, int device) {
   int per_sm = 0, sms = 0, coop = 0;
   if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device) != cudaSuccess || !coop) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop, kTailCoop, 0) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<false>, kTailCoop, 0) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M);
   const int64_t want = (work + kTailCoop - 1) / kTailCoop;
@@ -1573,15 +1661,15 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
     if (smem) {  // whole weight/cost tables staged per CTA: pack vehicles into 256-thread CTAs
       const int vpb = 256 / w.p.ants;
       if (w.p.scratch_mode)
-        k_colony_grid<true, true><<<blocks_for(VS, vpb), vpb * w.p.ants, smem, st>>>(w);
+        k_colony_grid<true, true><<<blocks_for(VS, vpb) + 1, vpb * w.p.ants, smem, st>>>(w);
       else
-        k_colony_grid<true, false><<<blocks_for(VS, vpb), vpb * w.p.ants, smem, st>>>(w);
+        k_colony_grid<true, false><<<blocks_for(VS, vpb) + 1, vpb * w.p.ants, smem, st>>>(w);
     } else {
       const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
       if (w.p.scratch_mode)
-        k_colony_grid<false, true><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
+        k_colony_grid<false, true><<<blocks_for(VS, vpb) + 1, threads, 0, st>>>(w);
       else
-        k_colony_grid<false, false><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
+        k_colony_grid<false, false><<<blocks_for(VS, vpb) + 1, threads, 0, st>>>(w);
     }
   } else if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
     // one vehicle's colony per block when it fills whole warps (no block
@@ -1615,12 +1703,16 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (walk_end) cudaEventRecordWithFlags(walk_end, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 1) return cudaGetLastError();
 tail:
+  const bool fused = w.p.algorithm == 4;  // colony walks run E2 themselves
   if (w.p.sharded) {
     if (r.exchange) {  // NCCL: decisions allgather + deposit allreduce (captured with the step)
       cudaError_t e = r.exchange(r.exchange_ctx, st);
       if (e != cudaSuccess) return e;
     }
-    k_apply_remote<<<blocks_for(V, 256), 256, 0, st>>>(w);
+    if (fused)
+      k_apply_remote_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
+    else
+      k_apply_remote<<<blocks_for(V, 256), 256, 0, st>>>(w);
   }
   if (r.coop_blocks > 0 && !w.p.need_positions) {
     cudaLaunchConfig_t lc = {};
@@ -1633,10 +1725,10 @@ tail:
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, k_tail_coop, w);
+    return fused ? cudaLaunchKernelEx(&lc, k_tail_coop<true>, w) : cudaLaunchKernelEx(&lc, k_tail_coop<false>, w);
   }
   if (S > 0) k_signals<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
-  k_move<<<blocks_for(V, kTail), kTail, 0, st>>>(w);
+  if (!fused) k_move<<<blocks_for(V, kTail), kTail, 0, st>>>(w);
   if (S > 0) k_e3<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
   if (w.p.algorithm == 2 || w.p.algorithm == 3) {
     if (w.p.siblings_only) {
@@ -1658,7 +1750,7 @@ int kernels_per_step(const DevWorld& w, const StepResources& r) {
   if (w.p.sharded) k += 1;   // k_apply_remote
   if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
   if (w.p.S > 0) k += 2;     // k_signals, k_e3
-  k += 1;                    // k_move
+  if (w.p.algorithm != 4) k += 1;  // k_move (colony walks run E2 themselves)
   if ((w.p.algorithm == 2 || w.p.algorithm == 3) && w.p.siblings_only) k += 1;  // k_scoped
   return k + 1;              // k_edges
 }
