@@ -343,6 +343,12 @@ def run_ours(args, rank, world, local):
     launches = args.steps
     walk_avg_s = (walk_ms / 1e3) / launches
     achieved = (alg_bytes / launches) / walk_avg_s / 1e9 if walk_avg_s > 0 else 0.0
+    traffic = None
+    try:  # DRAM bytes per walk launch from the committed ncu capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as f:
+            traffic = json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     line = {
         "metric": "ant-steps/sec",
         "value": tot_steps / t_dev,
@@ -365,7 +371,8 @@ def run_ours(args, rank, world, local):
         "walk_ms_per_step_p50": float(np.median(walk)),
         "gpu_launches": int(args.steps * kernels),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "traffic_source": "profiles/walk_traffic.json (ncu --set full, dram__bytes_read+write)",
                      "kernel": "k_colony_grid (stage-B colony walk)",
                      "algorithmic_bytes_per_launch": alg_bytes / launches,
                      "avg_launch_us": walk_avg_s * 1e6,
