@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
+                    help="BASELINE.json config (c2 = the metric's single-GPU config, the default)")
+    ap.add_argument("--skip-extra", action="store_true", help="skip the chained and e2e legs")
     ap.add_argument("--force-comm", action="store_true",
                     help="attach the NCCL exchange even at one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -69,7 +72,13 @@ def workload_config(seed: int, max_steps: int, vehicles: int = VEHICLES):
     return abi.colony_production(cfg, ants=ANTS)
 
 
-def config_block(args, world):
+def config_block(args, world, vehicles=None):
+    from paper_2010_14244_b200 import workloads
+    if args.config != "c2":
+        return {"workload": f"{args.config.upper()}: {workloads.DESCRIPTIONS[args.config]}",
+                "vehicles_total": vehicles, "iterations_timed": args.steps,
+                "l2": "flushed (512 MiB write) between timed iterations",
+                "parallelism": f"one world sharded over {world} GPUs" if world > 1 else "1 GPU"}
     return {
         "workload": "C2: 32x32 grid, signals at every intersection, 1000 vehicles per GPU, 64 ants/colony, "
                     "preemptive signals, congestion-modified pheromone, one colony iteration per step",
@@ -235,12 +244,26 @@ def cpu_baseline(seconds):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
-def make_engine(net, vehicles, seed, max_steps, local, rank, world, uid: bytes):
+def make_engine(wl, local, rank, world, uid: bytes, max_steps=None):
     from paper_2010_14244_b200.engine import Engine
-    eng = Engine(net, workload_config(seed, max_steps, vehicles), net.grid_distance(), device=local)
+    net, cfg, dist, _keep = wl
+    if max_steps is not None:
+        cfg.max_steps = max_steps
+    eng = Engine(net, cfg, dist, device=local)
     if uid:  # one world, vehicles sharded over the ranks; NCCL exchange inside the step graph
         eng.attach_comm(rank, world, uid)
     return eng
+
+
+def build_workload(args, world):
+    """(net, cfg, dist, keepalive) of --config.  C2 scales weakly (1,000
+    vehicles' colonies per GPU); the larger configs keep their fleet and
+    shard it (strong scaling), as BASELINE.json states them."""
+    from paper_2010_14244_b200 import workloads
+    max_steps = args.warmup + args.steps + 1
+    if args.config == "c2":
+        return workloads.c2(seed=1, max_steps=max_steps, vehicles=VEHICLES * world)
+    return workloads.CONFIGS[args.config](seed=1, max_steps=max_steps)
 
 
 def run_ours(args, rank, world, local):
@@ -267,15 +290,15 @@ def run_ours(args, rank, world, local):
         if dist:
             dist.broadcast_object_list(box, src=0)
         return box[0]
-    net = networks.grid(GRID, GRID, signals="all")
-    vehicles = VEHICLES * world  # weak scaling: 1,000 vehicles' colonies per GPU
-    max_steps = args.warmup + args.steps + 1
+    wl = build_workload(args, world)
+    net, cfg0 = wl[0], wl[1]
+    vehicles = cfg0.vehicle_count
 
     # ---- device-resident throughput (value) ---------------------------------
     # K back-to-back iterations enqueued without host sync, each bracketed by
     # CUDA events on the engine stream; a 512 MiB memset flushes L2 between
     # iterations outside the events.
-    eng = make_engine(net, vehicles, 1, max_steps, local, rank, world, fresh_uid())
+    eng = make_engine(wl, local, rank, world, fresh_uid())
     eng.step(args.warmup)
     c0 = eng.counters()
     torch.cuda.synchronize()
@@ -294,37 +317,42 @@ def run_ours(args, rank, world, local):
     kernels = c1.kernels_per_step
 
     # chained (no flush, multi-step CUDA graphs), for reference
-    eng2 = make_engine(net, vehicles, 1, max_steps, local, rank, world, fresh_uid())
-    eng2.step(args.warmup)
-    s0 = eng2.counters().ant_steps
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    eng2.step(args.steps)
-    chained_s = time.perf_counter() - t0
-    chained_steps = eng2.counters().ant_steps - s0
-    eng2.close()
+    chained_s, chained_steps = 1.0, 0
+    if not args.skip_extra:
+        eng2 = make_engine(wl, local, rank, world, fresh_uid())
+        eng2.step(args.warmup)
+        s0 = eng2.counters().ant_steps
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        eng2.step(args.steps)
+        chained_s = time.perf_counter() - t0
+        chained_steps = eng2.counters().ant_steps - s0
+        eng2.close()
 
     # ---- end to end through the C ABI from host buffers (e2e) ---------------
-    uid = fresh_uid()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    e = make_engine(net, vehicles, 1, max_steps, local, rank, world, uid)  # H2D of all inputs
-    h2d = net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1 + 0
-    st = np.zeros(vehicles, dtype=np.uint8)
-    oe = np.zeros(vehicles, dtype=np.int32)
-    view = abi.VehicleView(state=abi.ptr(st, C.c_uint8), on_edge=abi.ptr(oe, C.c_int32))
-    e.step(args.warmup)
-    for _ in range(args.steps):
-        e.step(1)
-        e._check(e.L.gmaco_get_vehicles(e.h, C.byref(view)))  # the step's decisions back to host
-    res = e.collect()
-    e2e_dt = time.perf_counter() - t0
-    e2e_steps = e.counters().ant_steps
-    e.close()
+    e2e_dt, e2e_steps, completed = 1.0, 0, None
+    h2d = net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1
     d2h = vehicles * 5
+    if not args.skip_extra:
+        uid = fresh_uid()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e = make_engine(wl, local, rank, world, uid)  # H2D of all inputs
+        st = np.zeros(vehicles, dtype=np.uint8)
+        oe = np.zeros(vehicles, dtype=np.int32)
+        view = abi.VehicleView(state=abi.ptr(st, C.c_uint8), on_edge=abi.ptr(oe, C.c_int32))
+        e.step(args.warmup)
+        for _ in range(args.steps):
+            e.step(1)
+            e._check(e.L.gmaco_get_vehicles(e.h, C.byref(view)))  # the step's decisions back to host
+        res = e.collect()
+        e2e_dt = time.perf_counter() - t0
+        e2e_steps = e.counters().ant_steps
+        completed = res[0].completed_count
+        e.close()
 
     # ---- reduce over ranks (time: max; work: sum) ------------------------------
     vals = torch.tensor([step_ms / 1e3, e2e_dt, chained_s, walk_ms], dtype=torch.float64, device="cuda")
@@ -362,7 +390,7 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "f64+int64",
         "data": "synthetic",
-        "config": config_block(args, world),
+        "config": config_block(args, world, vehicles),
         "vehicle_routes_per_sec": tot_routes / t_dev,
         "ant_steps_per_iteration": tot_steps / args.steps,
         "walk_kernel_share": (walk_ms / step_ms) if step_ms else None,
@@ -384,9 +412,9 @@ def run_ours(args, rank, world, local):
                 "includes": "gmaco_create from host arrays (H2D), warmup+timed steps, per-step D2H of "
                             "vehicle states, gmaco_collect"},
         "clocks": clk.summary(),
-        "completed_vehicles_e2e": res[0].completed_count,
+        "completed_vehicles_e2e": completed,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     eng.close()
     print(json.dumps(line))

@@ -269,9 +269,9 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
 int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches);
 int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
 /* Profiling hook: runs `steps` steps and returns the last one's stage
- * timestamps (ns, %globaltimer): walk start/staged/end, tail start, E1||E2,
- * E3 and F+G completion. */
-int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out8);
+ * timestamps (ns, %globaltimer, 12 slots; see DevCtl::trace in
+ * paper_2010_14244_b200/csrc/device.cuh). */
+int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
 /* Benchmark entry point: enqueues `steps` engine steps without host
  * synchronization, each bracketed by CUDA events on the engine stream
  * (walk kernel, whole step), with an L2-flushing memset of flush_bytes

@@ -74,28 +74,39 @@ struct DevParams {
   // the others' decisions arrive through the exchange (k_apply_remote)
   int32_t shard_lo, shard_hi, sharded;
   int32_t no_smem;          // A/B switch: read the walk tables from global memory
+  int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (walks <= 64 hops)
   int32_t record_paths;
 };
 
+// Control block.  The read-mostly step state shares one cache line; every
+// counter that blocks update atomically lives on its own 128-byte line, so
+// the per-block counter flushes of one stage neither serialize against each
+// other in one L2 slice nor stall the next kernel's read of `done`/`step`.
 struct DevCtl {
   int64_t step;        // w.step
   int64_t stop_at;     // host-set step limit for the current launch chunk
   int64_t n_t;         // count_active for the current step (engine.cpp:156-173)
-  int64_t n_next;      // accumulated for the next step
-  int64_t unfinished;  // vehicles not Arrived/Retired after motion
-  int64_t dcount;      // decisions this step
-  int64_t qtotal, qsamples;
-  int64_t ant_steps, vehicle_routes, decisions, candidates, degree_sum;
+  int64_t qsamples;
   int32_t done;
   int32_t max_occ;
-  uint32_t blocks_done;
-  int32_t error;  // device-side overflow flag (path buffer)
-  // stage trace of the current step (%globaltimer ns; written when trace is on):
-  // [0] walk start (min), [1] walk staging done (max), [2] walk end (max),
-  // [3] tail start (min), [4] E1||E2 done, [5] E3 done, [6] F+G done
-  unsigned long long trace[8];
+  int32_t error;       // device-side overflow flag (path buffer)
   int32_t trace_on;
-  int32_t _pad2;
+  alignas(128) int64_t n_next;      // accumulated for the next step
+  alignas(128) int64_t unfinished;  // vehicles not Arrived/Retired after motion
+  alignas(128) int64_t dcount;      // decisions this step
+  alignas(128) int64_t qtotal;
+  alignas(128) int64_t ant_steps;
+  alignas(128) int64_t vehicle_routes;
+  alignas(128) int64_t decisions;
+  alignas(128) int64_t candidates;
+  alignas(128) int64_t degree_sum;
+  alignas(128) uint32_t blocks_done;
+  alignas(128) int32_t max_occ_acc;  // atomicMax target of stage F+G
+  // stage trace of the current step (%globaltimer ns; written when trace_on
+  // is set): [0] walk start (min), [1] walk staging done (max), [2] walk end
+  // (max), [3] tail start (min), [4]/[7]-[11] probes, [5] signals done,
+  // [6] F+G done
+  alignas(128) unsigned long long trace[12];
 };
 
 struct DevVehicles {
@@ -146,6 +157,7 @@ struct DevWorld {
   int32_t* occ_new;   // [m] being accumulated this step
   int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)
   int32_t* dec_head;  // [m] decision stack per slot (network-wide MACO) or per node (scoped)
+  const int64_t* dep_amount;  // lattice: deposit_amount(h * edge length) for h = 0..plan_cap (host-computed)
 };
 
 }  // namespace gmaco

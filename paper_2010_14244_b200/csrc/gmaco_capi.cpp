@@ -704,8 +704,15 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.plan_cap = alg == GMACO_COLONY ? std::max(walk_bound, 1) : 1;
   if (alg == GMACO_COLONY && (size_t)V * p.plan_cap * 4 > (size_t(32) << 30))
     throw ValidationError("colony: planned-tour storage exceeds 32 GiB (set colony.max_hops)");
-  // scratch mode keeps every ant's tour (no winner replay) when it fits 2 GiB
-  p.scratch_mode = alg == GMACO_COLONY && (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(2) << 30);
+  // Tours on the lattice fast path with <= 64-hop walks live in registers as
+  // move bits; otherwise scratch mode keeps every ant's tour (no winner
+  // replay) when it fits 16 GiB of the B200's 180 GB; larger colonies replay
+  // the winner instead.
+  const bool lattice_walker = alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter &&
+                              p.ants <= 256;
+  p.grid_bits = lattice_walker && p.plan_cap <= 64 && !std::getenv("GMACO_NO_BITS");
+  p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits &&
+                   (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(16) << 30);
   if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound
     int64_t maxlen = 0;
     for (int64_t L : g.len) maxlen = std::max(maxlen, L);
@@ -736,6 +743,15 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.occ_new = B.filled<int32_t>(M, 0);
   w.dep = B.filled<int64_t>(M, 0);
   w.dec_head = B.filled<int32_t>(std::max(M, n), -1);
+  {  // lattice tours have length hops * edge length: tabulate deposit_amount (pheromone.cpp:73-78)
+    std::vector<int64_t> amt((size_t)p.plan_cap + 1, 0);
+    if (dd->kind == GMACO_DIST_GRID)
+      for (int32_t hh = 1; hh <= p.plan_cap; ++hh) {
+        const double km = static_cast<double>((int64_t)hh * g.len[0]) / 1e6;
+        amt[hh] = tau_from_double(c.pheromone.aco_deposit_q / km);
+      }
+    w.dep_amount = B.upload(amt);
+  }
 
   // ---- signals -----------------------------------------------------------
   DevSignals& ds = w.s;
@@ -1427,20 +1443,20 @@ int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, doubl
 
 // Profiling hook: stage timestamps (%globaltimer ns) of the next `steps`
 // steps' LAST step; see DevCtl::trace.  Not part of the reference surface.
-int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out8) {
-  if (!h || !out8) return GMACO_EVALIDATION;
+int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12) {
+  if (!h || !out12) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     for (int32_t i = 0; i < steps; ++i) {
       DevCtl t;
       CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
       t.trace_on = 1;
-      for (int k = 0; k < 8; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
+      for (int k = 0; k < 12; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
       CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
       run_steps(h, 1);
     }
     DevCtl t;
     CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < 8; ++k) out8[k] = t.trace[k];
+    for (int k = 0; k < 12; ++k) out12[k] = t.trace[k];
     t.trace_on = 0;
     CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
   });

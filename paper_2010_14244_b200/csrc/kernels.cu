@@ -853,7 +853,16 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 // sequential roulette and one tour-cost load — identical decisions to
 // k_colony / k_colony_ell4 (same candidate order, same arithmetic).
 // ---------------------------------------------------------------------------
-template <bool kSmem, bool kScratch>
+// Tour materialization of the lattice walker:
+//   kTourReplay  — the winner re-walks (counter RNG) into v.plan;
+//   kTourScratch — every ant writes its slots to v.scratch, the plan is the
+//                  winner's row;
+//   kTourBits    — walks of <= 64 hops keep one bit per hop (vertical or
+//                  horizontal move) in a register; the winner's tour is
+//                  rebuilt arithmetically into v.plan.  No per-hop stores.
+enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
+
+template <bool kSmem, int kTour>
 __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   if (skip_step(w.ctl)) return;
   if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
@@ -867,6 +876,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   __shared__ int32_t done_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
   __shared__ long long red5[7][32];
+  __shared__ unsigned long long bits_s[kTour == kTourBits ? 256 : 1];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
@@ -946,9 +956,9 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   if (live) start = start_s[lv];
   if (live && start >= 0) {
     const int32_t dest = v.dest[vid];
-    const int32_t cols = w.d.cols, rows = w.d.rows;
+    const int32_t cols = w.d.cols;
     const int32_t rd = dest / cols, cd = dest - rd * cols;
-    int32_t rx = start / cols, cx = start - rx * cols;
+    const int32_t rx = start / cols, cx = start - rx * cols;
     // The walk is monotone: the signs of (rd - rx, cd - cx) never flip and
     // every hop removes one unit of Manhattan distance, so the hop count is
     // known up front (the generic loop's x != dest / hop_limit / max_hops
@@ -959,9 +969,11 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     if (w.p.hop_limit && n > w.p.hop_limit) n = w.p.hop_limit;
     const bool capped = n > w.p.max_hops;  // generic walker fails at hop max_hops
     if (capped) n = w.p.max_hops;
-    int32_t* tp = kScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
+    int32_t* tp = kTour == kTourScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
     tour = tp;
-    int32_t idegs = 0, icands = 0;
+    int32_t idegs = 0;
+    int32_t n_two = 0;  // hops with two candidates (candidates = n + n_two)
+    unsigned long long mbits = 0;  // move_v per hop, first hop in the most significant used bit
     // Direction-slotted lattice rows: slot 4x+{0,1,2,3} = {up, left, right,
     // down} (holes at the border), i.e. ascending neighbour id.  With the
     // walk direction fixed, the candidate slots are per-walk constants: when
@@ -971,29 +983,35 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     const int step_h = dc, step_v = dr * cols;
     const bool v_first = dr < 0;
     int32_t x = start;
+    // One hop as straight-line predicated code (no branches: the compiler can
+    // interleave the next Philox block and the two hops of a pair).
     auto hop = [&](uint64_t bits) {
       const double u = to_unit(bits);
-      const bool two = rem_h > 0 && rem_v > 0;
-      const bool a_is_v = two ? v_first : rem_h == 0;
+      const bool two = (rem_h > 0) & (rem_v > 0);
+      const bool a_is_v = two ? v_first : (rem_h == 0);
       const int oa = a_is_v ? off_v : off_h, ob = a_is_v ? off_h : off_v;
-      const int xa = 4 * x + oa, xb = 4 * x + (two ? ob : oa);
-      const double wa = W[xa];
-      const double wb = two ? W[xb] : 0.0;
+      const int xb = 4 * x;
+      const double wa = W[xb + oa];
+      const double wr = W[xb + ob];  // in-row (a hole reads 0.0); used only when two
+      const double wb = two ? wr : 0.0;
       const double total = __dadd_rn(wa, wb);  // + exact 0.0 for a single candidate
-      // routing.cpp:100-113 without branches: total <= 0 or non-finite picks
-      // uniformly (floor(u*2) >= 1 takes the second), else the first
-      // candidate iff u*total < wa
-      const bool bad = !(total > 0.0) || __double_as_longlong(fabs(total)) >= 0x7ff0000000000000ll;
-      const bool take_b = two && (bad ? __dmul_rn(u, 2.0) >= 1.0 : !(__dmul_rn(u, total) < wa));
-      const bool move_v = take_b ? !a_is_v : a_is_v;
-      const int32_t s = take_b ? xb : xa;
+      const double pt = __dmul_rn(u, total), u2 = __dmul_rn(u, 2.0);
+      // routing.cpp:100-113: total <= 0 or non-finite picks uniformly
+      // (floor(u*2) >= 1 takes the second), else the first candidate iff
+      // u*total < wa (default: the last candidate)
+      const unsigned bad = (unsigned)!(total > 0.0) |
+                           (unsigned)(__double_as_longlong(fabs(total)) >= 0x7ff0000000000000ll);
+      const unsigned tb = (unsigned)two & ((bad & (unsigned)(u2 >= 1.0)) | (~bad & (unsigned)!(pt < wa)));
+      const unsigned mv = tb ? (unsigned)!a_is_v : (unsigned)a_is_v;
+      const int32_t s = xb + (mv ? off_v : off_h);
       cost += Cst[s];
-      if (kScratch) *tp++ = s;
+      if (kTour == kTourScratch) *tp++ = s;
+      if (kTour == kTourBits) mbits = (mbits << 1) | mv;
       idegs += kSmem ? sdeg[x] : __ldg(w.g.deg + x);
-      icands += 1 + two;
-      x += move_v ? step_v : step_h;
-      rem_v -= move_v;
-      rem_h -= !move_v;
+      n_two += two;
+      x += mv ? step_v : step_h;
+      rem_v -= mv;
+      rem_h -= mv ^ 1u;
     };
     if (w.p.rng == 1) {
       for (int32_t h = 0; h < n; ++h)
@@ -1016,30 +1034,108 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     hops = n;
     steps = n;
     degs = idegs;
-    cands = icands;
-    // best tour by (cost, ant); the vehicle's LAST ant to finish runs the
-    // epilogue, so no block barrier couples different vehicles' walk lengths
+    cands = n + n_two;
+    if (kTour == kTourBits) bits_s[threadIdx.x] = mbits;
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
+    if (kTour == kTourBits && (K & 31) == 0) {
+      // Whole-warp colonies: a per-vehicle named barrier (id 1+lv, K
+      // threads), then warp 0 of the vehicle runs the epilogue in parallel —
+      // lane i rebuilds hops i and i+32 directly from the winner's move bits
+      // (node after i hops = start + step_v*popc(first i bits) + step_h*rest)
+      // and issues their deposits; lane 0 does the bookkeeping and motion.
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + lv), "r"(K) : "memory");
+      if (ant < 32) {
+        const int winner = (int)(best[lv] & 1023u);
+        const unsigned long long wbits = bits_s[lv * K + winner];
+        const bool reached = hops == abs(rd - rx) + abs(cd - cx);
+        const bool dep = reached && w.p.deposit == 1;
+        const int64_t amount = dep ? w.dep_amount[hops] : 0;
+        int32_t* plan = v.plan + (size_t)vid * w.p.plan_cap;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int32_t i = ant + 32 * j;
+          if (i < hops) {
+            const unsigned long long head = i ? (wbits >> (hops - i)) : 0ull;  // first i move bits
+            const int32_t nv = __popcll(head);
+            const int32_t y = start + step_v * nv + step_h * (i - nv);
+            const unsigned mv = (unsigned)(wbits >> (hops - 1 - i)) & 1u;
+            const int32_t sl = 4 * y + (mv ? off_v : off_h);
+            plan[i] = sl;
+            if (dep) atomicAdd((unsigned long long*)&w.dep[sl], (unsigned long long)amount);
+          }
+        }
+        if (ant == 0) {
+          const bool deciding = deciding_s[lv];
+          v.plan_n[vid] = hops;
+          v.plan_step[vid] = step;
+          v.plan_done[vid] = reached && hops > 0;
+          if (deciding) {
+            const unsigned mv0 = (unsigned)(wbits >> (hops - 1)) & 1u;
+            take_edge(w, vid, 4 * start + (mv0 ? off_v : off_h), false, start);
+          }
+          routes = 1;
+          decided = deciding;
+          veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
+        }
+      }
+    } else {
+    // best tour by (cost, ant); the vehicle's LAST ant to finish runs the
+    // epilogue, so no block barrier couples different vehicles' walk lengths
     __threadfence_block();
     if (atomicAdd(&done_s[lv], 1) == K - 1) {
       __threadfence_block();
       const int winner = (int)(best[lv] & 1023u);
       const bool deciding = deciding_s[lv];
-      int32_t wh;
-      if (kScratch) {
-        v.plan_ant[vid] = winner;
-        tour = v.scratch + ((size_t)vid * K + winner) * (size_t)w.p.plan_cap;
-        wh = hops;  // every ant of the vehicle walks the same (capped) hop count
-      } else {  // replay the winner to materialize its tour
+      // Lattice epilogue (finish_colony without re-reading the tour): every
+      // ant walks the same hop count, edges have one length, and a walk
+      // reaches the destination iff it was not cut short.
+      const bool reached = hops == abs(rd - rx) + abs(cd - cx);
+      const bool dep = reached && w.p.deposit == 1;
+      const int64_t amount = dep ? w.dep_amount[hops] : 0;  // deposit_amount(hops * edge length)
+      int32_t first = -1;
+      if (kTour == kTourBits) {  // rebuild the winner's tour from its move bits
         tour = v.plan + (size_t)vid * w.p.plan_cap;
-        const Target<1> t(w.d, v.dest[vid]);
-        wh = ant_walk<1, true>(w, t, vid, winner, start, step, tour).hops;
+        const unsigned long long wb = bits_s[lv * K + winner];
+        int32_t y = start;
+        for (int32_t i = 0; i < hops; ++i) {
+          const unsigned mv = (unsigned)(wb >> (hops - 1 - i)) & 1u;
+          const int32_t sl = 4 * y + (mv ? off_v : off_h);
+          tour[i] = sl;
+          if (dep) atomicAdd((unsigned long long*)&w.dep[sl], (unsigned long long)amount);
+          y += mv ? step_v : step_h;
+          if (i == 0) first = sl;
+        }
+      } else {
+        if (kTour == kTourScratch) {
+          v.plan_ant[vid] = winner;
+          tour = v.scratch + ((size_t)vid * K + winner) * (size_t)w.p.plan_cap;
+        } else {  // replay the winner to materialize its tour
+          tour = v.plan + (size_t)vid * w.p.plan_cap;
+          const Target<1> t(w.d, v.dest[vid]);
+          hops = ant_walk<1, true>(w, t, vid, winner, start, step, tour).hops;
+        }
+        if (dep) {
+          int32_t i = 0;
+          for (; i + 4 <= hops; i += 4) {  // independent loads, pipelined
+            const int32_t a0 = tour[i], a1 = tour[i + 1], a2 = tour[i + 2], a3 = tour[i + 3];
+            atomicAdd((unsigned long long*)&w.dep[a0], (unsigned long long)amount);
+            atomicAdd((unsigned long long*)&w.dep[a1], (unsigned long long)amount);
+            atomicAdd((unsigned long long*)&w.dep[a2], (unsigned long long)amount);
+            atomicAdd((unsigned long long*)&w.dep[a3], (unsigned long long)amount);
+          }
+          for (; i < hops; ++i) atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+        }
+        if (hops > 0) first = tour[0];
       }
-      finish_colony(w, vid, start, tour, wh, deciding, step);
+      v.plan_n[vid] = hops;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = reached && hops > 0;
+      if (deciding) take_edge(w, vid, first, false, start);
       routes = 1;
       decided = deciding;
       veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
+    }
     }
   }
   const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided, act, unf}}, red5);
@@ -1341,6 +1437,7 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
 __device__ __forceinline__ void finalize_step(const DevWorld& w) {
   DevCtl* c = w.ctl;
   c->blocks_done = 0;
+  if (c->max_occ_acc > c->max_occ) c->max_occ = c->max_occ_acc;
   c->qsamples += w.p.S;
   c->n_t = c->n_next;
   c->n_next = 0;
@@ -1407,7 +1504,7 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   const int32_t occ = (s < w.g.M && w.g.slot_edge[s] >= 0) ? slot_fg(w, s) : 0;
   const int32_t m = block_max(occ, smax);
   if (threadIdx.x == 0) {
-    if (m > 0) atomicMax(&w.ctl->max_occ, m);
+    if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
     __threadfence();
     const unsigned prev = atomicAdd(&w.ctl->blocks_done, 1u);
     is_last = prev == gridDim.x - 1;
@@ -1507,7 +1604,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     int32_t m = 0;
     for (int64_t s = gtid; s < w.g.M; s += gstride) m = max(m, slot_fg(w, (int32_t)s));
     m = block_max(m, smax);
-    if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ, m);
+    if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ_acc, m);
     if (threadIdx.x == 0) trace_max(w.ctl, 6);
     grid.sync();
     if (gtid == 0) finalize_step(w);
@@ -1543,7 +1640,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   for (int64_t s = gtid; s < w.g.M; s += gstride)
     if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
   m = block_max(m, smax);
-  if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ, m);
+  if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ_acc, m);
   if (threadIdx.x == 0) trace_max(w.ctl, 6);
   grid.sync();
   if (gtid == 0) finalize_step(w);
@@ -1627,9 +1724,11 @@ size_t grid_smem_bytes(const DevWorld& w) {
 }
 
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(k_colony_grid<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_colony_grid<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+  for (auto f : {k_colony_grid<true, kTourBits>, k_colony_grid<true, kTourScratch>, k_colony_grid<true, kTourReplay>}) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // Grid size of the cooperative tail: enough 128-thread blocks for the
@@ -1637,7 +1736,11 @@ cudaError_t configure_kernels() {
 int coop_tail_blocks(const DevWorld& w, int device) {
   int per_sm = 0, sms = 0, coop = 0;
   if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device) != cudaSuccess || !coop) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<false>, kTailCoop, 0) != cudaSuccess) return 0;
+  // the variant that will be launched (colony worlds run the fused one)
+  const cudaError_t oe = w.p.algorithm == 4
+                             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<true>, kTailCoop, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<false>, kTailCoop, 0);
+  if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M);
   const int64_t want = (work + kTailCoop - 1) / kTailCoop;
@@ -1658,19 +1761,22 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   if (r.part == 2) goto tail;
   if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
     const size_t smem = grid_smem_bytes(w);
-    if (smem) {  // whole weight/cost tables staged per CTA: pack vehicles into 256-thread CTAs
-      const int vpb = 256 / w.p.ants;
-      if (w.p.scratch_mode)
-        k_colony_grid<true, true><<<blocks_for(VS, vpb) + 1, vpb * w.p.ants, smem, st>>>(w);
-      else
-        k_colony_grid<true, false><<<blocks_for(VS, vpb) + 1, vpb * w.p.ants, smem, st>>>(w);
+    const int mode = w.p.grid_bits ? kTourBits : (w.p.scratch_mode ? kTourScratch : kTourReplay);
+    // staged tables: pack vehicles into 256-thread CTAs; otherwise one
+    // vehicle's colony per CTA when it fills whole warps
+    const int threads = smem ? (256 / w.p.ants) * w.p.ants : ((w.p.ants % 32 == 0) ? w.p.ants : 256);
+    const unsigned grid = blocks_for(VS, threads / w.p.ants) + 1;  // +1: prefetch CTA
+#define GMACO_GRID(SM, MODE) k_colony_grid<SM, MODE><<<grid, threads, SM ? smem : 0, st>>>(w)
+    if (smem) {
+      if (mode == kTourBits) GMACO_GRID(true, kTourBits);
+      else if (mode == kTourScratch) GMACO_GRID(true, kTourScratch);
+      else GMACO_GRID(true, kTourReplay);
     } else {
-      const int threads = (w.p.ants % 32 == 0) ? w.p.ants : 256, vpb = threads / w.p.ants;
-      if (w.p.scratch_mode)
-        k_colony_grid<false, true><<<blocks_for(VS, vpb) + 1, threads, 0, st>>>(w);
-      else
-        k_colony_grid<false, false><<<blocks_for(VS, vpb) + 1, threads, 0, st>>>(w);
+      if (mode == kTourBits) GMACO_GRID(false, kTourBits);
+      else if (mode == kTourScratch) GMACO_GRID(false, kTourScratch);
+      else GMACO_GRID(false, kTourReplay);
     }
+#undef GMACO_GRID
   } else if (w.p.algorithm == 4 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
     // one vehicle's colony per block when it fills whole warps (no block
     // barrier couples different vehicles' walk lengths), else packed

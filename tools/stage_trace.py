@@ -15,7 +15,9 @@ for V in (10, 1000):
     e = Engine(net, cfg, net.grid_distance())
     e.step(5)
     for rep in range(3):
-        t = e.debug_trace(1).astype(np.int64)
+        raw = e.debug_trace(1)
+        t = raw.astype(np.int64)
         rel = (t - t[0]) / 1e3
-        print(f"{os.environ.get('TAG', '')} V={V} walk: staged {rel[1]:.2f} end {rel[2]:.2f} | tail start {rel[3]:.2f} E12 {rel[4]:.2f} "
-              f"E3 {rel[5]:.2f} FG {rel[6]:.2f} (us)")
+        print(f"{os.environ.get('TAG', '')} V={V} walk: staged {rel[1]:.2f} end {rel[2]:.2f} | "
+              f"tail start {rel[3]:.2f} signals {rel[5]:.2f} FG {rel[6]:.2f} (us) | max epilogue cycles: "
+              f"rebuild+deposit {raw[7]} take_edge {raw[8]} move {raw[9]} | walk(loop..epilogue start) {raw[10]} | block0 reduce {raw[11]}")
