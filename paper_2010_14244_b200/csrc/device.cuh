@@ -33,6 +33,7 @@ struct DevGraph {
   const int32_t* slot_edge; // [m] reference edge id per slot
   const int32_t* slot_from; // [m] edge.from per slot
   const double* eta_beta;   // [m] pow(1/(len/1000), beta), host std::pow (routing.cpp:92-94)
+  const int2* nrow;         // [M] general-graph walker: {first, span | deg << 8} of col[slot]'s row
 };
 
 // Distance service read by the candidate filter (routing.cpp:16-30).
@@ -43,6 +44,12 @@ struct DevDist {
   int32_t n;
   const int64_t* table;    // [slot * n + x] = dist(x, dest of slot), kInf unreachable
   const int32_t* slot_of;  // node -> table row (targets), nullptr = identity (dense)
+  // Progress-filter bitmaps (general-graph walker): per table row t and slot
+  // word, {closer, reach} bits of slot s = dist_t(col[s]) < dist_t(from[s]) and
+  // dist_t(col[s]) != inf (routing.cpp:16-30 evaluated ahead of time, exact
+  // int64 comparisons); fbw words per row incl. one padding word.
+  const uint2* fbits;
+  int64_t fbw;
 };
 
 struct DevParams {
@@ -75,6 +82,8 @@ struct DevParams {
   int32_t shard_lo, shard_hi, sharded;
   int32_t no_smem;          // A/B switch: read the walk tables from global memory
   int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (walks <= 64 hops)
+  int32_t max_degree;       // largest out-degree (general-graph walker bound)
+  int32_t csr_walker;       // colony runs on k_colony_csr (bitmaps + nrow built)
   int32_t record_paths;
 };
 

@@ -678,6 +678,39 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // debugging / A-B switches (defaults are the production configuration)
   p.prefetch = std::getenv("GMACO_NO_PREFETCH") ? 0 : 1;
   p.no_smem = std::getenv("GMACO_NO_SMEM") ? 1 : 0;
+  p.max_degree = maxdeg;
+  // general-graph colony walker: progress-filter bitmaps + next-row
+  // descriptors replace the per-hop neighbour distance gathers
+  p.csr_walker = alg == GMACO_COLONY && dd->kind != GMACO_DIST_GRID && p.progress_filter && ell != 4 &&
+                 c.colony.ants <= 256 && maxdeg <= 16;
+  if (p.csr_walker) {
+    std::vector<int2> nrow(M, make_int2(0, 0));
+    for (int32_t s = 0; s < M; ++s)
+      if (col[s] >= 0) nrow[s] = make_int2(row[col[s]].x, row[col[s]].y | (deg[col[s]] << 8));
+    w.g.nrow = B.upload(nrow);
+    const int32_t T = dd->kind == GMACO_DIST_TARGETS ? (int32_t)targets.size() : n;
+    const int64_t fbw = (M + 31) / 32 + 1;
+    std::vector<uint2> fb((size_t)T * fbw, make_uint2(0, 0));
+    const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int th = 0; th < nt; ++th)
+      pool.emplace_back([&, th] {
+        for (int32_t t = th; t < T; t += nt) {
+          const int64_t* dt = table.data() + (size_t)t * n;
+          uint2* out = fb.data() + (size_t)t * fbw;
+          for (int32_t s = 0; s < M; ++s) {
+            if (col[s] < 0) continue;
+            const int64_t dn = dt[col[s]];
+            if (dn == kInf) continue;
+            out[s >> 5].y |= 1u << (s & 31);
+            if (dn < dt[slot_from[s]]) out[s >> 5].x |= 1u << (s & 31);
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    w.d.fbits = B.upload(fb);
+    w.d.fbw = fbw;
+  }
   p.shard_lo = 0;
   p.shard_hi = V;
   p.sharded = 0;
@@ -706,13 +739,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     throw ValidationError("colony: planned-tour storage exceeds 32 GiB (set colony.max_hops)");
   // Tours on the lattice fast path with <= 64-hop walks live in registers as
   // move bits; otherwise scratch mode keeps every ant's tour (no winner
-  // replay) when it fits 16 GiB of the B200's 180 GB; larger colonies replay
+  // replay) when it fits 48 GiB of the B200's 180 GB; larger colonies replay
   // the winner instead.
   const bool lattice_walker = alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter &&
                               p.ants <= 256;
   p.grid_bits = lattice_walker && p.plan_cap <= 64 && !std::getenv("GMACO_NO_BITS");
-  p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits &&
-                   (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(16) << 30);
+  p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits && !std::getenv("GMACO_NO_SCRATCH") &&
+                   (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(48) << 30);
   if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound
     int64_t maxlen = 0;
     for (int64_t L : g.len) maxlen = std::max(maxlen, L);

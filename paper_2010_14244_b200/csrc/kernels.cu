@@ -844,6 +844,191 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 }
 
 // ---------------------------------------------------------------------------
+// B (colony) on general graphs (CSR or ELL-8 rows, distance tables, progress
+// filter on).  One thread per ant.  The candidate filter (routing.cpp:16-30)
+// is read from precomputed {closer, reach} bitmaps of the destination's table
+// row instead of gathering every neighbour's distance, and each slot carries
+// its head node's row descriptor, so a hop is two dependent round trips:
+// (filter bits + the row's weights, issued together), then (chosen slot's
+// head, next row descriptor, edge cost).  The decision is register-only
+// (sequential left-to-right roulette, routing.cpp:88-113).  Same semantics
+// as k_colony.
+// ---------------------------------------------------------------------------
+template <int MAXD, bool kScratch>
+__global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block
+    if (w.p.prefetch) prefetch_tail_state(w);
+    return;
+  }
+  constexpr int kMaxVpb = 256;
+  __shared__ unsigned long long best[kMaxVpb];
+  __shared__ int32_t start_s[kMaxVpb];
+  __shared__ uint8_t deciding_s[kMaxVpb];
+  __shared__ long long red5[7][32];
+  const int K = w.p.ants;
+  const int vpb = blockDim.x / K;
+  const int lv = threadIdx.x / K;
+  const int ant = threadIdx.x - lv * K;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * vpb + lv;
+  const bool live = lv < vpb && vid < w.p.shard_hi;
+  const int64_t step = w.ctl->step;
+  const DevVehicles& v = w.v;
+  long long act = 0, unf = 0;
+  if (live && ant == 0) {
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    int32_t start = -1;
+    const bool deciding = st == kAtNode;
+    if (deciding)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kQueued)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kOnEdge)
+      start = w.g.col[v.on_edge[vid]];
+    if (start >= 0 && start == v.dest[vid]) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      start = -1;
+    }
+    start_s[lv] = start;
+    deciding_s[lv] = deciding;
+    if (w.p.sharded) v.dec_rec[vid] = -1;
+    if (start < 0) veh_move(w, vid, act, unf);
+    best[lv] = ~0ull;
+  }
+  __syncthreads();
+  long long steps = 0, cands = 0, degs = 0, routes = 0, decided = 0;
+  int32_t start = -1;
+  bool first_ok = false;
+  int32_t hops = 0;
+  if (live) start = start_s[lv];
+  if (live && start >= 0) {
+    const int32_t dest = v.dest[vid];
+    const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+    const int64_t* __restrict__ trow = tslot < 0 ? nullptr : w.d.table + (size_t)tslot * w.d.n;
+    const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit;
+    int32_t* tp = kScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
+    int64_t cost = 0;
+    int32_t x = start;
+    const uint2* __restrict__ fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
+    const int2 r0 = __ldg(w.g.row + start);
+    int32_t first = r0.x, span = r0.y, deg = __ldg(w.g.deg + start);
+    uint4 rnd = make_uint4(0, 0, 0, 0);
+    while (x != dest && (hop_limit == 0 || hops < hop_limit)) {
+      if (hops >= max_hops) {
+        cost = kInf;
+        break;
+      }
+      // round trip 1: the row's filter bits and weights (independent loads)
+      uint32_t closer = 0, reach = 0;
+      if (fb) {
+        const uint2 lo = __ldg(fb + (first >> 5)), hi = __ldg(fb + (first >> 5) + 1);
+        const uint32_t msk = (1u << span) - 1u;
+        closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
+        reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
+      }
+      double wv[MAXD];
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) wv[i] = i < span ? w.weight[first + i] : 0.0;
+      degs += deg;
+      const uint32_t cand = closer ? closer : reach;
+      if (!cand) {
+        cost = kInf;
+        break;
+      }
+      if (hops == 0) first_ok = true;
+      cands += __popc(cand);
+      double u;
+      if (w.p.rng == 1) {
+        u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                         (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
+      } else {
+        if ((hops & 1) == 0)
+          rnd = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hops >> 1), w.p.rk);
+        u = to_unit(philox_half(rnd, hops));
+      }
+      // sequential left-to-right roulette over the candidates (registers only)
+      double total = 0.0;
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i)
+        if (cand & (1u << i)) {
+          total = __dadd_rn(total, wv[i]);
+          ++c;
+        }
+      int pick = 31 - __clz(cand);  // default: last candidate
+      if (total <= 0.0 || !isfinite(total)) {
+        const int pp = min((int)__dmul_rn(u, (double)c), c - 1);
+        uint32_t mm = cand;
+        for (int j = 0; j < pp; ++j) mm &= mm - 1;
+        pick = __ffs(mm) - 1;
+      } else {
+        const double point = __dmul_rn(u, total);
+        double cum = 0.0;
+        bool found = false;
+#pragma unroll
+        for (int i = 0; i < MAXD; ++i)
+          if (!found && (cand & (1u << i))) {
+            cum = __dadd_rn(cum, wv[i]);
+            if (point < cum) {
+              pick = i;
+              found = true;
+            }
+          }
+      }
+      // round trip 2: the chosen slot's head node, its row descriptor, its cost
+      const int32_t sl = first + pick;
+      x = __ldg(w.g.col + sl);
+      const int2 nr = __ldg(w.g.nrow + sl);
+      cost += w.ecost[sl];
+      if (kScratch) tp[hops] = sl;
+      first = nr.x;
+      span = nr.y & 0xff;
+      deg = nr.y >> 8;
+      ++hops;
+      ++steps;
+    }
+    const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
+    atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
+  }
+  __syncthreads();
+  if (live && start >= 0 && ant == (int)(best[lv] & 1023u)) {
+    const bool deciding = deciding_s[lv];
+    if (!first_ok) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      if (deciding) {
+        v.state[vid] = kRetired;
+        if (w.p.sharded) v.dec_rec[vid] = -2;
+      }
+    } else {
+      int32_t* tour;
+      if (kScratch) {
+        tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+        v.plan_ant[vid] = ant;
+      } else {  // replay the winner to materialize its tour
+        tour = v.plan + (size_t)vid * w.p.plan_cap;
+        const Target<0> t(w.d, v.dest[vid]);
+        hops = ant_walk<0, true>(w, t, vid, ant, start, step, tour).hops;
+      }
+      finish_colony(w, vid, start, tour, hops, deciding, step);
+      routes = 1;
+      decided = deciding;
+    }
+    veh_move(w, vid, act, unf);
+  }
+  const Sum5 t = block_sum5(Sum5{{steps, cands, degs, routes, decided, act, unf}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
+}
+
+// ---------------------------------------------------------------------------
 // B (colony) on a validated uniform lattice (GMACO_DIST_GRID, progress filter
 // on).  The distance service is closed-form and the lattice is checked at
 // create, so a node's candidate set needs no loads at all: the strictly
@@ -1785,6 +1970,17 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       k_colony_ell4<1><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
     else
       k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
+  } else if (w.p.csr_walker) {
+    const int vpb = 256 / w.p.ants;
+    const unsigned grid = blocks_for(VS, vpb) + 1;  // +1: prefetch CTA
+    const int threads = vpb * w.p.ants;
+    if (w.p.max_degree <= 8) {
+      if (w.p.scratch_mode) k_colony_csr<8, true><<<grid, threads, 0, st>>>(w);
+      else k_colony_csr<8, false><<<grid, threads, 0, st>>>(w);
+    } else {
+      if (w.p.scratch_mode) k_colony_csr<16, true><<<grid, threads, 0, st>>>(w);
+      else k_colony_csr<16, false><<<grid, threads, 0, st>>>(w);
+    }
   } else if (w.p.algorithm == 4) {
     int threads, vpb;
     colony_shape(w.p.ants, &threads, &vpb);

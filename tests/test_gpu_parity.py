@@ -284,3 +284,51 @@ def test_colony_replay_mode_large_ants():
     _same_snapshot(gpu, cpu, "ants=512")
     for vid in range(40):
         assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+
+
+def _rgg_targets(nodes, targets, seed):
+    net = networks.random_geometric(nodes, k=3, seed=seed)
+    rng = np.random.default_rng(seed)
+    tgt = np.sort(rng.choice(nodes, size=targets, replace=False)).astype(np.int32)
+    dist = abi.DistanceDesc(kind=abi.DIST_TARGETS, targets=abi.ptr(tgt, __import__("ctypes").c_int32),
+                            target_count=targets)
+    return net, dist, tgt
+
+
+@pytest.mark.parametrize("mode", ["scratch", "replay"])
+def test_colony_rgg_targets_csr_walker(mode, monkeypatch):
+    """C4's path at small scale: random-geometric graph (CSR rows, degree up
+    to ~9 -> the MAXD=16 general walker), TARGETS distance tables, long
+    multi-hop tours; scratch tours and winner replay both bit-exact."""
+    if mode == "replay":
+        monkeypatch.setenv("GMACO_NO_SCRATCH", "1")
+    net, dist, tgt = _rgg_targets(3000, 12, 77)
+    cfg = abi.colony_production(_cfg("colony", 400, 5, max_steps=40), ants=16)
+    cfg.colony.max_hops = 512
+    gpu = Engine(net, cfg, dist)
+    cpu = O.PortWorld(net, cfg, dist)
+    for k in (1, 3, 8):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, f"rgg {mode}")
+        for vid in range(0, 400, 7):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_colony_rgg_max_hops_cap():
+    """Hop cap shorter than many tours: capped ants fail (cost = inf), and
+    vehicles whose every ant failed keep their previous plan state."""
+    net, dist, tgt = _rgg_targets(2000, 6, 3)
+    cfg = abi.colony_production(_cfg("colony", 200, 8, max_steps=25), ants=32)
+    cfg.colony.max_hops = 20
+    gpu = Engine(net, cfg, dist)
+    cpu = O.PortWorld(net, cfg, dist)
+    for k in (1, 4, 12):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, "rgg max_hops")
+    assert O.results_identical(gpu.run(), cpu.run())
