@@ -84,6 +84,7 @@ struct DevParams {
   int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (walks <= 64 hops)
   int32_t max_degree;       // largest out-degree (general-graph walker bound)
   int32_t csr_walker;       // colony runs on k_colony_csr (bitmaps + nrow built)
+  int32_t ant_queue;        // csr walker in scratch mode: prologue / ant-queue walk / epilogue kernels
   int32_t record_paths;
 };
 
@@ -110,6 +111,8 @@ struct DevCtl {
   alignas(128) int64_t candidates;
   alignas(128) int64_t degree_sum;
   alignas(128) uint32_t blocks_done;
+  alignas(128) unsigned long long q_walkers;  // ant queue: walking vehicles this step
+  unsigned long long q_next;                  // ant queue: next (vehicle, ant) item
   alignas(128) int32_t max_occ_acc;  // atomicMax target of stage F+G
   // stage trace of the current step (%globaltimer ns; written when trace_on
   // is set): [0] walk start (min), [1] walk staging done (max), [2] walk end
@@ -137,6 +140,14 @@ struct DevVehicles {
   int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
   int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)
   int32_t* plan_ant;            // winning ant per vehicle (scratch mode)
+  // ant-queue walker (general graphs, scratch mode): per-vehicle walk start
+  // (-1 = not walking), deciding flag, packed (cost, ant) argmin key, the
+  // walking-vehicle list the queue indexes, and per-ant hop counts
+  int32_t* walk_start;
+  uint8_t* walk_dec;
+  unsigned long long* best_key;
+  int32_t* walkers;
+  int32_t* ant_hops;            // [V * ants] hops, -1 when the first hop had no candidate
   int32_t* dec_rec;             // [V_pad] this step's decision per vehicle: slot, -1 none, -2 retired
   int64_t* plan_step;
   uint8_t* plan_done;

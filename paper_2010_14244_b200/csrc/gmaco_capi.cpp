@@ -833,6 +833,14 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
   dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
   dv.plan_ant = B.filled<int32_t>(V, 0);
+  p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE");
+  if (p.ant_queue) {
+    dv.walk_start = B.filled<int32_t>(V, -1);
+    dv.walk_dec = B.filled<uint8_t>(V, 0);
+    dv.best_key = B.filled<unsigned long long>(V, ~0ull);
+    dv.walkers = B.filled<int32_t>(V, 0);
+    dv.ant_hops = B.filled<int32_t>((size_t)V * p.ants, 0);
+  }
   dv.dec_rec = B.filled<int32_t>(V, -1);
   dv.plan_n = B.filled<int32_t>(V, 0);
   dv.plan_step = B.filled<int64_t>(V, -1);
@@ -857,6 +865,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
   }
   h->res.coop_blocks = coop_tail_blocks(w, h->device);
+  h->res.queue_blocks = queue_blocks(w, h->device);
+  if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");
   CK(cudaEventCreate(&h->ev_a));
   CK(cudaEventCreate(&h->ev_b));
   CK(cudaDeviceSynchronize());

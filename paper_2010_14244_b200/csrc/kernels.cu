@@ -844,6 +844,290 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 }
 
 // ---------------------------------------------------------------------------
+// B (colony) on general graphs, ant-queue form (scratch mode).  Long and
+// uneven walks (C4: ~1000 hops, heavy tail) make any CTA-wide barrier wait
+// for the slowest ant, so the step runs as three kernels:
+//   k_colony_pro  one thread per vehicle: departure, walk start, fused
+//                 motion of non-walkers, walking-vehicle list;
+//   k_colony_q    persistent: every lane pulls (vehicle, ant) items from a
+//                 global counter and advances its ant ONE HOP per loop trip,
+//                 so a lane whose ant finished fetches the next item at once
+//                 (no reconvergence on walk length); argmin via atomicMin on
+//                 the packed (cost, ant) key;
+//   k_colony_epi  one warp per vehicle: winner's tour from scratch, exact
+//                 int64 deposits strided over the warp, take_edge, motion.
+// Semantics identical to k_colony_csr / k_colony (routing.cpp:16-30, 88-113).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  __shared__ long long red5[7][32];
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  long long act = 0, unf = 0;
+  bool walking = false;
+  if (vid < w.p.shard_hi) {
+    uint8_t st = v.state[vid];
+    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+      st = kAtNode;
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    int32_t start = -1;
+    const bool deciding = st == kAtNode;
+    if (deciding)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kQueued)
+      start = v.at_node[vid];
+    else if (w.p.replan_all && st == kOnEdge)
+      start = w.g.col[v.on_edge[vid]];
+    if (start >= 0 && start == v.dest[vid]) {
+      v.plan_n[vid] = 0;
+      v.plan_step[vid] = step;
+      v.plan_done[vid] = 0;
+      start = -1;
+    }
+    if (w.p.sharded) v.dec_rec[vid] = -1;
+    v.walk_start[vid] = start;
+    if (start >= 0) {
+      v.walk_dec[vid] = deciding;
+      v.best_key[vid] = ~0ull;
+      walking = true;
+    } else {
+      veh_move(w, vid, act, unf);
+    }
+  }
+  // warp-aggregated append to the walking-vehicle list (order is immaterial:
+  // every per-vehicle result is independent of processing order)
+  const unsigned m = __ballot_sync(0xffffffffu, walking);
+  if (m) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(&w.ctl->q_walkers, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (walking) v.walkers[base + __popc(m & ((1u << lane) - 1u))] = vid;
+  }
+  const Sum5 t = block_sum5(Sum5{{0, 0, 0, 0, 0, act, unf}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
+}
+
+template <int MAXD>
+__global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const DevVehicles& v = w.v;
+  const int K = w.p.ants;
+  const int64_t step = w.ctl->step;
+  const unsigned long long total = w.ctl->q_walkers * (unsigned long long)K;
+  const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit;
+  long long steps = 0, cands = 0, degs = 0;
+  // current ant
+  int32_t vid = 0, ant = 0, x = 0, dest = 0, first = 0, span = 0, deg = 0, hops = 0;
+  int64_t cost = 0;
+  bool first_ok = false, active = false;
+  const uint2* fb = nullptr;
+  int32_t* tp = nullptr;
+  uint4 rnd = make_uint4(0, 0, 0, 0);
+  // Grouped form (K divides 32): K consecutive lanes own one vehicle's
+  // colony and fetch the next vehicle together once all K ants finished, so a
+  // vehicle's ants walk side by side (shared rows hit L1, same-node loads
+  // coalesce).  Otherwise every lane fetches single ants.
+  const bool grouped = K <= 32 && (32 % K) == 0;
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
+  unsigned live = 0xffffffffu;  // warp lanes still in the loop (uniform)
+  for (;;) {
+    bool fetch = !active;
+    if (grouped) {
+      const unsigned idle = __ballot_sync(live, !active);
+      fetch = (idle & gmask) == gmask;
+    }
+    unsigned long long a = 0;
+    if (fetch) {
+      if (grouped) {  // the whole group is fetching: one atomic for K ants
+        unsigned long long b = 0;
+        if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
+        a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
+      } else {
+        a = atomicAdd(&w.ctl->q_next, 1ull);
+      }
+    }
+    const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
+    if (grouped) live &= ~__ballot_sync(live, out);
+    if (out) break;
+    if (fetch) {
+      vid = v.walkers[a / K];
+      ant = (int32_t)(a % K);
+      x = v.walk_start[vid];
+      dest = v.dest[vid];
+      const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+      fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
+      const int2 r0 = __ldg(w.g.row + x);
+      first = r0.x;
+      span = r0.y;
+      deg = __ldg(w.g.deg + x);
+      tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+      hops = 0;
+      cost = 0;
+      first_ok = false;
+      active = true;
+    }
+    if (!active) continue;  // idle lane waiting for its group (grouped form)
+    bool fin = false;
+    if (hops >= max_hops) {
+      cost = kInf;
+      fin = true;
+    } else {
+      uint32_t closer = 0, reach = 0;
+      if (fb) {
+        const uint2 lo = __ldg(fb + (first >> 5)), hi = __ldg(fb + (first >> 5) + 1);
+        const uint32_t msk = (1u << span) - 1u;
+        closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
+        reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
+      }
+      double wv[MAXD];
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) wv[i] = i < span ? w.weight[first + i] : 0.0;
+      degs += deg;
+      const uint32_t cand = closer ? closer : reach;
+      if (!cand) {
+        cost = kInf;
+        fin = true;
+      } else {
+        if (hops == 0) first_ok = true;
+        cands += __popc(cand);
+        double u;
+        if (w.p.rng == 1) {
+          u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                           (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
+        } else {
+          if ((hops & 1) == 0)
+            rnd = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hops >> 1),
+                             w.p.rk);
+          u = to_unit(philox_half(rnd, hops));
+        }
+        double total_w = 0.0;
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < MAXD; ++i)
+          if (cand & (1u << i)) {
+            total_w = __dadd_rn(total_w, wv[i]);
+            ++c;
+          }
+        int pick = 31 - __clz(cand);
+        if (total_w <= 0.0 || !isfinite(total_w)) {
+          const int pp = min((int)__dmul_rn(u, (double)c), c - 1);
+          uint32_t mm = cand;
+          for (int j = 0; j < pp; ++j) mm &= mm - 1;
+          pick = __ffs(mm) - 1;
+        } else {
+          const double point = __dmul_rn(u, total_w);
+          double cum = 0.0;
+          bool found = false;
+#pragma unroll
+          for (int i = 0; i < MAXD; ++i)
+            if (!found && (cand & (1u << i))) {
+              cum = __dadd_rn(cum, wv[i]);
+              if (point < cum) {
+                pick = i;
+                found = true;
+              }
+            }
+        }
+        const int32_t sl = first + pick;
+        x = __ldg(w.g.col + sl);
+        const int2 nr = __ldg(w.g.nrow + sl);
+        cost += w.ecost[sl];
+        tp[hops] = sl;
+        first = nr.x;
+        span = nr.y & 0xff;
+        deg = nr.y >> 8;
+        ++hops;
+        ++steps;
+        fin = x == dest || (hop_limit != 0 && hops >= hop_limit);
+      }
+    }
+    if (fin) {
+      const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
+      v.ant_hops[(size_t)vid * K + ant] = first_ok ? hops : -1;
+      atomicMin(&v.best_key[vid], (cc << 10) | (uint64_t)ant);
+      active = false;
+    }
+  }
+  // per-warp counter flush (lanes leave the loop at different times)
+  __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) {
+    steps += __shfl_xor_sync(0xffffffffu, steps, o);
+    cands += __shfl_xor_sync(0xffffffffu, cands, o);
+    degs += __shfl_xor_sync(0xffffffffu, degs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
+    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
+    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block
+    if (w.p.prefetch) prefetch_tail_state(w);
+    if (threadIdx.x == 0) {  // the queue walk is complete: re-arm the queue
+      w.ctl->q_walkers = 0;
+      w.ctl->q_next = 0;
+    }
+    return;
+  }
+  __shared__ long long red5[7][32];
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  const int lane = threadIdx.x & 31;
+  const int32_t vid = w.p.shard_lo + blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  long long routes = 0, decided = 0, act = 0, unf = 0;
+  const int32_t start = vid < w.p.shard_hi ? v.walk_start[vid] : -1;
+  if (start >= 0) {
+    const int K = w.p.ants;
+    const bool deciding = v.walk_dec[vid];
+    const int ant = (int)(v.best_key[vid] & 1023u);
+    const int32_t hops = v.ant_hops[(size_t)vid * K + ant];
+    if (hops < 0) {  // no candidate at the first hop
+      if (lane == 0) {
+        v.plan_n[vid] = 0;
+        v.plan_step[vid] = step;
+        v.plan_done[vid] = 0;
+        if (deciding) {
+          v.state[vid] = kRetired;
+          if (w.p.sharded) v.dec_rec[vid] = -2;
+        }
+      }
+    } else {
+      const int32_t* tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+      const bool done = hops > 0 && w.g.col[tour[hops - 1]] == v.dest[vid];
+      if (done && w.p.deposit == 1) {  // finish_colony's deposit, strided over the warp
+        long long len = 0;
+        for (int i = lane; i < hops; i += 32) len += w.g.len[tour[i]];
+        for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
+        const double km = __ddiv_rn((double)len, 1e6);
+        const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+        for (int i = lane; i < hops; i += 32)
+          atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+      }
+      if (lane == 0) {
+        v.plan_ant[vid] = ant;
+        v.plan_n[vid] = hops;
+        v.plan_step[vid] = step;
+        v.plan_done[vid] = done;
+        if (deciding) take_edge(w, vid, tour[0], false, start);
+        routes = 1;
+        decided = deciding;
+      }
+    }
+    if (lane == 0) veh_move(w, vid, act, unf);
+  }
+  const Sum5 t = block_sum5(Sum5{{0, 0, 0, routes, decided, act, unf}}, red5);
+  if (threadIdx.x == 0) flush_counters(w.ctl, t);
+}
+
+// ---------------------------------------------------------------------------
 // B (colony) on general graphs (CSR or ELL-8 rows, distance tables, progress
 // filter on).  One thread per ant.  The candidate filter (routing.cpp:16-30)
 // is read from precomputed {closer, reach} bitmaps of the destination's table
@@ -1932,6 +2216,17 @@ int coop_tail_blocks(const DevWorld& w, int device) {
   return (int)std::min<int64_t>(want, (int64_t)per_sm * sms);
 }
 
+int queue_blocks(const DevWorld& w, int device) {
+  if (!w.p.ant_queue) return 0;
+  int per_sm = 0, sms = 0;
+  const cudaError_t oe = w.p.max_degree <= 8
+                             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q<8>, 128, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q<16>, 128, 0);
+  if (oe != cudaSuccess || per_sm < 1) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  return per_sm * sms;  // persistent: one full wave
+}
+
 void colony_shape(int ants, int* threads, int* vpb) {
   int t = ants <= 256 ? 256 : ((ants + 31) / 32) * 32;
   *threads = t;
@@ -1970,6 +2265,13 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       k_colony_ell4<1><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
     else
       k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
+  } else if (w.p.ant_queue) {
+    k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
+    if (w.p.max_degree <= 8)
+      k_colony_q<8><<<r.queue_blocks, 128, 0, st>>>(w);
+    else
+      k_colony_q<16><<<r.queue_blocks, 128, 0, st>>>(w);
+    k_colony_epi<<<blocks_for(VS, 8) + 1, 256, 0, st>>>(w);  // +1: prefetch CTA
   } else if (w.p.csr_walker) {
     const int vpb = 256 / w.p.ants;
     const unsigned grid = blocks_for(VS, vpb) + 1;  // +1: prefetch CTA
@@ -2049,6 +2351,7 @@ tail:
 // the CUB scan and NCCL collectives are not counted).
 int kernels_per_step(const DevWorld& w, const StepResources& r) {
   int k = 1;                 // stage-B walk / decide
+  if (w.p.ant_queue) k += 2; // k_colony_pro + k_colony_epi around k_colony_q
   if (w.p.sharded) k += 1;   // k_apply_remote
   if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
   if (w.p.S > 0) k += 2;     // k_signals, k_e3

@@ -16,6 +16,7 @@ struct StepResources {
   bool capturing = false;
   int part = 0;  // 0 whole step, 1 stage-B walk only, 2 stages C..G only
   int coop_blocks = 0;  // >0: stages C..G as one cooperative launch of this many blocks
+  int queue_blocks = 0; // ant-queue walker: persistent grid (one full wave)
   // sharded runs: enqueues the decision / deposit exchange between stage B
   // and the rest of the step (NCCL); null for host-mediated exchange
   cudaError_t (*exchange)(void* ctx, cudaStream_t st) = nullptr;
@@ -30,6 +31,7 @@ size_t scan_temp_bytes(int V);
 int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
+int queue_blocks(const DevWorld& w, int device);
 void colony_shape(int ants, int* threads, int* vpb);
 cudaError_t launch_next_node(const DevWorld& w, int algorithm, int count, const int32_t* cur,
                              const int32_t* dst, const uint64_t* entity, const uint64_t* stepk, int64_t n_t,

@@ -295,13 +295,17 @@ def _rgg_targets(nodes, targets, seed):
     return net, dist, tgt
 
 
-@pytest.mark.parametrize("mode", ["scratch", "replay"])
+@pytest.mark.parametrize("mode", ["queue", "block", "replay"])
 def test_colony_rgg_targets_csr_walker(mode, monkeypatch):
     """C4's path at small scale: random-geometric graph (CSR rows, degree up
     to ~9 -> the MAXD=16 general walker), TARGETS distance tables, long
-    multi-hop tours; scratch tours and winner replay both bit-exact."""
+    multi-hop tours.  queue = persistent ant-queue walker (the default in
+    scratch mode), block = one-CTA-per-vehicles walker with scratch tours,
+    replay = winner replay; all bit-exact."""
     if mode == "replay":
         monkeypatch.setenv("GMACO_NO_SCRATCH", "1")
+    if mode == "block":
+        monkeypatch.setenv("GMACO_NO_QUEUE", "1")
     net, dist, tgt = _rgg_targets(3000, 12, 77)
     cfg = abi.colony_production(_cfg("colony", 400, 5, max_steps=40), ants=16)
     cfg.colony.max_hops = 512
