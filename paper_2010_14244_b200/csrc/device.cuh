@@ -172,6 +172,8 @@ struct DevWorld {
   DevCtl* ctl;
   int64_t* tau;       // [m] pheromone micro-units (slot order)
   double* weight;     // [m] roulette weight for the coming step
+  int4* rec;          // [M] ant-queue walker slot records {weight, head node, head row}; weight half
+                      //     rewritten with `weight` (nullptr unless p.ant_queue)
   int64_t* ecost;     // [m] colony tour cost per edge for the coming step
   int32_t* occ_cur;   // [m] edge occupancy of the previous step (engine.hpp:166)
   int32_t* occ_new;   // [m] being accumulated this step

@@ -568,16 +568,27 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   for (int32_t u = 0; u < n; ++u) maxdeg = std::max(maxdeg, g.out_ptr[u + 1] - g.out_ptr[u]);
   const bool lattice = dd->kind == GMACO_DIST_GRID;  // lattice shape validated above
   const int32_t ell = lattice || maxdeg <= 4 ? 4 : (maxdeg <= 8 ? 8 : 0);
-  const int32_t M = ell ? n * ell : m;
+  // general-graph colony walker: CSR rows padded to multiples of 4 slots so
+  // a row's slot records are whole 16-B vectors from a 64-B aligned start
+  const bool csr_like = alg == GMACO_COLONY && dd->kind != GMACO_DIST_GRID && c.routing.progress_filter &&
+                        c.colony.ants <= 256 && maxdeg <= 16;
+  const bool align4 = ell == 0 && csr_like;
+  std::vector<int64_t> off4;
+  if (align4) {
+    off4.assign(n + 1, 0);
+    for (int32_t u = 0; u < n; ++u) off4[u + 1] = off4[u] + ((g.out_ptr[u + 1] - g.out_ptr[u] + 3) & ~3);
+    if (off4[n] >= (int64_t(1) << 29)) throw ValidationError("graph too large for the aligned slot layout");
+  }
+  const int32_t M = ell ? n * ell : (align4 ? (int32_t)off4[n] : m);
   h->ell = ell;
   h->M = M;
   h->slot_edge.assign(M, -1);
   std::vector<int2> row(n);
   std::vector<int32_t> deg(n);
   for (int32_t u = 0; u < n; ++u) {
-    const int32_t first = ell ? u * ell : g.out_ptr[u];
+    const int32_t first = ell ? u * ell : (align4 ? (int32_t)off4[u] : g.out_ptr[u]);
     deg[u] = g.out_ptr[u + 1] - g.out_ptr[u];
-    row[u] = make_int2(first, ell ? ell : deg[u]);
+    row[u] = make_int2(first, ell ? ell : (align4 ? (deg[u] + 3) & ~3 : deg[u]));
     for (int32_t i = 0; i < deg[u]; ++i) {
       const int32_t e = g.out_edge[g.out_ptr[u] + i];
       int32_t slot = first + i;
@@ -833,8 +844,17 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
   dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
   dv.plan_ant = B.filled<int32_t>(V, 0);
-  p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE");
+  p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE") && (ell == 8 || align4);
   if (p.ant_queue) {
+    // slot records {weight (double), head node, head row (first/4) << 5 | degree}
+    std::vector<int4> rec(M, make_int4(0, 0, -1, 0));
+    for (int32_t s = 0; s < M; ++s) {
+      if (col[s] < 0) continue;
+      const int32_t hd = col[s];
+      rec[s] = make_int4(0, 0, hd, ((row[hd].x >> 2) << 5) | deg[hd]);
+    }
+    w.rec = B.upload(rec);
+    CK(sync_rec_weights(w, h->stream));
     dv.walk_start = B.filled<int32_t>(V, -1);
     dv.walk_dec = B.filled<uint8_t>(V, 0);
     dv.best_key = B.filled<unsigned long long>(V, ~0ull);
@@ -1266,6 +1286,10 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
     }
     CK(cudaMemcpy(h->w.tau, t.data(), m * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->w.weight, wt.data(), m * 8, cudaMemcpyHostToDevice));
+    if (h->w.rec) {
+      CK(sync_rec_weights(h->w, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
   });
 }
 

@@ -911,18 +911,30 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
   if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
-template <int MAXD>
-__global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
+__device__ __forceinline__ double rec_weight(const int4* r) {
+  const int4 v = __ldg(r);
+  return __hiloint2double(v.y, v.x);
+}
+
+// One hop of the queue walker is ONE dependent round trip: the row's filter
+// bits plus the 16-B slot records {weight, head node, head row} of its first
+// 8 slots (rows start 64-B aligned) are issued together; the pick is register-local, so the next row is known
+// at once.  Rows wider than 8 slots (rare on road graphs) finish the roulette
+// from global memory (L1-hot).
+__global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
+  constexpr int W8 = 8;
   if (skip_step(w.ctl)) return;
   const DevVehicles& v = w.v;
   const int K = w.p.ants;
   const int64_t step = w.ctl->step;
   const unsigned long long total = w.ctl->q_walkers * (unsigned long long)K;
   const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit;
+  const int4* __restrict__ R = w.rec;
+  const int32_t ell = w.g.ell;  // 8 (ELL-8 rows) or 0 (4-aligned CSR rows)
   long long steps = 0, cands = 0, degs = 0;
   // current ant
-  int32_t vid = 0, ant = 0, x = 0, dest = 0, first = 0, span = 0, deg = 0, hops = 0;
-  int64_t cost = 0;
+  int32_t vid = 0, ant = 0, dest = 0, first = 0, span = 0, deg = 0, hops = 0;
+  int64_t cost = 0, ec = 0;  // ec: edge cost of the previous hop (load in flight)
   bool first_ok = false, active = false;
   const uint2* fb = nullptr;
   int32_t* tp = nullptr;
@@ -957,17 +969,18 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
     if (fetch) {
       vid = v.walkers[a / K];
       ant = (int32_t)(a % K);
-      x = v.walk_start[vid];
+      const int32_t x0 = v.walk_start[vid];
       dest = v.dest[vid];
       const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
       fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
-      const int2 r0 = __ldg(w.g.row + x);
+      const int2 r0 = __ldg(w.g.row + x0);
       first = r0.x;
       span = r0.y;
-      deg = __ldg(w.g.deg + x);
+      deg = __ldg(w.g.deg + x0);
       tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
       hops = 0;
       cost = 0;
+      ec = 0;
       first_ok = false;
       active = true;
     }
@@ -977,16 +990,22 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       cost = kInf;
       fin = true;
     } else {
-      uint32_t closer = 0, reach = 0;
+      // ---- the hop's single round trip ----
+      uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
       if (fb) {
-        const uint2 lo = __ldg(fb + (first >> 5)), hi = __ldg(fb + (first >> 5) + 1);
-        const uint32_t msk = (1u << span) - 1u;
-        closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
-        reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
+        lo = __ldg(fb + (first >> 5));
+        hi = __ldg(fb + (first >> 5) + 1);
       }
-      double wv[MAXD];
+      int4 rc[W8];  // slot records: weight, head node, head row
 #pragma unroll
-      for (int i = 0; i < MAXD; ++i) wv[i] = i < span ? w.weight[first + i] : 0.0;
+      for (int i = 0; i < W8; ++i) rc[i] = i < span ? __ldg(R + first + i) : make_int4(0, 0, -1, 0);
+      double wv[W8];
+#pragma unroll
+      for (int i = 0; i < W8; ++i) wv[i] = __hiloint2double(rc[i].y, rc[i].x);
+      cost += ec;  // previous hop's edge cost (its load overlapped this trip)
+      const uint32_t msk = (1u << span) - 1u;
+      const uint32_t closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
+      const uint32_t reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
       degs += deg;
       const uint32_t cand = closer ? closer : reach;
       if (!cand) {
@@ -1005,14 +1024,20 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
                              w.p.rk);
           u = to_unit(philox_half(rnd, hops));
         }
+        // sequential left-to-right roulette over the candidates
         double total_w = 0.0;
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < MAXD; ++i)
+        for (int i = 0; i < W8; ++i)
           if (cand & (1u << i)) {
             total_w = __dadd_rn(total_w, wv[i]);
             ++c;
           }
+        const uint32_t wide = cand >> W8;  // slots 8.. of a wide row (rare)
+        for (uint32_t m = wide; m; m &= m - 1) {
+          total_w = __dadd_rn(total_w, rec_weight(R + first + W8 + __ffs(m) - 1));
+          ++c;
+        }
         int pick = 31 - __clz(cand);
         if (total_w <= 0.0 || !isfinite(total_w)) {
           const int pp = min((int)__dmul_rn(u, (double)c), c - 1);
@@ -1024,7 +1049,7 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
           double cum = 0.0;
           bool found = false;
 #pragma unroll
-          for (int i = 0; i < MAXD; ++i)
+          for (int i = 0; i < W8; ++i)
             if (!found && (cand & (1u << i))) {
               cum = __dadd_rn(cum, wv[i]);
               if (point < cum) {
@@ -1032,18 +1057,38 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
                 found = true;
               }
             }
+          for (uint32_t m = found ? 0u : wide; m; m &= m - 1) {
+            const int i = W8 + __ffs(m) - 1;
+            cum = __dadd_rn(cum, rec_weight(R + first + i));
+            if (point < cum) {
+              pick = i;
+              break;
+            }
+          }
+        }
+        int32_t x = -1, meta = 0;
+        if (pick < W8) {
+#pragma unroll
+          for (int i = 0; i < W8; ++i)
+            if (i == pick) {
+              x = rc[i].z;
+              meta = rc[i].w;
+            }
+        } else {
+          const int4 r = __ldg(R + first + pick);
+          x = r.z;
+          meta = r.w;
         }
         const int32_t sl = first + pick;
-        x = __ldg(w.g.col + sl);
-        const int2 nr = __ldg(w.g.nrow + sl);
-        cost += w.ecost[sl];
+        ec = w.ecost[sl];  // consumed next hop
         tp[hops] = sl;
-        first = nr.x;
-        span = nr.y & 0xff;
-        deg = nr.y >> 8;
+        first = (meta >> 5) << 2;
+        deg = meta & 31;
+        span = ell ? ell : (deg + 3) & ~3;
         ++hops;
         ++steps;
         fin = x == dest || (hop_limit != 0 && hops >= hop_limit);
+        if (fin) cost += ec;
       }
     }
     if (fin) {
@@ -1897,6 +1942,7 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
       cost = cost + cost * (int64_t)load;
     }
     w.weight[s] = wt;
+    if (w.rec) *reinterpret_cast<double*>(w.rec + s) = wt;
     w.ecost[s] = cost;
   }
   return occ;
@@ -2216,12 +2262,21 @@ int coop_tail_blocks(const DevWorld& w, int device) {
   return (int)std::min<int64_t>(want, (int64_t)per_sm * sms);
 }
 
+__global__ void k_rec_weights(DevWorld w) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < w.g.M) *reinterpret_cast<double*>(w.rec + s) = w.weight[s];
+}
+
+cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st) {
+  if (!w.rec) return cudaSuccess;
+  k_rec_weights<<<blocks_for(w.g.M, 256), 256, 0, st>>>(w);
+  return cudaGetLastError();
+}
+
 int queue_blocks(const DevWorld& w, int device) {
   if (!w.p.ant_queue) return 0;
   int per_sm = 0, sms = 0;
-  const cudaError_t oe = w.p.max_degree <= 8
-                             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q<8>, 128, 0)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q<16>, 128, 0);
+  const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q, 128, 0);
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   return per_sm * sms;  // persistent: one full wave
@@ -2267,10 +2322,7 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
   } else if (w.p.ant_queue) {
     k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
-    if (w.p.max_degree <= 8)
-      k_colony_q<8><<<r.queue_blocks, 128, 0, st>>>(w);
-    else
-      k_colony_q<16><<<r.queue_blocks, 128, 0, st>>>(w);
+    k_colony_q<<<r.queue_blocks, 128, 0, st>>>(w);
     k_colony_epi<<<blocks_for(VS, 8) + 1, 256, 0, st>>>(w);  // +1: prefetch CTA
   } else if (w.p.csr_walker) {
     const int vpb = 256 / w.p.ants;

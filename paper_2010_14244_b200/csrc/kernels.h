@@ -32,6 +32,8 @@ int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
+// Copies `weight` into the weight half of the slot records (ant-queue walker).
+cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st);
 void colony_shape(int ants, int* threads, int* vpb);
 cudaError_t launch_next_node(const DevWorld& w, int algorithm, int count, const int32_t* cur,
                              const int32_t* dst, const uint64_t* entity, const uint64_t* stepk, int64_t n_t,
