@@ -911,6 +911,14 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
   if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
+// 256-bit read-only global load (sm_100a LDG.256): two slot records per
+// instruction, halving L1 wavefronts for lane-divergent rows.
+__device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 __device__ __forceinline__ double rec_weight(const int4* r) {
   const int4 v = __ldg(r);
   return __hiloint2double(v.y, v.x);
@@ -931,6 +939,8 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
   const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit;
   const int4* __restrict__ R = w.rec;
   const int32_t ell = w.g.ell;  // 8 (ELL-8 rows) or 0 (4-aligned CSR rows)
+  const bool vec_tour = (w.p.plan_cap & 3) == 0;
+  int4 tb = make_int4(0, 0, 0, 0);
   long long steps = 0, cands = 0, degs = 0;
   // current ant
   int32_t vid = 0, ant = 0, dest = 0, first = 0, span = 0, deg = 0, hops = 0;
@@ -994,11 +1004,16 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
       uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
       if (fb) {
         lo = __ldg(fb + (first >> 5));
-        hi = __ldg(fb + (first >> 5) + 1);
+        if ((first & 31) + span > 32) hi = __ldg(fb + (first >> 5) + 1);  // row crosses a word
       }
-      int4 rc[W8];  // slot records: weight, head node, head row
+      int4 rc[W8];  // slot records: weight, head node, head row (span is a multiple of 4)
 #pragma unroll
-      for (int i = 0; i < W8; ++i) rc[i] = i < span ? __ldg(R + first + i) : make_int4(0, 0, -1, 0);
+      for (int i = 0; i < W8; i += 2) {
+        if (i < span)
+          ld256(R + first + i, rc[i], rc[i + 1]);
+        else
+          rc[i] = rc[i + 1] = make_int4(0, 0, -1, 0);
+      }
       double wv[W8];
 #pragma unroll
       for (int i = 0; i < W8; ++i) wv[i] = __hiloint2double(rc[i].y, rc[i].x);
@@ -1081,7 +1096,15 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
         }
         const int32_t sl = first + pick;
         ec = w.ecost[sl];  // consumed next hop
-        tp[hops] = sl;
+        // tour: 4 hops per 16-B store when the scratch stride allows
+        tb.x = (hops & 3) == 0 ? sl : tb.x;
+        tb.y = (hops & 3) == 1 ? sl : tb.y;
+        tb.z = (hops & 3) == 2 ? sl : tb.z;
+        tb.w = (hops & 3) == 3 ? sl : tb.w;
+        if (!vec_tour)
+          tp[hops] = sl;
+        else if ((hops & 3) == 3)
+          *reinterpret_cast<int4*>(tp + hops - 3) = tb;
         first = (meta >> 5) << 2;
         deg = meta & 31;
         span = ell ? ell : (deg + 3) & ~3;
@@ -1092,6 +1115,8 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
       }
     }
     if (fin) {
+      if (vec_tour)  // flush the partial 4-hop tour buffer
+        for (int j = hops & ~3; j < hops; ++j) tp[j] = (j & 3) == 0 ? tb.x : (j & 3) == 1 ? tb.y : tb.z;
       const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
       v.ant_hops[(size_t)vid * K + ant] = first_ok ? hops : -1;
       atomicMin(&v.best_key[vid], (cc << 10) | (uint64_t)ant);
