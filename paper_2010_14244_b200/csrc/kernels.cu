@@ -929,7 +929,7 @@ __device__ __forceinline__ double rec_weight(const int4* r) {
 // 8 slots (rows start 64-B aligned) are issued together; the pick is register-local, so the next row is known
 // at once.  Rows wider than 8 slots (rare on road graphs) finish the roulette
 // from global memory (L1-hot).
-__global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
+__global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   constexpr int W8 = 8;
   if (skip_step(w.ctl)) return;
   const DevVehicles& v = w.v;
@@ -1039,15 +1039,20 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
                              w.p.rk);
           u = to_unit(philox_half(rnd, hops));
         }
-        // sequential left-to-right roulette over the candidates
+        // sequential left-to-right roulette over the candidates; the running
+        // sums are kept: the cumulative pass of routing.cpp:104-110 adds the
+        // same weights in the same order, so its values ARE these prefixes
         double total_w = 0.0;
+        double pre[W8];
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < W8; ++i)
+        for (int i = 0; i < W8; ++i) {
           if (cand & (1u << i)) {
             total_w = __dadd_rn(total_w, wv[i]);
             ++c;
           }
+          pre[i] = total_w;
+        }
         const uint32_t wide = cand >> W8;  // slots 8.. of a wide row (rare)
         for (uint32_t m = wide; m; m &= m - 1) {
           total_w = __dadd_rn(total_w, rec_weight(R + first + W8 + __ffs(m) - 1));
@@ -1061,17 +1066,14 @@ __global__ void __launch_bounds__(128, 5) k_colony_q(DevWorld w) {
           pick = __ffs(mm) - 1;
         } else {
           const double point = __dmul_rn(u, total_w);
-          double cum = 0.0;
-          bool found = false;
+          // first candidate whose prefix exceeds the point (independent compares)
+          uint32_t hit = 0;
 #pragma unroll
-          for (int i = 0; i < W8; ++i)
-            if (!found && (cand & (1u << i))) {
-              cum = __dadd_rn(cum, wv[i]);
-              if (point < cum) {
-                pick = i;
-                found = true;
-              }
-            }
+          for (int i = 0; i < W8; ++i) hit |= (point < pre[i] ? 1u : 0u) << i;
+          hit &= cand;
+          const bool found = hit != 0;
+          if (found) pick = __ffs(hit) - 1;
+          double cum = pre[W8 - 1];
           for (uint32_t m = found ? 0u : wide; m; m &= m - 1) {
             const int i = W8 + __ffs(m) - 1;
             cum = __dadd_rn(cum, rec_weight(R + first + i));
