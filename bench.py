@@ -371,12 +371,19 @@ def run_ours(args, rank, world, local):
     launches = args.steps
     walk_avg_s = (walk_ms / 1e3) / launches
     achieved = (alg_bytes / launches) / walk_avg_s / 1e9 if walk_avg_s > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes per walk launch from the committed ncu capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as f:
-            traffic = json.load(f)["dram_bytes_per_launch"]
+            rec = json.load(f)[args.config]
+        traffic, traffic_src = rec["dram_bytes_per_launch"], rec["source"]
     except (OSError, KeyError, ValueError):
         pass
+    lattice = args.config != "c4"
+    walk_kernel = ("k_colony_grid (stage-B lattice colony walk)" if lattice else
+                   "k_colony_q (stage-B ant-queue colony walk; pro/epi kernels inside the timed walk)")
+    note = ("latency-bound: one colony iteration is a ~15 us dependent walk over L2/SMEM-resident state "
+            "(~1 MB), see DESIGN.md §7" if args.config in ("c1", "c2") else
+            "throughput-bound gather walk, see DESIGN.md §7")
     line = {
         "metric": "ant-steps/sec",
         "value": tot_steps / t_dev,
@@ -400,12 +407,12 @@ def run_ours(args, rank, world, local):
         "gpu_launches": int(args.steps * kernels),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "traffic_source": "profiles/walk_traffic.json (ncu --set full, dram__bytes_read+write)",
-                     "kernel": "k_colony_grid (stage-B colony walk)",
+                     "traffic_source": traffic_src,
+                     "kernel": walk_kernel,
                      "algorithmic_bytes_per_launch": alg_bytes / launches,
+                     "algorithmic_bytes_model": "SURVEY 8(d): 8 + 4d + 4d(table dist) + 12c + 4(tour) per ant-step",
                      "avg_launch_us": walk_avg_s * 1e6,
-                     "note": "C2 is latency-bound (longest dependent walk; L2/SMEM-resident ~1 MB state), "
-                             "see DESIGN.md §7"},
+                     "note": note},
         "e2e": {"value": tot_e2e / e2e_dt, "unit": "ant-steps/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h,

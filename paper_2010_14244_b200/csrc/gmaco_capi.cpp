@@ -1390,16 +1390,15 @@ int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out) {
     out->candidates = c.candidates;
     out->degree_sum = c.degree_sum;
     out->kernels_per_step = kernels_per_step(h->w, h->res);
-    // algorithmic bytes of the walks: the lattice walker reads
-    // the candidate weights and the chosen edge's tour cost; the generic
-    // walkers also read the row descriptor, the columns and (table kinds) one
-    // distance per scanned neighbour
+    // algorithmic bytes of the walks, SURVEY §8(d) / DESIGN.md §5: per
+    // ant-step 8 (row pair) + 4 per scanned neighbour (column) + 4 per scanned
+    // neighbour (int32 distance; 0 with the grid closed form) + 12 per
+    // candidate (int32 tau + f64 eta) + 4 (tour write; 0 when tours are not
+    // stored).  Independent of this engine's layouts (bitmaps, records).
     const DevWorld& w = h->w;
-    if (w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.algorithm == GMACO_COLONY)
-      out->walk_bytes = 8 * c.candidates + 8 * c.ant_steps;
-    else
-      out->walk_bytes = 8 * c.ant_steps + 4 * c.degree_sum + (w.d.kind == 1 ? 0 : 8 * c.degree_sum) +
-                        8 * c.candidates + 8 * c.ant_steps;
+    const int64_t tour = w.p.scratch_mode ? 4 : 0;
+    out->walk_bytes = (8 + tour) * c.ant_steps + 4 * c.degree_sum + (w.d.kind == 1 ? 0 : 4 * c.degree_sum) +
+                      12 * c.candidates;
   });
 }
 
