@@ -295,9 +295,9 @@ def run_ours(args, rank, world, local):
     vehicles = cfg0.vehicle_count
 
     # ---- device-resident throughput (value) ---------------------------------
-    # K back-to-back iterations enqueued without host sync, each bracketed by
-    # CUDA events on the engine stream; a 512 MiB memset flushes L2 between
-    # iterations outside the events.
+    # K back-to-back iterations enqueued without host sync (one CUDA graph
+    # each), each bracketed by exactly two CUDA events on the engine stream; a
+    # 512 MiB memset flushes L2 before every iteration, outside the events.
     eng = make_engine(wl, local, rank, world, fresh_uid())
     eng.step(args.warmup)
     c0 = eng.counters()
@@ -305,16 +305,31 @@ def run_ours(args, rank, world, local):
     if dist:
         dist.barrier()
     with ClockSampler(local) as clk:
-        walk, stepms = eng.bench_steps(args.steps, L2_FLUSH_BYTES)
+        _, stepms = eng.bench_steps(args.steps, L2_FLUSH_BYTES, "step")
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     c1 = eng.counters()
-    walk_ms, step_ms = float(walk.sum()), float(stepms.sum())
+    step_ms = float(stepms.sum())
     ant_steps = c1.ant_steps - c0.ant_steps
     routes = c1.vehicle_routes - c0.vehicle_routes
     alg_bytes = c1.walk_bytes - c0.walk_bytes
     kernels = c1.kernels_per_step
+    eng.close()
+
+    # walk kernel split (roofline): the same K iterations replayed on a fresh,
+    # identically seeded engine (the run is deterministic), two events per
+    # iteration around stage B only
+    engw = make_engine(wl, local, rank, world, fresh_uid())
+    engw.step(args.warmup)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    walk, _ = engw.bench_steps(args.steps, L2_FLUSH_BYTES, "walk")
+    torch.cuda.synchronize()
+    assert engw.counters().ant_steps == c1.ant_steps, "walk replay diverged from the timed run"
+    engw.close()
+    walk_ms = float(walk.sum())
 
     # chained (no flush, multi-step CUDA graphs), for reference
     chained_s, chained_steps = 1.0, 0

@@ -273,9 +273,11 @@ int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
  * paper_2010_14244_b200/csrc/device.cuh). */
 int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
 /* Benchmark entry point: enqueues `steps` engine steps without host
- * synchronization, each bracketed by CUDA events on the engine stream
- * (walk kernel, whole step), with an L2-flushing memset of flush_bytes
- * between steps outside the events; returns per-step device times. */
+ * synchronization (one CUDA graph per step), with an L2-flushing memset of
+ * flush_bytes before each step outside the timed span; returns per-step
+ * device times.  Pass step_ms only (events: begin, end of step), walk_ms only
+ * (begin, end of the stage-B walk; the rest of the step runs untimed), or
+ * both (three events; each event node costs ~2-3 us of serialization). */
 int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms);
 
 const char* gmaco_last_error(const gmaco_engine* h);

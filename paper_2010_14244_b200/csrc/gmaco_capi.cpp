@@ -276,6 +276,14 @@ struct gmaco_engine {
   cudaGraphExec_t graph_big = nullptr, graph_one = nullptr;
   cudaGraphExec_t tgraph_big = nullptr, tgraph_one = nullptr;
   cudaGraphExec_t graph_walk = nullptr, graph_tail = nullptr;  // bench split
+  // bench graph: [L2 flush memset] -> ev0 -> step (walk, ev1, tail) -> ev2; the
+  // three event-record nodes are retargeted per launch to that step's events
+  cudaGraph_t bench_tmpl = nullptr;
+  cudaGraphExec_t bench_exec = nullptr;
+  cudaGraphNode_t bench_ev_node[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t bench_ev[3] = {nullptr, nullptr, nullptr};
+  int64_t bench_flush = -1;
+  int bench_mode = 0;
   void* flush = nullptr;
   int64_t flush_bytes = 0;
   std::vector<cudaEvent_t> ev_begin, ev_end;  // timing mode, kGraphSteps pairs
@@ -290,6 +298,10 @@ struct gmaco_engine {
 
   ~gmaco_engine() {
     if (device >= 0) cudaSetDevice(device);
+    if (bench_exec) cudaGraphExecDestroy(bench_exec);
+    if (bench_tmpl) cudaGraphDestroy(bench_tmpl);
+    for (auto e : bench_ev)
+      if (e) cudaEventDestroy(e);
     for (auto ge : {graph_big, graph_one, tgraph_big, tgraph_one, graph_walk, graph_tail})
       if (ge) cudaGraphExecDestroy(ge);
     if (flush) cudaFree(flush);
@@ -1471,36 +1483,87 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
   });
 }
 
+// One graph per timed step: the L2 flush (outside the timed span), then the
+// step bracketed by three event-record nodes (begin, walk end, step end).
+// mode: 1 = step only (ev0, step, ev2), 2 = walk only (ev0, walk, ev1, tail),
+// 3 = both.  Every event-record node serializes the GPU (~2-3 us on B200),
+// so the headline leg brackets each step with exactly two.
+void build_bench_graph(gmaco_engine* h, int64_t flush_bytes, int mode) {
+  if (h->bench_exec) cudaGraphExecDestroy(h->bench_exec);
+  if (h->bench_tmpl) cudaGraphDestroy(h->bench_tmpl);
+  h->bench_exec = nullptr;
+  h->bench_tmpl = nullptr;
+  for (auto& e : h->bench_ev)
+    if (!e) CK(cudaEventCreate(&e));
+  StepResources r = h->res;
+  r.capturing = true;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = cudaSuccess;
+  if (flush_bytes > 0) err = cudaMemsetAsync(h->flush, 0x5a, flush_bytes, h->stream);
+  if (err == cudaSuccess) err = launch_step(h->w, r, h->stream, h->bench_ev[0], (mode & 2) ? h->bench_ev[1] : nullptr);
+  if (err == cudaSuccess && (mode & 1))
+    err = cudaEventRecordWithFlags(h->bench_ev[2], h->stream, cudaEventRecordExternal);
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &h->bench_tmpl);
+  CK(err);
+  CK(e2);
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(h->bench_tmpl, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CK(cudaGraphGetNodes(h->bench_tmpl, nodes.data(), &nn));
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t));
+    if (t != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e = nullptr;
+    CK(cudaGraphEventRecordNodeGetEvent(nd, &e));
+    for (int k = 0; k < 3; ++k)
+      if (e == h->bench_ev[k]) h->bench_ev_node[k] = nd;
+  }
+  if (!h->bench_ev_node[0] || ((mode & 2) && !h->bench_ev_node[1]) || ((mode & 1) && !h->bench_ev_node[2]))
+    throw std::runtime_error("bench graph: event node not found");
+  CK(cudaGraphInstantiate(&h->bench_exec, h->bench_tmpl, 0));
+  CK(cudaGraphUpload(h->bench_exec, h->stream));
+  h->bench_flush = flush_bytes;
+  h->bench_mode = mode;
+}
+
 int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms) {
   if (!h || steps < 0) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     refresh_ctl(h);
     *h->stop_host = h->ctl_host->step + steps;
     CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
-    if (!h->graph_walk) h->graph_walk = capture_part(h, 1);
-    if (!h->graph_tail) h->graph_tail = capture_part(h, 2);
     if (flush_bytes > 0 && h->flush_bytes < flush_bytes) {
       if (h->flush) cudaFree(h->flush);
       CK(cudaMalloc(&h->flush, flush_bytes));
       h->flush_bytes = flush_bytes;
+      h->bench_flush = -1;
+    }
+    const int mode = (step_ms ? 1 : 0) | (walk_ms ? 2 : 0);
+    if (!mode) throw ValidationError("bench_steps: walk_ms or step_ms required");
+    if (!h->bench_exec || h->bench_flush != flush_bytes || h->bench_mode != mode) {
+      for (auto& nd : h->bench_ev_node) nd = nullptr;
+      build_bench_graph(h, flush_bytes, mode);
     }
     std::vector<cudaEvent_t> ev(3 * (size_t)steps);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     for (int32_t i = 0; i < steps; ++i) {
-      if (flush_bytes > 0) CK(cudaMemsetAsync(h->flush, i & 0xff, flush_bytes, h->stream));
-      CK(cudaEventRecord(ev[3 * i], h->stream));
-      CK(cudaGraphLaunch(h->graph_walk, h->stream));
-      CK(cudaEventRecord(ev[3 * i + 1], h->stream));
-      CK(cudaGraphLaunch(h->graph_tail, h->stream));
-      CK(cudaEventRecord(ev[3 * i + 2], h->stream));
+      for (int k = 0; k < 3; ++k)
+        if (h->bench_ev_node[k])
+          CK(cudaGraphExecEventRecordNodeSetEvent(h->bench_exec, h->bench_ev_node[k], ev[3 * i + k]));
+      CK(cudaGraphLaunch(h->bench_exec, h->stream));
     }
     CK(cudaStreamSynchronize(h->stream));
     for (int32_t i = 0; i < steps; ++i) {
       float a = 0.f, b = 0.f;
-      CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
-      CK(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 2]));
-      if (walk_ms) walk_ms[i] = a;
-      if (step_ms) step_ms[i] = b;
+      if (walk_ms) {
+        CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+        walk_ms[i] = a;
+      }
+      if (step_ms) {
+        CK(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 2]));
+        step_ms[i] = b;
+      }
     }
     for (auto& e : ev) cudaEventDestroy(e);
     refresh_ctl(h);

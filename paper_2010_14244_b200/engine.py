@@ -202,12 +202,16 @@ class Engine:
     def set_timing(self, on: bool):
         self._check(self.L.gmaco_set_timing(self.h, int(on)))
 
-    def bench_steps(self, steps: int, flush_bytes: int):
-        """Per-step device times (walk kernel, whole step) in ms of `steps`
-        back-to-back steps with an L2 flush between them (outside the events)."""
-        walk = np.zeros(steps, dtype=np.float64)
-        step = np.zeros(steps, dtype=np.float64)
-        self._check(self.L.gmaco_bench_steps(self.h, steps, flush_bytes, abi.ptr(walk, f64), abi.ptr(step, f64)))
+    def bench_steps(self, steps: int, flush_bytes: int, what: str = "both"):
+        """Per-step device times in ms of `steps` back-to-back steps with an L2
+        flush before each (outside the events).  what = "step" (whole step,
+        two events), "walk" (stage-B walk, two events) or "both" (three
+        events); returns (walk, step), None for the leg not timed."""
+        walk = np.zeros(steps, dtype=np.float64) if what in ("walk", "both") else None
+        step = np.zeros(steps, dtype=np.float64) if what in ("step", "both") else None
+        self._check(self.L.gmaco_bench_steps(self.h, steps, flush_bytes,
+                                             abi.ptr(walk, f64) if walk is not None else None,
+                                             abi.ptr(step, f64) if step is not None else None))
         return walk, step
 
     def debug_trace(self, steps: int = 1) -> np.ndarray:

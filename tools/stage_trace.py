@@ -1,23 +1,31 @@
-"""Per-stage latency of one engine step from the device stage trace."""
+"""Per-stage latency of one engine step from the device stage trace.
+
+  python tools/stage_trace.py            warm and L2-flushed traces at V=10 and V=1000 (C2 grid)
+"""
+import os
 import sys
 
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 from paper_2010_14244_b200 import abi, networks  # noqa: E402
 from paper_2010_14244_b200.engine import Engine  # noqa: E402
 
 net = networks.grid(32, 32, signals="all")
-import os
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for V in (10, 1000):
     cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive", vehicle_count=V,
                                                    seed=1, max_steps=100), 64)
     e = Engine(net, cfg, net.grid_distance())
     e.step(5)
-    for rep in range(3):
-        raw = e.debug_trace(1)
-        t = raw.astype(np.int64)
-        rel = (t - t[0]) / 1e3
-        print(f"{os.environ.get('TAG', '')} V={V} walk: staged {rel[1]:.2f} end {rel[2]:.2f} | "
-              f"tail start {rel[3]:.2f} signals {rel[5]:.2f} FG {rel[6]:.2f} (us) | max epilogue cycles: "
-              f"rebuild+deposit {raw[7]} take_edge {raw[8]} move {raw[9]} | walk(loop..epilogue start) {raw[10]} | block0 reduce {raw[11]}")
+    for mode in ("warm", "flushed"):
+        for rep in range(3):
+            if mode == "flushed":
+                flush.fill_(rep + 1)
+                torch.cuda.synchronize()
+            raw = e.debug_trace(1)
+            t = raw.astype(np.int64)
+            rel = (t - t[0]) / 1e3
+            print(f"{os.environ.get('TAG', '')} V={V} {mode:7s} walk: staged {rel[1]:.2f} end {rel[2]:.2f} | "
+                  f"tail start {rel[3]:.2f} signals {rel[5]:.2f} FG {rel[6]:.2f} (us)")
