@@ -228,7 +228,10 @@ int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64
 
 /* Executes up to `steps` engine steps (sequential_step, engine.cpp:352-400),
  * stopping early once finished() (engine.cpp:146-152) holds.  `executed`
- * (may be NULL) receives the number of steps run. */
+ * (may be NULL) receives the number of steps run.  With executed == NULL the
+ * call returns once the steps are enqueued on the engine's stream (steps past
+ * finished() are no-ops); every later read (gmaco_get_*, gmaco_collect, ...)
+ * is ordered after them. */
 int gmaco_step(gmaco_engine* h, int64_t steps, int64_t* executed);
 /* finished(w) (engine.cpp:146-152). */
 int gmaco_finished(gmaco_engine* h, int32_t* out);
@@ -264,8 +267,9 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
                     const int32_t* dest, const uint64_t* rng_entity, const uint64_t* rng_step,
                     int64_t n_t, int32_t* out_next, int32_t* out_via, uint8_t* out_deviated);
 
-/* Device event timing of the last gmaco_step call's kernels (ms), for the
- * bench roofline: walk kernel total and whole-step total. */
+/* Device event timing of the last gmaco_step call's kernels (ms): walk
+ * kernel total and whole-step total.  Recorded only while timing is enabled
+ * (gmaco_set_timing), since every event serializes the stream (~2-3 us). */
 int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches);
 int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
 /* Profiling hook: runs `steps` steps and returns the last one's stage

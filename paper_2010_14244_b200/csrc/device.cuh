@@ -85,6 +85,7 @@ struct DevParams {
   int32_t max_degree;       // largest out-degree (general-graph walker bound)
   int32_t csr_walker;       // colony runs on k_colony_csr (bitmaps + nrow built)
   int32_t ant_queue;        // csr walker in scratch mode: prologue / ant-queue walk / epilogue kernels
+  int32_t pdl;              // cooperative tail launched as a programmatic dependent of the walk
   int32_t record_paths;
 };
 
@@ -175,6 +176,8 @@ struct DevWorld {
   int4* rec;          // [M] ant-queue walker slot records {weight, head node, head row}; weight half
                       //     rewritten with `weight` (nullptr unless p.ant_queue)
   int64_t* ecost;     // [m] colony tour cost per edge for the coming step
+  int32_t* ecost32;   // [M] int32 copy for the lattice walker's SMEM staging when
+                      //     max len * (1 + V) < 2^31 (nullptr otherwise)
   int32_t* occ_cur;   // [m] edge occupancy of the previous step (engine.hpp:166)
   int32_t* occ_new;   // [m] being accumulated this step
   int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)

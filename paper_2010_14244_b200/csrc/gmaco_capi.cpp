@@ -271,6 +271,11 @@ struct gmaco_engine {
   DevCtl* ctl = nullptr;
   DevCtl* ctl_host = nullptr;  // pinned mirror
   int64_t* stop_host = nullptr;
+  int64_t stop_written = -1;  // last stop_at value enqueued to the device
+  bool ctl_valid = false;     // ctl_host mirrors the device control block
+  bool pending = false;       // steps enqueued without a host sync
+  void* stage = nullptr;      // pinned staging for batched device->host reads
+  size_t stage_bytes = 0;
   StepResources res;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph_big = nullptr, graph_one = nullptr;
@@ -311,6 +316,7 @@ struct gmaco_engine {
     if (ev_b) cudaEventDestroy(ev_b);
     if (ctl_host) cudaFreeHost(ctl_host);
     if (stop_host) cudaFreeHost(stop_host);
+    if (stage) cudaFreeHost(stage);
     if (stream) cudaStreamDestroy(stream);
     destroy_comm();
   }
@@ -329,9 +335,16 @@ namespace {
 thread_local std::string g_create_err;
 
 template <class F>
-int guarded(gmaco_engine* h, F&& f) {
+int guarded(gmaco_engine* h, F&& f, bool stream_ordered = false) {
   try {
     if (h) CK(cudaSetDevice(h->device));
+    // steps enqueued by gmaco_step(executed = NULL) may still be running on
+    // the (non-blocking) engine stream: settle them before any entry point
+    // that reads or writes device state outside that stream's order
+    if (h && h->pending && !stream_ordered) {
+      CK(cudaStreamSynchronize(h->stream));
+      h->pending = false;
+    }
     f();
     return GMACO_OK;
   } catch (const ValidationError& e) {
@@ -700,6 +713,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
   // debugging / A-B switches (defaults are the production configuration)
   p.prefetch = std::getenv("GMACO_NO_PREFETCH") ? 0 : 1;
+  p.pdl = std::getenv("GMACO_NO_PDL") ? 0 : 1;
   p.no_smem = std::getenv("GMACO_NO_SMEM") ? 1 : 0;
   p.max_degree = maxdeg;
   // general-graph colony walker: progress-filter bitmaps + next-row
@@ -795,6 +809,16 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.tau = B.upload(tau);
   w.weight = B.upload(wt);
   w.ecost = B.upload(ecost);
+  {  // int32 tour costs for the lattice walker's SMEM staging: load <= V, so
+     // every cost len * (1 + load) <= max len * (1 + V) must stay below 2^31
+    int64_t maxlen = 0;
+    for (int64_t L : g.len) maxlen = std::max(maxlen, L);
+    if (lattice_walker && (long double)maxlen * (1.0L + V) < 2147483648.0L) {
+      std::vector<int32_t> e32(M);
+      for (int32_t s = 0; s < M; ++s) e32[s] = (int32_t)ecost[s];
+      w.ecost32 = B.upload(e32);
+    }
+  }
   w.occ_cur = B.filled<int32_t>(M, 0);
   w.occ_new = B.filled<int32_t>(M, 0);
   w.dep = B.filled<int64_t>(M, 0);
@@ -941,11 +965,40 @@ cudaGraphExec_t capture(gmaco_engine* h, int steps, bool timing) {
 void refresh_ctl(gmaco_engine* h) {
   CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  h->ctl_valid = true;
   if (h->ctl_host->error) throw std::runtime_error("device path buffer overflow");
 }
 
-int64_t run_steps(gmaco_engine* h, int64_t steps) {
-  refresh_ctl(h);
+// Step graphs never overshoot a target (32-step graphs launch only while at
+// least 32 steps remain), so the device-side stop marker stays unbounded and
+// is written once instead of once per call.
+void unbound_stop(gmaco_engine* h) {
+  if (h->stop_written == INT64_MAX) return;
+  *h->stop_host = INT64_MAX;
+  CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+  h->stop_written = INT64_MAX;
+}
+
+// need_count = false: the steps stay enqueued (no final host sync); the
+// control-block mirror is refreshed by the next synchronizing call (e.g. the
+// batched gmaco_get_vehicles), so a step/read loop costs one round trip.
+int64_t run_steps(gmaco_engine* h, int64_t steps, bool need_count = true) {
+  if (!need_count && !h->timing) {  // enqueue only: no mirror needed (steps past finished() are no-ops)
+    if (steps <= 0) return -1;
+    unbound_stop(h);
+    for (int64_t i = 0; i < steps / kGraphSteps; ++i) {
+      if (!h->graph_big) h->graph_big = capture(h, kGraphSteps, false);
+      CK(cudaGraphLaunch(h->graph_big, h->stream));
+    }
+    for (int64_t i = 0; i < steps % kGraphSteps; ++i) {
+      if (!h->graph_one) h->graph_one = capture(h, 1, false);
+      CK(cudaGraphLaunch(h->graph_one, h->stream));
+    }
+    h->ctl_valid = false;
+    h->pending = true;
+    return -1;
+  }
+  if (!h->ctl_valid) refresh_ctl(h);  // else the mirror from the last synchronizing call is current
   const int64_t start = h->ctl_host->step;
   if (steps <= 0 || h->ctl_host->done) return 0;
   const int64_t target = start + steps;
@@ -957,11 +1010,11 @@ int64_t run_steps(gmaco_engine* h, int64_t steps) {
       CK(cudaEventCreate(&h->ev_end[i]));
     }
   }
-  *h->stop_host = target;
-  CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+  unbound_stop(h);
+  h->ctl_valid = false;
   h->last_walk_ms = 0.0;
   h->last_walk_launches = 0;
-  CK(cudaEventRecord(h->ev_a, h->stream));
+  if (h->timing) CK(cudaEventRecord(h->ev_a, h->stream));  // event nodes serialize the GPU: opt-in
   int64_t cur = start;
   while (cur < target && !h->ctl_host->done) {
     const int64_t remaining = target - cur;
@@ -989,10 +1042,10 @@ int64_t run_steps(gmaco_engine* h, int64_t steps) {
       cur += 1;
     }
   }
-  CK(cudaEventRecord(h->ev_b, h->stream));
+  if (h->timing) CK(cudaEventRecord(h->ev_b, h->stream));
   refresh_ctl(h);
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, h->ev_a, h->ev_b));
+  if (h->timing) CK(cudaEventElapsedTime(&ms, h->ev_a, h->ev_b));
   h->last_step_ms = ms;
   return h->ctl_host->step - start;
 }
@@ -1139,6 +1192,7 @@ int gmaco_nccl_unique_id(void* out128) {
 }
 
 int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id) {
+  if (h) h->ctl_valid = false;
   if (!h || !nccl_id || world < 1 || rank < 0 || rank >= world) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const int32_t V = h->w.p.V;
@@ -1158,6 +1212,7 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
 }
 
 int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
+  if (h) h->ctl_valid = false;
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     set_shard(h, lo, hi, 0);
@@ -1166,12 +1221,12 @@ int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
 }
 
 int gmaco_step_split(gmaco_engine* h, int32_t part) {
+  if (h) h->ctl_valid = false;
   if (!h || (part != 1 && part != 2)) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     if (part == 1) {
       refresh_ctl(h);
-      *h->stop_host = h->ctl_host->step + 1;
-      CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+      unbound_stop(h);
       if (!h->graph_walk) h->graph_walk = capture_part(h, 1);
       CK(cudaGraphLaunch(h->graph_walk, h->stream));
     } else {
@@ -1198,6 +1253,7 @@ int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits
 }
 
 int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64_t* deposits) {
+  if (h) h->ctl_valid = false;
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const DevWorld& w = h->w;
@@ -1237,9 +1293,9 @@ int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist,
 int gmaco_step(gmaco_engine* h, int64_t steps, int64_t* executed) {
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
-    const int64_t k = run_steps(h, steps);
+    const int64_t k = run_steps(h, steps, executed != nullptr);
     if (executed) *executed = k;
-  });
+  }, /*stream_ordered=*/true);
 }
 
 int gmaco_finished(gmaco_engine* h, int32_t* out) {
@@ -1284,6 +1340,7 @@ int gmaco_get_pheromone(gmaco_engine* h, int64_t* tau) {
 }
 
 int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
+  if (h) h->ctl_valid = false;
   if (!h || !tau) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const int32_t m = h->M;
@@ -1315,38 +1372,67 @@ int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
   return guarded(h, [&] {
     const DevVehicles& d = h->w.v;
     const size_t V = h->w.p.V;
-    auto cp = [&](auto* dst, const auto* src) {
-      if (dst) CK(cudaMemcpy(dst, src, V * sizeof(*dst), cudaMemcpyDeviceToHost));
+    // requested fields: async copies into one pinned staging buffer, one
+    // stream sync, then host copies out (one round trip instead of one per field)
+    std::vector<std::pair<void*, size_t>> outs;  // (user dst, staging offset)
+    std::vector<std::pair<const void*, size_t>> srcs;
+    size_t total = 0;
+    auto plan = [&](void* dst, const void* src, size_t elem) {
+      if (!dst) return;
+      outs.emplace_back(dst, total);
+      srcs.emplace_back(src, V * elem);
+      total += (V * elem + 15) & ~size_t(15);
     };
-    cp(v->origin, d.origin);
-    cp(v->dest, d.dest);
-    cp(v->advance_mm, d.advance);
-    cp(v->state, d.state);
-    cp(v->at_node, d.at_node);
-    cp(v->progress_mm, d.progress);
-    cp(v->overshoot_mm, d.overshoot);
-    cp(v->queued_phase, d.queued_phase);
-    cp(v->queue_joined_step, d.joined);
-    cp(v->depart_step, d.depart);
-    cp(v->arrive_step, d.arrive);
-    cp(v->latency_debt_us, d.latency_debt);
-    cp(v->driving_steps, d.driving);
-    cp(v->queued_steps, d.queued);
-    cp(v->latency_steps, d.lat_steps);
-    cp(v->decisions, d.decisions);
-    cp(v->deviations, d.deviations);
-    cp(v->path_length_mm, d.path_len_mm);
-    if (v->on_edge) {
-      auto oe = download(d.on_edge, V);
-      for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
+    plan(v->origin, d.origin, 4);
+    plan(v->dest, d.dest, 4);
+    plan(v->advance_mm, d.advance, 8);
+    plan(v->state, d.state, 1);
+    plan(v->at_node, d.at_node, 4);
+    plan(v->progress_mm, d.progress, 8);
+    plan(v->overshoot_mm, d.overshoot, 8);
+    plan(v->queued_phase, d.queued_phase, 4);
+    plan(v->queue_joined_step, d.joined, 8);
+    plan(v->depart_step, d.depart, 8);
+    plan(v->arrive_step, d.arrive, 8);
+    plan(v->latency_debt_us, d.latency_debt, 8);
+    plan(v->driving_steps, d.driving, 8);
+    plan(v->queued_steps, d.queued, 8);
+    plan(v->latency_steps, d.lat_steps, 8);
+    plan(v->decisions, d.decisions, 4);
+    plan(v->deviations, d.deviations, 4);
+    plan(v->path_length_mm, d.path_len_mm, 8);
+    const size_t oe_off = total;
+    if (v->on_edge) total += V * 4;
+    total += 16;  // never empty: the control block copy + sync always run
+    {
+      if (h->stage_bytes < total) {
+        if (h->stage) cudaFreeHost(h->stage);
+        h->stage = nullptr;
+        CK(cudaMallocHost(&h->stage, total));
+        h->stage_bytes = total;
+      }
+      char* st = static_cast<char*>(h->stage);
+      for (size_t i = 0; i < outs.size(); ++i)
+        CK(cudaMemcpyAsync(st + outs[i].second, srcs[i].first, srcs[i].second, cudaMemcpyDeviceToHost, h->stream));
+      if (v->on_edge) CK(cudaMemcpyAsync(st + oe_off, d.on_edge, V * 4, cudaMemcpyDeviceToHost, h->stream));
+      // the control block rides along: the mirror is current after this sync
+      CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      h->pending = false;
+      h->ctl_valid = true;
+      if (h->ctl_host->error) throw std::runtime_error("device path buffer overflow");
+      for (size_t i = 0; i < outs.size(); ++i) std::memcpy(outs[i].first, st + outs[i].second, srcs[i].second);
+      if (v->on_edge) {
+        const int32_t* oe = reinterpret_cast<const int32_t*>(st + oe_off);
+        for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
+      }
     }
     if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
       for (size_t i = 0; i < V; ++i)
         v->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
     }
-  });
+  }, /*stream_ordered=*/true);
 }
-
 int gmaco_signal_count(gmaco_engine* h, int32_t* out) {
   if (!h || !out) return GMACO_EVALIDATION;
   *out = h->S;
@@ -1531,8 +1617,8 @@ int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, doubl
   if (!h || steps < 0) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     refresh_ctl(h);
-    *h->stop_host = h->ctl_host->step + steps;
-    CK(cudaMemcpyAsync(&h->ctl->stop_at, h->stop_host, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    unbound_stop(h);
+    h->ctl_valid = false;
     if (flush_bytes > 0 && h->flush_bytes < flush_bytes) {
       if (h->flush) cudaFree(h->flush);
       CK(cudaMalloc(&h->flush, flush_bytes));
@@ -1573,6 +1659,7 @@ int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, doubl
 // Profiling hook: stage timestamps (%globaltimer ns) of the next `steps`
 // steps' LAST step; see DevCtl::trace.  Not part of the reference surface.
 int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12) {
+  if (h) h->ctl_valid = false;
   if (!h || !out12) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     for (int32_t i = 0; i < steps; ++i) {

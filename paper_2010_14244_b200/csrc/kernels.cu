@@ -71,6 +71,17 @@ __device__ __forceinline__ uint4 philox4_rk(uint4 c, const uint32_t* rk) {
   }
   return c;
 }
+// Rounds [R0, R1) of philox4_rk, so callers can interleave a block's rounds
+// with independent dependent chains (warps issue in order).
+template <int R0, int R1>
+__device__ __forceinline__ void philox_rounds(uint4& c, const uint32_t* rk) {
+#pragma unroll
+  for (int r = R0; r < R1; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0);
+  }
+}
 __device__ __forceinline__ uint64_t philox_half(uint4 o, int32_t hop) {
   return (hop & 1) ? (((uint64_t)o.z << 32) | o.w) : (((uint64_t)o.x << 32) | o.y);
 }
@@ -911,6 +922,11 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
   if (threadIdx.x == 0) flush_counters(w.ctl, t);
 }
 
+// Programmatic dependent launch (sm_90+): the dependent grid waits here for
+// the full completion (and memory flush) of the grid it depends on.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // 256-bit read-only global load (sm_100a LDG.256): two slot records per
 // instruction, halving L1 wavefronts for lane-divergent rows.
 __device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
@@ -1140,6 +1156,7 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
 }
 
 __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
+  griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
   if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block
     if (w.p.prefetch) prefetch_tail_state(w);
@@ -1405,6 +1422,7 @@ enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 
 template <bool kSmem, int kTour>
 __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
+  griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
   if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
@@ -1429,29 +1447,27 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   const DevVehicles& v = w.v;
   const double* __restrict__ W = w.weight;
   const int64_t* __restrict__ Cst = w.ecost;
-  const int32_t* sdeg = nullptr;
+  const int32_t* Cst32 = nullptr;  // staged int32 tour costs (host-checked bound)
   __shared__ __align__(8) uint64_t stage_bar;
   if (kSmem) {
     // Stage this step's weight / tour-cost tables and the degree table in
     // shared memory with three TMA bulk copies (cp.async.bulk) completing on
     // one mbarrier; the other threads overlap the vehicle prologue below.
-    const uint32_t bW = 8u * (uint32_t)w.g.M, bD = 4u * (uint32_t)w.g.n;
+    const uint32_t bW = 8u * (uint32_t)w.g.M, bC = 4u * (uint32_t)w.g.M;
     if (threadIdx.x == 0) {
       const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dyn_smem);
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bW + bD) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bW + bC) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                    ::"r"(dst), "l"(w.weight), "r"(bW), "r"(bar) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst + bW), "l"(w.ecost), "r"(bW), "r"(bar) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst + 2 * bW), "l"(w.g.deg), "r"(bD), "r"(bar) : "memory");
+                   ::"r"(dst + bW), "l"(w.ecost32), "r"(bC), "r"(bar) : "memory");
     }
     W = reinterpret_cast<const double*>(dyn_smem);
-    Cst = reinterpret_cast<const int64_t*>(dyn_smem + bW);
-    sdeg = reinterpret_cast<const int32_t*>(dyn_smem + 2 * bW);
+    Cst32 = reinterpret_cast<const int32_t*>(dyn_smem + bW);
+
   }
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
@@ -1513,6 +1529,8 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     int32_t* tp = kTour == kTourScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
     tour = tp;
     int32_t idegs = 0;
+    const int32_t rows = w.d.rows;
+    int32_t rr = rx, cq = cx;
     int32_t n_two = 0;  // hops with two candidates (candidates = n + n_two)
     unsigned long long mbits = 0;  // move_v per hop, first hop in the most significant used bit
     // Direction-slotted lattice rows: slot 4x+{0,1,2,3} = {up, left, right,
@@ -1545,12 +1563,15 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       const unsigned tb = (unsigned)two & ((bad & (unsigned)(u2 >= 1.0)) | (~bad & (unsigned)!(pt < wa)));
       const unsigned mv = tb ? (unsigned)!a_is_v : (unsigned)a_is_v;
       const int32_t s = xb + (mv ? off_v : off_h);
-      cost += Cst[s];
+      cost += kSmem ? (int64_t)Cst32[s] : Cst[s];
       if (kTour == kTourScratch) *tp++ = s;
       if (kTour == kTourBits) mbits = (mbits << 1) | mv;
-      idegs += kSmem ? sdeg[x] : __ldg(w.g.deg + x);
+      // out-degree of x on the validated full lattice (degree_sum counter)
+      idegs += (rr > 0) + (rr < rows - 1) + (cq > 0) + (cq < cols - 1);
       n_two += two;
       x += mv ? step_v : step_h;
+      rr += mv ? dr : 0;
+      cq += mv ? 0 : dc;
       rem_v -= mv;
       rem_h -= mv ^ 1u;
     };
@@ -1564,8 +1585,11 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       uint4 cur = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, 0u), w.p.rk);
       const int32_t pairs = n >> 1;
       for (int32_t p = 0; p < pairs; ++p) {
-        const uint4 nxt = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)p + 1u), w.p.rk);
+        // next block's rounds split across the pair's two dependent hops
+        uint4 nxt = make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)p + 1u);
+        philox_rounds<0, 5>(nxt, w.p.rk);
         hop(((uint64_t)cur.x << 32) | cur.y);
+        philox_rounds<5, 10>(nxt, w.p.rk);
         hop(((uint64_t)cur.z << 32) | cur.w);
         cur = nxt;
       }
@@ -1971,6 +1995,7 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
     w.weight[s] = wt;
     if (w.rec) *reinterpret_cast<double*>(w.rec + s) = wt;
     w.ecost[s] = cost;
+    if (w.ecost32) w.ecost32[s] = (int32_t)cost;  // bound checked on the host
   }
   return occ;
 }
@@ -2119,6 +2144,7 @@ __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
 // ---------------------------------------------------------------------------
 template <bool kFusedMotion>
 __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
+  griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
   if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) trace_min(w.ctl, 3);
@@ -2260,9 +2286,10 @@ constexpr int kTail = 64;
 // Dynamic shared memory of the staged grid walker (0 = read from global):
 // weight + tour-cost tables, 16 B per slot, when they fit 96 KiB.
 size_t grid_smem_bytes(const DevWorld& w) {
-  // TMA bulk copies need 16-byte multiples: M is a multiple of 4 (ELL-4), n of 4
-  const size_t bytes = 16 * (size_t)w.g.M + 4 * (size_t)w.g.n;
-  return (!w.p.no_smem && w.g.n % 4 == 0 && bytes <= (96u << 10)) ? bytes : 0;
+  // staged: f64 weights + int32 tour costs (TMA bulk copies need 16-byte
+  // multiples: M is a multiple of 4 on the ELL-4 lattice)
+  const size_t bytes = 12 * (size_t)w.g.M;
+  return (!w.p.no_smem && w.ecost32 && bytes <= (96u << 10)) ? bytes : 0;
 }
 
 cudaError_t configure_kernels() {
@@ -2403,11 +2430,15 @@ tail:
     lc.blockDim = dim3(kTailCoop);
     lc.dynamicSmemBytes = 0;
     lc.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    // programmatic dependent launch: the tail's CTAs are scheduled while the
+    // walk drains and wait in griddepcontrol.wait for its completion + memory
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = w.p.pdl ? 2 : 1;
     return fused ? cudaLaunchKernelEx(&lc, k_tail_coop<true>, w) : cudaLaunchKernelEx(&lc, k_tail_coop<false>, w);
   }
   if (S > 0) k_signals<<<blocks_for(S, kTail), kTail, 0, st>>>(w);

@@ -107,7 +107,12 @@ class Engine:
         self.close()
 
     # -- stepping ---------------------------------------------------------------
-    def step(self, n: int = 1) -> int:
+    def step(self, n: int = 1, count: bool = True):
+        """Run up to n steps; returns the number executed, or None with
+        count=False (steps only enqueued; later reads are ordered after them)."""
+        if not count:
+            self._check(self.L.gmaco_step(self.h, n, None))
+            return None
         k = i64()
         self._check(self.L.gmaco_step(self.h, n, C.byref(k)))
         return k.value

@@ -336,3 +336,24 @@ def test_colony_rgg_max_hops_cap():
         cpu.step(k)
         _same_snapshot(gpu, cpu, "rgg max_hops")
     assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_async_step_then_read_equals_oracle():
+    """gmaco_step with executed == NULL only enqueues; the batched
+    gmaco_get_vehicles read (which also refreshes the control block) is
+    ordered after it.  Stepping past finished() stays a no-op."""
+    net = networks.grid(10, 10, signals="all")
+    cfg = abi.colony_production(_cfg("colony", 150, 4, max_steps=30), ants=32)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for _ in range(12):
+        assert gpu.step(1, count=False) is None
+        cpu.step(1)
+        _same_snapshot(gpu, cpu, "async step")
+    assert gpu.current_step() == cpu.current_step()
+    for _ in range(40):  # runs past max_steps: extra enqueued steps are no-ops
+        gpu.step(1, count=False)
+    cpu.step(40)
+    assert gpu.finished() and cpu.finished()
+    assert gpu.current_step() == cpu.current_step()
+    assert O.results_identical(gpu.collect(), cpu.collect())

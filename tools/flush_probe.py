@@ -12,6 +12,6 @@ net = networks.grid(32, 32, signals="all")
 for fb in (0, 1 << 20, 128 << 20, 512 << 20, 0):
     e = Engine(net, bench.workload_config(1, 100000), net.grid_distance())
     e.step(5)
-    w, s = e.bench_steps(100, fb)
-    print(f"flush {fb >> 20:4d} MiB: step p50 {np.median(s) * 1e3:.2f} us  walk p50 {np.median(w) * 1e3:.2f} us")
+    _, s = e.bench_steps(100, fb, "step")
+    print(f"flush {fb >> 20:4d} MiB: step p50 {np.median(s) * 1e3:.2f} us")
     e.close()
