@@ -14,6 +14,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <unordered_map>
+#include <mutex>
+#include <cstdio>
 #include <cmath>
 #include <cstdarg>
 #include <cstdlib>
@@ -219,20 +222,107 @@ void reverse_csr(const HostGraph& g, std::vector<int32_t>& rptr, std::vector<int
   }
 }
 
+// ---- create-phase profiler (GMACO_CREATE_PROFILE=1 prints to stderr) -------
+struct PhaseTimer {
+  bool on = std::getenv("GMACO_CREATE_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gmaco create] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // ---- device buffers --------------------------------------------------------
+// Process-wide pinned host memory: cudaMallocHost costs milliseconds per
+// call, so engines take blocks from 4 MiB slabs and return them on destroy.
+class PinnedPool {
+ public:
+  static void* take(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    std::lock_guard<std::mutex> lk(mu());
+    auto& fr = free_list();
+    for (size_t i = 0; i < fr.size(); ++i)
+      if (fr[i].second >= bytes) {
+        void* p = fr[i].first;
+        if (fr[i].second > bytes) {
+          fr[i].first = static_cast<char*>(p) + bytes;
+          fr[i].second -= bytes;
+        } else {
+          fr.erase(fr.begin() + i);
+        }
+        sizes()[p] = bytes;
+        return p;
+      }
+    const size_t slab = std::max(bytes, size_t(4) << 20);
+    void* s = nullptr;
+    CK(cudaMallocHost(&s, slab));
+    if (slab > bytes) fr.emplace_back(static_cast<char*>(s) + bytes, slab - bytes);
+    sizes()[s] = bytes;
+    return s;
+  }
+  static void give(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu());
+    auto it = sizes().find(p);
+    if (it == sizes().end()) return;
+    free_list().emplace_back(p, it->second);
+    sizes().erase(it);
+  }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<std::pair<void*, size_t>>& free_list() {
+    static auto* v = new std::vector<std::pair<void*, size_t>>();  // process lifetime
+    return *v;
+  }
+  static std::unordered_map<void*, size_t>& sizes() {
+    static auto* m = new std::unordered_map<void*, size_t>();
+    return *m;
+  }
+};
+
+// Device allocations of one engine.  Direct mode (default): one cudaMalloc
+// and one synchronous copy per array.  Arena mode (build_world): arrays under
+// kArenaMax are sub-allocated (256-B aligned) from kChunk device chunks and
+// their contents are written into a host shadow of each chunk; flush() sends
+// every chunk in one copy.  gmaco_create then costs a handful of CUDA calls
+// instead of ~100 mallocs and synchronous copies.  Until flush() no kernel
+// may touch arena memory and no other writer may target it.
 struct DevBuffers {
+  static constexpr size_t kChunk = size_t(8) << 20, kArenaMax = size_t(1) << 20, kAlign = 256;
+  struct Chunk {
+    char* dev = nullptr;
+    std::unique_ptr<char[]> shadow;  // uninitialized: only written ranges are touched / sent
+    size_t used = 0, sent = 0;       // [sent, used) not yet on the device
+  };
   std::vector<void*> ptrs;
+  std::vector<Chunk> chunks;
+  bool arena = false;
   template <class T>
   T* alloc(size_t n) {
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    if (arena && bytes <= kArenaMax) return static_cast<T*>(carve(bytes, nullptr));
     void* p = nullptr;
-    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMalloc(&p, bytes));
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
   template <class T>
   T* upload(const std::vector<T>& h) {
+    const size_t bytes = h.size() * sizeof(T);
+    if (arena && bytes && bytes <= kArenaMax) {
+      T* d = static_cast<T*>(carve(bytes, nullptr));
+      std::memcpy(shadow_of(d), h.data(), bytes);
+      return d;
+    }
     T* d = alloc<T>(h.size());
-    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!h.empty()) CK(cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice));
     return d;
   }
   template <class T>
@@ -240,8 +330,47 @@ struct DevBuffers {
     std::vector<T> h(n, value);
     return upload(h);
   }
+  template <class T>
+  T* upload_one(const T& v) {
+    return upload(std::vector<T>{v});
+  }
+  // Sends every arena chunk's not-yet-sent range to the device (one copy per
+  // chunk); ranges already sent are device-authoritative from then on.
+  void flush() {
+    for (auto& ch : chunks)
+      if (ch.used > ch.sent) {
+        CK(cudaMemcpy(ch.dev + ch.sent, ch.shadow.get() + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice));
+        ch.sent = ch.used;
+      }
+  }
+  void seal() {
+    flush();
+    for (auto& ch : chunks) ch.shadow.reset();
+    arena = false;
+  }
   ~DevBuffers() {
     for (void* p : ptrs) cudaFree(p);
+    for (auto& ch : chunks) cudaFree(ch.dev);
+  }
+
+ private:
+  void* carve(size_t bytes, const void*) {
+    const size_t need = (bytes + kAlign - 1) & ~(kAlign - 1);
+    if (chunks.empty() || chunks.back().used + need > kChunk) {
+      Chunk ch;
+      CK(cudaMalloc(&ch.dev, kChunk));
+      ch.shadow.reset(new char[kChunk]);
+      chunks.push_back(std::move(ch));
+    }
+    Chunk& ch = chunks.back();
+    void* p = ch.dev + ch.used;
+    ch.used += need;
+    return p;
+  }
+  char* shadow_of(const void* d) {
+    for (auto& ch : chunks)
+      if (d >= ch.dev && d < ch.dev + kChunk) return ch.shadow.get() + (static_cast<const char*>(d) - ch.dev);
+    throw std::runtime_error("arena: pointer outside every chunk");
   }
 };
 
@@ -314,9 +443,9 @@ struct gmaco_engine {
     for (auto e : ev_end) cudaEventDestroy(e);
     if (ev_a) cudaEventDestroy(ev_a);
     if (ev_b) cudaEventDestroy(ev_b);
-    if (ctl_host) cudaFreeHost(ctl_host);
-    if (stop_host) cudaFreeHost(stop_host);
-    if (stage) cudaFreeHost(stage);
+    PinnedPool::give(ctl_host);
+    // stop_host lives inside the ctl_host pinned block
+    PinnedPool::give(stage);
     if (stream) cudaStreamDestroy(stream);
     destroy_comm();
   }
@@ -490,8 +619,10 @@ Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
 
 void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distance_desc* dd,
                  const gmaco_sim_config* cfg) {
+  PhaseTimer pt0;
   build_graph(gd, h->g);
   validate_config(cfg);
+  pt0.mark("graph + config validation");
   if (!dd) throw ValidationError("distance descriptor is null");
   HostGraph& g = h->g;
   const int32_t n = g.n, m = g.m;
@@ -503,7 +634,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       throw ValidationError(fmt("node %d out-degree exceeds the engine bound of %d", u, kMaxDegree));
 
   DevBuffers& B = h->buf;
+  B.arena = true;  // sub-allocate + shadow small arrays; sealed (one copy per chunk) below
   DevWorld& w = h->w;
+  PhaseTimer pt;
 
   // ---- distance service ---------------------------------------------------
   DistHost dh;
@@ -573,8 +706,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   } else {
     throw ValidationError(fmt("unknown distance kind %d", dd->kind));
   }
+  pt.mark("distance service (host)");
   // ---- spawn (host, engine.cpp:71-114) -------------------------------------
   Spawned sp = spawn(c, g, dh, targets);
+  pt.mark("spawn (host)");
   const int32_t V = c.vehicle_count;
   // all host-side validation is done: from here on the device is required
   int dev_count = 0;
@@ -583,6 +718,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   CK(cudaSetDevice(h->device));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CK(configure_kernels());
+  pt.mark("device init");
   if (!table.empty()) w.d.table = B.upload(table);
   if (!slot_of.empty()) w.d.slot_of = B.upload(slot_of);
 
@@ -674,6 +810,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.g.slot_from = B.upload(slot_from);
   w.g.eta_beta = B.upload(eta);
 
+  pt.mark("graph slots + upload");
   // ---- params ----------------------------------------------------------------
   DevParams& p = w.p;
   p.algorithm = alg;
@@ -849,6 +986,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   ds.head_wait = B.filled<double>((size_t)S * kPhases, 0.0);
   ds.rem = B.filled<double>((size_t)S * kPhases, 0.0);
 
+  pt.mark("params, tables, pheromone, signals");
   // ---- vehicles ------------------------------------------------------------
   DevVehicles& dv = w.v;
   dv.origin = B.upload(sp.origin);
@@ -890,7 +1028,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       rec[s] = make_int4(0, 0, hd, ((row[hd].x >> 2) << 5) | deg[hd]);
     }
     w.rec = B.upload(rec);
+    B.flush();  // the kernel below reads arena arrays
     CK(sync_rec_weights(w, h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // before any later flush rewrites the chunk
     dv.walk_start = B.filled<int32_t>(V, -1);
     dv.walk_dec = B.filled<uint8_t>(V, 0);
     dv.best_key = B.filled<unsigned long long>(V, ~0ull);
@@ -902,6 +1042,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan_step = B.filled<int64_t>(V, -1);
   dv.plan_done = B.filled<uint8_t>(V, 0);
 
+  pt.mark("vehicles");
   // ---- control block -----------------------------------------------------------
   DevCtl c0{};
   c0.step = 0;
@@ -910,12 +1051,15 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   for (int32_t vid = 0; vid < V; ++vid) n0 += sp.depart[vid] == 0;  // count_active at step 0
   c0.n_t = n0;
   c0.done = c.max_steps <= 0 ? 1 : 0;
-  h->ctl = B.alloc<DevCtl>(1);
-  CK(cudaMemcpy(h->ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
+  h->ctl = B.upload_one(c0);
   w.ctl = h->ctl;
-  CK(cudaMallocHost(&h->ctl_host, sizeof(DevCtl)));
+  {  // one pinned block: control-block mirror + stop marker
+    void* pin = PinnedPool::take(sizeof(DevCtl) + 64);
+    h->ctl_host = static_cast<DevCtl*>(pin);
+    h->stop_host = reinterpret_cast<int64_t*>(static_cast<char*>(pin) + sizeof(DevCtl));
+  }
   *h->ctl_host = c0;
-  CK(cudaMallocHost(&h->stop_host, sizeof(int64_t)));
+  pt.mark("ctl upload + pinned mirror");
   if (p.need_positions) {
     h->res.scan_temp_bytes = scan_temp_bytes(V);
     h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
@@ -923,9 +1067,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   h->res.coop_blocks = coop_tail_blocks(w, h->device);
   h->res.queue_blocks = queue_blocks(w, h->device);
   if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");
+  pt.mark("occupancy queries");
+  B.seal();
+  pt.mark("arena seal (copies)");
   CK(cudaEventCreate(&h->ev_a));
   CK(cudaEventCreate(&h->ev_b));
   CK(cudaDeviceSynchronize());
+  pt.mark("control block, occupancy, sync");
 }
 
 // part 1 = stage-B walk kernel only, part 2 = the rest of the step (C..G)
@@ -1406,9 +1554,9 @@ int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
     total += 16;  // never empty: the control block copy + sync always run
     {
       if (h->stage_bytes < total) {
-        if (h->stage) cudaFreeHost(h->stage);
+        PinnedPool::give(h->stage);
         h->stage = nullptr;
-        CK(cudaMallocHost(&h->stage, total));
+        h->stage = PinnedPool::take(total);
         h->stage_bytes = total;
       }
       char* st = static_cast<char*>(h->stage);
