@@ -347,7 +347,7 @@ def run_ours(args, rank, world, local):
         eng2.close()
 
     # ---- end to end through the C ABI from host buffers (e2e) ---------------
-    e2e_dt, e2e_steps, completed = 1.0, 0, None
+    e2e_dt, e2e_steps, completed, e2e_phases = 1.0, 0, None, None
     h2d = net.edge_count * (4 + 4 + 8 + 4) + net.node_count * 1
     d2h = vehicles * 5
     if not args.skip_extra:
@@ -359,12 +359,17 @@ def run_ours(args, rank, world, local):
         st = np.zeros(vehicles, dtype=np.uint8)
         oe = np.zeros(vehicles, dtype=np.int32)
         view = abi.VehicleView(state=abi.ptr(st, C.c_uint8), on_edge=abi.ptr(oe, C.c_int32))
+        t1 = time.perf_counter()
         e.step(args.warmup)
+        t2 = time.perf_counter()
         for _ in range(args.steps):
             e.step(1, count=False)  # enqueue; the read below is the step's one round trip
             e._check(e.L.gmaco_get_vehicles(e.h, C.byref(view)))  # the step's decisions back to host
+        t3 = time.perf_counter()
         res = e.collect()
         e2e_dt = time.perf_counter() - t0
+        e2e_phases = {"create_ms": 1e3 * (t1 - t0), "warmup_ms": 1e3 * (t2 - t1),
+                      "loop_us_per_step": 1e6 * (t3 - t2) / args.steps, "collect_ms": 1e3 * (e2e_dt - (t3 - t0))}
         e2e_steps = e.counters().ant_steps
         completed = res[0].completed_count
         e.close()
@@ -432,7 +437,8 @@ def run_ours(args, rank, world, local):
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h,
                 "includes": "gmaco_create from host arrays (H2D), warmup+timed steps, per-step D2H of "
-                            "vehicle states, gmaco_collect"},
+                            "vehicle states, gmaco_collect",
+                "phases": e2e_phases},
         "clocks": clk.summary(),
         "completed_vehicles_e2e": completed,
     }

@@ -258,7 +258,8 @@ class PinnedPool {
       }
     const size_t slab = std::max(bytes, size_t(4) << 20);
     void* s = nullptr;
-    CK(cudaMallocHost(&s, slab));
+    // mapped: kernels write readbacks straight into it (k_pack)
+    CK(cudaHostAlloc(&s, slab, cudaHostAllocMapped | cudaHostAllocPortable));
     if (slab > bytes) fr.emplace_back(static_cast<char*>(s) + bytes, slab - bytes);
     sizes()[s] = bytes;
     return s;
@@ -1560,11 +1561,17 @@ int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
         h->stage_bytes = total;
       }
       char* st = static_cast<char*>(h->stage);
-      for (size_t i = 0; i < outs.size(); ++i)
-        CK(cudaMemcpyAsync(st + outs[i].second, srcs[i].first, srcs[i].second, cudaMemcpyDeviceToHost, h->stream));
-      if (v->on_edge) CK(cudaMemcpyAsync(st + oe_off, d.on_edge, V * 4, cudaMemcpyDeviceToHost, h->stream));
-      // the control block rides along: the mirror is current after this sync
-      CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream));
+      char* st_dev = nullptr;
+      void* ctl_dev = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), h->stage, 0));
+      CK(cudaHostGetDevicePointer(&ctl_dev, h->ctl_host, 0));
+      // one gather kernel into mapped pinned memory; the control block rides
+      // along, so the host mirror is current after the single sync
+      PackDesc pd;
+      for (size_t i = 0; i < outs.size(); ++i) pd.f[pd.n++] = PackField{srcs[i].first, st_dev + outs[i].second, srcs[i].second};
+      if (v->on_edge) pd.f[pd.n++] = PackField{d.on_edge, st_dev + oe_off, V * 4};
+      pd.f[pd.n++] = PackField{h->ctl, ctl_dev, sizeof(DevCtl)};
+      CK(launch_pack(pd, h->stream));
       CK(cudaStreamSynchronize(h->stream));
       h->pending = false;
       h->ctl_valid = true;

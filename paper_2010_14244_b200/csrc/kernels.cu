@@ -2327,6 +2327,33 @@ cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Gathers several device arrays into mapped pinned host memory in one launch
+// (the batched readback of gmaco_get_vehicles: one kernel + one sync instead
+// of one copy per field).
+__global__ void k_pack(PackDesc d) {
+  const PackField f = d.f[blockIdx.y];
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(f.src) | reinterpret_cast<uintptr_t>(f.dst)) & 15) == 0;
+  size_t done = 0;
+  if (vec) {
+    const size_t n16 = f.bytes / 16;
+    for (size_t i = tid; i < n16; i += stride)
+      reinterpret_cast<uint4*>(f.dst)[i] = reinterpret_cast<const uint4*>(f.src)[i];
+    done = n16 * 16;
+  }
+  for (size_t i = done + tid; i < f.bytes; i += stride)
+    static_cast<char*>(f.dst)[i] = static_cast<const char*>(f.src)[i];
+}
+
+cudaError_t launch_pack(const PackDesc& d, cudaStream_t st) {
+  if (d.n <= 0) return cudaSuccess;
+  size_t mx = 0;
+  for (int i = 0; i < d.n; ++i) mx = std::max(mx, d.f[i].bytes);
+  const unsigned bx = (unsigned)std::min<size_t>(std::max<size_t>((mx / 16 + 255) / 256, 1), 1024);
+  k_pack<<<dim3(bx, d.n), 256, 0, st>>>(d);
+  return cudaGetLastError();
+}
+
 int queue_blocks(const DevWorld& w, int device) {
   if (!w.p.ant_queue) return 0;
   int per_sm = 0, sms = 0;

@@ -32,6 +32,17 @@ int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
+// Batched gather of device arrays into (mapped pinned) host memory.
+struct PackField {
+  const void* src;
+  void* dst;  // device-visible pointer
+  size_t bytes;
+};
+struct PackDesc {
+  PackField f[24];
+  int n = 0;
+};
+cudaError_t launch_pack(const PackDesc& d, cudaStream_t st);
 // Copies `weight` into the weight half of the slot records (ant-queue walker).
 cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st);
 void colony_shape(int ants, int* threads, int* vpb);
