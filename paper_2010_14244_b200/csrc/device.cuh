@@ -81,7 +81,8 @@ struct DevParams {
   // the others' decisions arrive through the exchange (k_apply_remote)
   int32_t shard_lo, shard_hi, sharded;
   int32_t no_smem;          // A/B switch: read the walk tables from global memory
-  int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (walks <= 64 hops)
+  int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (SMEM words)
+  int32_t bit_words;        // 64-hop move-bit words per ant (ceil(plan_cap / 64))
   int32_t max_degree;       // largest out-degree (general-graph walker bound)
   int32_t csr_walker;       // colony runs on k_colony_csr (bitmaps + nrow built)
   int32_t ant_queue;        // csr walker in scratch mode: prologue / ant-queue walk / epilogue kernels

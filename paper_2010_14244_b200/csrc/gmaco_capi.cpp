@@ -912,13 +912,16 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.plan_cap = alg == GMACO_COLONY ? std::max(walk_bound, 1) : 1;
   if (alg == GMACO_COLONY && (size_t)V * p.plan_cap * 4 > (size_t(32) << 30))
     throw ValidationError("colony: planned-tour storage exceeds 32 GiB (set colony.max_hops)");
-  // Tours on the lattice fast path with <= 64-hop walks live in registers as
-  // move bits; otherwise scratch mode keeps every ant's tour (no winner
+  // Tours on the lattice fast path live as move bits (one bit per hop, SMEM);
+  // otherwise scratch mode keeps every ant's tour (no winner
   // replay) when it fits 48 GiB of the B200's 180 GB; larger colonies replay
   // the winner instead.
   const bool lattice_walker = alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter &&
                               p.ants <= 256;
-  p.grid_bits = lattice_walker && p.plan_cap <= 64 && !std::getenv("GMACO_NO_BITS");
+  // move bits: 1 bit per hop in 64-hop SMEM words per ant, when a CTA's
+  // words fit 48 KB (lattice CTAs hold <= 256 ants)
+  p.bit_words = (p.plan_cap + 63) / 64;
+  p.grid_bits = lattice_walker && (size_t)256 * p.bit_words * 8 <= (size_t(48) << 10) && !std::getenv("GMACO_NO_BITS");
   p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits && !std::getenv("GMACO_NO_SCRATCH") &&
                    (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(48) << 30);
   if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound

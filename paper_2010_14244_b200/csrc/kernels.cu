@@ -1402,6 +1402,9 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
 }
 
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ size_t grid_staged_bytes_dev(const DevWorld& w) {
+  return (12 * (size_t)w.g.M + 15) & ~size_t(15);  // f64 weights + int32 costs (kSmem variant)
+}
 // B (colony) on a validated uniform lattice (GMACO_DIST_GRID, progress filter
 // on).  The distance service is closed-form and the lattice is checked at
 // create, so a node's candidate set needs no loads at all: the strictly
@@ -1421,7 +1424,7 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
 enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 
 template <bool kSmem, int kTour>
-__global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
+__global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
   if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
@@ -1435,7 +1438,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
   __shared__ int32_t done_s[kMaxVpb];
   __shared__ uint8_t deciding_s[kMaxVpb];
   __shared__ long long red5[7][32];
-  __shared__ unsigned long long bits_s[kTour == kTourBits ? 256 : 1];
+  // move-bit words [blockDim][bit_words] after the staged tables (kTourBits)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int K = w.p.ants;
   const int vpb = blockDim.x / K;
@@ -1469,6 +1472,9 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     Cst32 = reinterpret_cast<const int32_t*>(dyn_smem + bW);
 
   }
+  const int nw = w.p.bit_words;
+  unsigned long long* const bits_w =
+      reinterpret_cast<unsigned long long*>(dyn_smem + (kSmem ? grid_staged_bytes_dev(w) : 0));
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
     uint8_t st = v.state[vid];
@@ -1532,7 +1538,8 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     const int32_t rows = w.d.rows;
     int32_t rr = rx, cq = cx;
     int32_t n_two = 0;  // hops with two candidates (candidates = n + n_two)
-    unsigned long long mbits = 0;  // move_v per hop, first hop in the most significant used bit
+    unsigned long long mbits = 0;  // move_v per hop of the current 64-hop word
+    int32_t hb = 0, wj = 0;        // hops in the current word, words flushed
     // Direction-slotted lattice rows: slot 4x+{0,1,2,3} = {up, left, right,
     // down} (holes at the border), i.e. ascending neighbour id.  With the
     // walk direction fixed, the candidate slots are per-walk constants: when
@@ -1565,7 +1572,13 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       const int32_t s = xb + (mv ? off_v : off_h);
       cost += kSmem ? (int64_t)Cst32[s] : Cst[s];
       if (kTour == kTourScratch) *tp++ = s;
-      if (kTour == kTourBits) mbits = (mbits << 1) | mv;
+      if (kTour == kTourBits) {  // 64 hops per word, first hop of a word at bit 63
+        mbits = (mbits << 1) | mv;
+        if (++hb == 64) {
+          bits_w[threadIdx.x * nw + wj++] = mbits;
+          hb = 0;
+        }
+      }
       // out-degree of x on the validated full lattice (degree_sum counter)
       idegs += (rr > 0) + (rr < rows - 1) + (cq > 0) + (cq < cols - 1);
       n_two += two;
@@ -1600,7 +1613,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
     steps = n;
     degs = idegs;
     cands = n + n_two;
-    if (kTour == kTourBits) bits_s[threadIdx.x] = mbits;
+    if (kTour == kTourBits && hb) bits_w[threadIdx.x * nw + wj] = mbits << (64 - hb);  // left-aligned
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
     if (kTour == kTourBits && (K & 31) == 0) {
@@ -1612,23 +1625,27 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       asm volatile("bar.sync %0, %1;" ::"r"(1 + lv), "r"(K) : "memory");
       if (ant < 32) {
         const int winner = (int)(best[lv] & 1023u);
-        const unsigned long long wbits = bits_s[lv * K + winner];
+        const unsigned long long* wb = bits_w + (size_t)(lv * K + winner) * nw;
         const bool reached = hops == abs(rd - rx) + abs(cd - cx);
         const bool dep = reached && w.p.deposit == 1;
         const int64_t amount = dep ? w.dep_amount[hops] : 0;
         int32_t* plan = v.plan + (size_t)vid * w.p.plan_cap;
+        int32_t before = 0;  // vertical moves in the words before word j
+        for (int32_t j = 0; 64 * j < hops; ++j) {
+          const unsigned long long word = wb[j];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int32_t i = ant + 32 * j;
-          if (i < hops) {
-            const unsigned long long head = i ? (wbits >> (hops - i)) : 0ull;  // first i move bits
-            const int32_t nv = __popcll(head);
-            const int32_t y = start + step_v * nv + step_h * (i - nv);
-            const unsigned mv = (unsigned)(wbits >> (hops - 1 - i)) & 1u;
-            const int32_t sl = 4 * y + (mv ? off_v : off_h);
-            plan[i] = sl;
-            if (dep) atomicAdd((unsigned long long*)&w.dep[sl], (unsigned long long)amount);
+          for (int t = 0; t < 2; ++t) {
+            const int32_t r = ant + 32 * t, i = 64 * j + r;
+            if (i < hops) {
+              const int32_t nv = before + (r ? __popcll(word >> (64 - r)) : 0);  // vertical moves before hop i
+              const int32_t y = start + step_v * nv + step_h * (i - nv);
+              const unsigned mv = (unsigned)(word >> (63 - r)) & 1u;
+              const int32_t sl = 4 * y + (mv ? off_v : off_h);
+              plan[i] = sl;
+              if (dep) atomicAdd((unsigned long long*)&w.dep[sl], (unsigned long long)amount);
+            }
           }
+          before += __popcll(word);
         }
         if (ant == 0) {
           const bool deciding = deciding_s[lv];
@@ -1636,7 +1653,7 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
           v.plan_step[vid] = step;
           v.plan_done[vid] = reached && hops > 0;
           if (deciding) {
-            const unsigned mv0 = (unsigned)(wbits >> (hops - 1)) & 1u;
+            const unsigned mv0 = (unsigned)(wb[0] >> 63) & 1u;
             take_edge(w, vid, 4 * start + (mv0 ? off_v : off_h), false, start);
           }
           routes = 1;
@@ -1661,10 +1678,10 @@ __global__ void __launch_bounds__(256) k_colony_grid(DevWorld w) {
       int32_t first = -1;
       if (kTour == kTourBits) {  // rebuild the winner's tour from its move bits
         tour = v.plan + (size_t)vid * w.p.plan_cap;
-        const unsigned long long wb = bits_s[lv * K + winner];
+        const unsigned long long* wb = bits_w + (size_t)(lv * K + winner) * nw;
         int32_t y = start;
         for (int32_t i = 0; i < hops; ++i) {
-          const unsigned mv = (unsigned)(wb >> (hops - 1 - i)) & 1u;
+          const unsigned mv = (unsigned)(wb[i >> 6] >> (63 - (i & 63))) & 1u;
           const int32_t sl = 4 * y + (mv ? off_v : off_h);
           tour[i] = sl;
           if (dep) atomicAdd((unsigned long long*)&w.dep[sl], (unsigned long long)amount);
@@ -2292,9 +2309,15 @@ size_t grid_smem_bytes(const DevWorld& w) {
   return (!w.p.no_smem && w.ecost32 && bytes <= (96u << 10)) ? bytes : 0;
 }
 
+// Move-bit words of a CTA (kTourBits): [threads][bit_words] u64.
+size_t grid_bits_bytes(const DevWorld& w, int threads) {
+  return w.p.grid_bits ? (size_t)threads * w.p.bit_words * 8 : 0;
+}
+
 cudaError_t configure_kernels() {
-  for (auto f : {k_colony_grid<true, kTourBits>, k_colony_grid<true, kTourScratch>, k_colony_grid<true, kTourReplay>}) {
-    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+  for (auto f : {k_colony_grid<true, kTourBits>, k_colony_grid<true, kTourScratch>, k_colony_grid<true, kTourReplay>,
+                 k_colony_grid<false, kTourBits>}) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 << 10);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -2382,7 +2405,8 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
     // vehicle's colony per CTA when it fills whole warps
     const int threads = smem ? (256 / w.p.ants) * w.p.ants : ((w.p.ants % 32 == 0) ? w.p.ants : 256);
     const unsigned grid = blocks_for(VS, threads / w.p.ants) + 1;  // +1: prefetch CTA
-#define GMACO_GRID(SM, MODE) k_colony_grid<SM, MODE><<<grid, threads, SM ? smem : 0, st>>>(w)
+    const size_t dyn = smem + grid_bits_bytes(w, threads);  // staged tables, then move-bit words
+#define GMACO_GRID(SM, MODE) k_colony_grid<SM, MODE><<<grid, threads, dyn, st>>>(w)
     if (smem) {
       if (mode == kTourBits) GMACO_GRID(true, kTourBits);
       else if (mode == kTourScratch) GMACO_GRID(true, kTourScratch);

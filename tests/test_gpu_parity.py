@@ -357,3 +357,25 @@ def test_async_step_then_read_equals_oracle():
     assert gpu.finished() and cpu.finished()
     assert gpu.current_step() == cpu.current_step()
     assert O.results_identical(gpu.collect(), cpu.collect())
+
+
+@pytest.mark.parametrize("shape,ants", [((40, 40), 64), ((40, 40), 20), ((70, 72), 64)])
+def test_colony_lattice_multiword_move_bits(shape, ants):
+    """Lattice walks longer than 64 hops keep one move bit per hop in several
+    64-hop SMEM words (2 words at 40x40, 3 at 70x72); the winner's tour is
+    rebuilt from prefix popcounts across words (warp epilogue for K % 32 == 0,
+    serial otherwise).  Planned tours, pheromone and state bit-exact."""
+    R, Cc = shape
+    net = networks.grid(R, Cc, signals="interior")
+    cfg = abi.colony_production(_cfg("colony", 250, 17, max_steps=40), ants=ants)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for k in (1, 2, 6):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, f"multiword {shape} K={ants}")
+        for vid in range(0, 250, 5):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
+        assert getattr(a, f) == getattr(b, f), f
