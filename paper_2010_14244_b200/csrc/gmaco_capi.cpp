@@ -1257,6 +1257,8 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -1273,9 +1275,12 @@ NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(l, "ncclCommInitRank"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(l, "ncclAllGather"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(l, "ncclAllReduce"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(l, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(l, "ncclGroupEnd"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(l, "ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(l, "ncclGetErrorString"));
-    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.CommDestroy)
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.CommDestroy ||
+        !api.GroupStart || !api.GroupEnd)
       throw std::runtime_error("NCCL runtime lacks required symbols");
     api.lib = l;
   }
@@ -1295,12 +1300,14 @@ cudaError_t nccl_exchange(void* ctx, cudaStream_t st) {
   auto* h = static_cast<gmaco_engine*>(ctx);
   const DevWorld& w = h->w;
   const size_t P = h->shard_pad;
-  if (nccl().AllGather(w.v.dec_rec + (size_t)h->rank * P, w.v.dec_rec, P, ncclInt32, h->comm, st) != ncclSuccess)
-    return cudaErrorUnknown;
-  if (w.p.deposit == GMACO_DEPOSIT_BEST_TOUR &&
-      nccl().AllReduce(w.dep, w.dep, (size_t)w.g.M, ncclInt64, ncclSum, h->comm, st) != ncclSuccess)
-    return cudaErrorUnknown;
-  return cudaSuccess;
+  // both collectives in one NCCL group: a single fused launch per step
+  const NcclApi& N = nccl();
+  if (N.GroupStart() != ncclSuccess) return cudaErrorUnknown;
+  ncclResult_t r = N.AllGather(w.v.dec_rec + (size_t)h->rank * P, w.v.dec_rec, P, ncclInt32, h->comm, st);
+  if (r == ncclSuccess && w.p.deposit == GMACO_DEPOSIT_BEST_TOUR)
+    r = N.AllReduce(w.dep, w.dep, (size_t)w.g.M, ncclInt64, ncclSum, h->comm, st);
+  const ncclResult_t e = N.GroupEnd();
+  return (r == ncclSuccess && e == ncclSuccess) ? cudaSuccess : cudaErrorUnknown;
 }
 
 void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
