@@ -1070,6 +1070,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   }
   h->res.coop_blocks = coop_tail_blocks(w, h->device);
   h->res.queue_blocks = queue_blocks(w, h->device);
+  CK(configure_grid_carveout(w));
   if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");
   pt.mark("occupancy queries");
   B.seal();

@@ -1423,7 +1423,11 @@ __device__ __forceinline__ size_t grid_staged_bytes_dev(const DevWorld& w) {
 //                  rebuilt arithmetically into v.plan.  No per-hop stores.
 enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 
-template <bool kSmem, int kTour>
+// kOneVeh: the CTA holds exactly one vehicle's colony (threads == K, K a
+// multiple of 32), so its per-vehicle barrier is the literal id 1: ptxas then
+// reserves 2 named barriers instead of 16, which would otherwise cap the SM
+// at 4 resident CTAs.
+template <bool kSmem, int kTour, bool kOneVeh = false>
 __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
@@ -1622,7 +1626,10 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       // lane i rebuilds hops i and i+32 directly from the winner's move bits
       // (node after i hops = start + step_v*popc(first i bits) + step_h*rest)
       // and issues their deposits; lane 0 does the bookkeeping and motion.
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + lv), "r"(K) : "memory");
+      if (kOneVeh)
+        asm volatile("bar.sync 1, %0;" ::"r"(K) : "memory");
+      else
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + lv), "r"(K) : "memory");
       if (ant < 32) {
         const int winner = (int)(best[lv] & 1023u);
         const unsigned long long* wb = bits_w + (size_t)(lv * K + winner) * nw;
@@ -2314,9 +2321,31 @@ size_t grid_bits_bytes(const DevWorld& w, int threads) {
   return w.p.grid_bits ? (size_t)threads * w.p.bit_words * 8 : 0;
 }
 
+// Shared-memory carveout of the non-staged lattice walker: just enough SMEM
+// for the register-limited number of CTAs per SM (move-bit words + static
+// arrays), the rest stays L1 for the weight / cost gathers.  Without it the
+// driver favours L1 and the move-bit words cap residency (5 CTAs instead of 12
+// on C5).
+cudaError_t configure_grid_carveout(const DevWorld& w) {
+  if (!w.p.grid_bits || grid_smem_bytes(w)) return cudaSuccess;
+  const int K = w.p.ants, threads = (K % 32 == 0) ? K : 256;
+  cudaFuncAttributes fa{};
+  const bool one = threads == K;
+  cudaError_t e = one ? cudaFuncGetAttributes(&fa, k_colony_grid<false, kTourBits, true>)
+                      : cudaFuncGetAttributes(&fa, k_colony_grid<false, kTourBits>);
+  if (e != cudaSuccess) return e;
+  const int regs_blocks = 65536 / std::max(1, fa.numRegs * threads);
+  const size_t per_block = fa.sharedSizeBytes + grid_bits_bytes(w, threads) + 1024;  // + per-CTA reserve
+  const size_t need = per_block * std::max(1, std::min(regs_blocks, 32));
+  const int pct = (int)std::min<size_t>(100, (need * 100 + (228u << 10) - 1) / (228u << 10));
+  return one ? cudaFuncSetAttribute(k_colony_grid<false, kTourBits, true>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct)
+             : cudaFuncSetAttribute(k_colony_grid<false, kTourBits>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 cudaError_t configure_kernels() {
   for (auto f : {k_colony_grid<true, kTourBits>, k_colony_grid<true, kTourScratch>, k_colony_grid<true, kTourReplay>,
-                 k_colony_grid<false, kTourBits>}) {
+                 k_colony_grid<false, kTourBits>, k_colony_grid<false, kTourBits, true>}) {
     const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 << 10);
     if (e != cudaSuccess) return e;
   }
@@ -2412,7 +2441,9 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       else if (mode == kTourScratch) GMACO_GRID(true, kTourScratch);
       else GMACO_GRID(true, kTourReplay);
     } else {
-      if (mode == kTourBits) GMACO_GRID(false, kTourBits);
+      if (mode == kTourBits && threads == w.p.ants)
+        k_colony_grid<false, kTourBits, true><<<grid, threads, dyn, st>>>(w);
+      else if (mode == kTourBits) GMACO_GRID(false, kTourBits);
       else if (mode == kTourScratch) GMACO_GRID(false, kTourScratch);
       else GMACO_GRID(false, kTourReplay);
     }

@@ -32,6 +32,7 @@ int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
+cudaError_t configure_grid_carveout(const DevWorld& w);
 // Batched gather of device arrays into (mapped pinned) host memory.
 struct PackField {
   const void* src;
