@@ -379,3 +379,57 @@ def test_colony_lattice_multiword_move_bits(shape, ants):
     a, b = gpu.counters(), cpu.counters()
     for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
         assert getattr(a, f) == getattr(b, f), f
+
+
+def _hub_graph(hub_degree, seed=5):
+    """12x12 grid plus hubs whose out-degree is raised to `hub_degree` by
+    bidirectional shortcut edges (shorter than the grid path, so the progress
+    filter keeps them as candidates)."""
+    base = networks.grid(12, 12, signals="interior")
+    rng = np.random.default_rng(seed)
+    n = base.node_count
+    src, dst = list(base.edge_from), list(base.edge_to)
+    ln, la = list(base.edge_length_mm), list(base.edge_lanes)
+    have = set(zip(src, dst))
+    deg = np.bincount(np.asarray(src), minlength=n)
+    for hub in (13, 40, 77, 101, 130):
+        others = [v for v in rng.permutation(n) if v != hub]
+        for v in others:
+            if deg[hub] >= hub_degree:
+                break
+            if (hub, v) in have or (v, hub) in have:
+                continue
+            for a, b in ((hub, v), (v, hub)):
+                src.append(a); dst.append(b)
+                ln.append(int(rng.integers(150_000, 900_000))); la.append(2)
+                have.add((a, b)); deg[a] += 1
+    return networks.Network(node_count=n, signalized=base.signalized.copy(),
+                            edge_from=np.asarray(src, np.int32), edge_to=np.asarray(dst, np.int32),
+                            edge_length_mm=np.asarray(ln, np.int64), edge_lanes=np.asarray(la, np.int32))
+
+
+@pytest.mark.parametrize("hub_degree,mode", [(14, "queue"), (14, "block"), (14, "replay"), (20, "generic")])
+def test_colony_wide_rows(hub_degree, mode, monkeypatch):
+    """Rows wider than the queue walker's 8-slot register window (span 16 on
+    the 4-aligned CSR layout) and, at degree 20, beyond the CSR walkers'
+    16-slot bound (generic kernel); dense distance tables."""
+    if mode == "replay":
+        monkeypatch.setenv("GMACO_NO_SCRATCH", "1")
+    if mode == "block":
+        monkeypatch.setenv("GMACO_NO_QUEUE", "1")
+    net = _hub_graph(hub_degree)
+    maxdeg = np.bincount(net.edge_from).max()
+    assert (8 < maxdeg <= 16) if hub_degree <= 16 else maxdeg > 16
+    cfg = abi.colony_production(_cfg("colony", 300, 23, max_steps=40), ants=32)
+    gpu = Engine(net, cfg)
+    cpu = O.PortWorld(net, cfg)
+    for k in (1, 3, 8):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, f"hubs {hub_degree} {mode}")
+        for vid in range(0, 300, 3):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert O.results_identical(gpu.run(), cpu.run())
