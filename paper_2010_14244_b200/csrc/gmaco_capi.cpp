@@ -187,27 +187,6 @@ void validate_config(const gmaco_sim_config* c) {
 }
 
 // ---- Dijkstra to a destination over reversed edges (net.cpp:359-383) ------
-void dijkstra_to(const HostGraph& g, const std::vector<int32_t>& rptr, const std::vector<int32_t>& rsrc,
-                 const std::vector<int32_t>& redge, int32_t dst, int64_t* dist) {
-  std::fill(dist, dist + g.n, kInf);
-  using Item = std::pair<int64_t, int32_t>;
-  std::priority_queue<Item, std::vector<Item>, std::greater<>> heap;
-  dist[dst] = 0;
-  heap.emplace(0, dst);
-  while (!heap.empty()) {
-    auto [d, u] = heap.top();
-    heap.pop();
-    if (d != dist[u]) continue;
-    for (int32_t k = rptr[u]; k < rptr[u + 1]; ++k) {
-      const int64_t nd = d + g.len[redge[k]];
-      if (nd < dist[rsrc[k]]) {
-        dist[rsrc[k]] = nd;
-        heap.emplace(nd, rsrc[k]);
-      }
-    }
-  }
-}
-
 void reverse_csr(const HostGraph& g, std::vector<int32_t>& rptr, std::vector<int32_t>& rsrc,
                  std::vector<int32_t>& redge) {
   rptr.assign(g.n + 1, 0);
@@ -305,6 +284,16 @@ struct DevBuffers {
   std::vector<void*> ptrs;
   std::vector<Chunk> chunks;
   bool arena = false;
+  cudaStream_t stream = nullptr;  // flushes are ordered on the engine stream
+  // Always a dedicated allocation: for arrays a kernel writes before seal()
+  // (a later flush of the arena must never overwrite them).
+  template <class T>
+  T* alloc_direct(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
   template <class T>
   T* alloc(size_t n) {
     const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
@@ -338,11 +327,15 @@ struct DevBuffers {
   // Sends every arena chunk's not-yet-sent range to the device (one copy per
   // chunk); ranges already sent are device-authoritative from then on.
   void flush() {
+    bool any = false;
     for (auto& ch : chunks)
       if (ch.used > ch.sent) {
-        CK(cudaMemcpy(ch.dev + ch.sent, ch.shadow.get() + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ch.dev + ch.sent, ch.shadow.get() + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice,
+                           stream));
         ch.sent = ch.used;
+        any = true;
       }
+    if (any) CK(cudaStreamSynchronize(stream));
   }
   void seal() {
     flush();
@@ -618,6 +611,70 @@ Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
   return s;
 }
 
+// The device is required from here on (there is no CPU path): checked once,
+// then the engine's stream and kernel attributes are set up.
+void ensure_device(gmaco_engine* h) {
+  if (h->stream) return;
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->buf.stream = h->stream;
+  CK(configure_kernels());
+}
+
+// Exact distances dist(x -> dests[t]) for every node x on the device
+// (all_pairs_distances / dijkstra_to semantics, net.cpp:359-437): returns the
+// device table [T][n] (owned by B) and copies it to `host` for setup (spawn).
+int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::vector<int32_t>& dests,
+                               std::vector<int64_t>& host) {
+  const int32_t n = g.n, T = (int32_t)dests.size();
+  const size_t total = (size_t)T * n;
+  if (total >= (size_t(1) << 32)) throw ValidationError("distance table exceeds 2^32 entries");
+  PhaseTimer pt;
+  DevBuffers& B = h->buf;
+  std::vector<int32_t> rp, rs, re;
+  reverse_csr(g, rp, rs, re);
+  std::vector<int64_t> rl(g.m);
+  for (int32_t k = 0; k < g.m; ++k) rl[k] = g.len[re[k]];
+  DevBuffers tmp;  // scratch of the computation (frontiers, flags, reversed graph)
+  SsspArgs a;
+  a.n = n;
+  a.rptr = tmp.upload(rp);
+  a.rsrc = tmp.upload(rs);
+  a.rlen = tmp.upload(rl);
+  a.D = B.alloc_direct<int64_t>(total);  // written by kernels before the arena seal
+  a.inq = tmp.alloc<uint32_t>(total);
+  CK(cudaMemsetAsync(a.inq, 0, total * 4, h->stream));
+  uint32_t* q[2] = {tmp.alloc<uint32_t>(total), tmp.alloc<uint32_t>(total)};
+  uint32_t* cnt = tmp.alloc<uint32_t>(2);
+  const int32_t* ddests = tmp.upload(dests);
+  CK(sssp_fill_seed(a.D, total, ddests, T, n, q[0], h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  pt.mark("sssp setup (reverse CSR, alloc)");
+  uint32_t count = (uint32_t)T, host_cnt = 0;
+  int cur = 0, iters = 0;
+  size_t relaxed = 0;
+  while (count) {
+    ++iters;
+    relaxed += count;
+    CK(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, h->stream));
+    CK(sssp_relax(a, q[cur], count, q[cur ^ 1], cnt + (cur ^ 1), h->stream));
+    CK(cudaMemcpyAsync(&host_cnt, cnt + (cur ^ 1), 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    count = host_cnt;
+    cur ^= 1;
+  }
+  if (pt.on) std::fprintf(stderr, "[gmaco create] sssp: %d rounds, %zu state relaxations (%.2f per state)\n", iters,
+                          relaxed, (double)relaxed / (double)total);
+  pt.mark("sssp rounds");
+  host.resize(total);
+  CK(cudaMemcpy(host.data(), a.D, total * 8, cudaMemcpyDeviceToHost));
+  pt.mark("table download");
+  return a.D;
+}
+
 void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distance_desc* dd,
                  const gmaco_sim_config* cfg) {
   PhaseTimer pt0;
@@ -652,16 +709,11 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     if (dd->dist_mm) {
       for (int32_t u = 0; u < n; ++u)
         for (int32_t v = 0; v < n; ++v) table[(size_t)v * n + u] = dd->dist_mm[(size_t)u * n + v];
-    } else {  // all_pairs_distances (net.cpp:419-437), one Dijkstra per destination
-      std::vector<int32_t> rp, rs, re;
-      reverse_csr(g, rp, rs, re);
-      const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-      std::vector<std::thread> pool;
-      for (int t = 0; t < nt; ++t)
-        pool.emplace_back([&, t] {
-          for (int32_t d = t; d < n; d += nt) dijkstra_to(g, rp, rs, re, d, table.data() + (size_t)d * n);
-        });
-      for (auto& th : pool) th.join();
+    } else {  // all_pairs_distances (net.cpp:419-437): every node a destination, on the device
+      ensure_device(h);
+      std::vector<int32_t> all(n);
+      for (int32_t d = 0; d < n; ++d) all[d] = d;
+      w.d.table = device_distance_table(h, g, all, table);
     }
     dh.table = &table;
   } else if (dd->kind == GMACO_DIST_GRID) {
@@ -691,17 +743,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
         throw ValidationError(fmt("targets distance: invalid or duplicate target %d", x));
       slot_of[x] = t;
     }
-    table.resize((size_t)targets.size() * n);
-    std::vector<int32_t> rp, rs, re;
-    reverse_csr(g, rp, rs, re);
-    const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t)
-      pool.emplace_back([&, t] {
-        for (size_t k = t; k < targets.size(); k += nt)
-          dijkstra_to(g, rp, rs, re, targets[k], table.data() + k * n);
-      });
-    for (auto& th : pool) th.join();
+    ensure_device(h);
+    w.d.table = device_distance_table(h, g, targets, table);
     dh.table = &table;
     dh.slot_of = &slot_of;
   } else {
@@ -713,14 +756,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   pt.mark("spawn (host)");
   const int32_t V = c.vehicle_count;
   // all host-side validation is done: from here on the device is required
-  int dev_count = 0;
-  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
-    throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
-  CK(cudaSetDevice(h->device));
-  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  CK(configure_kernels());
+  ensure_device(h);
   pt.mark("device init");
-  if (!table.empty()) w.d.table = B.upload(table);
+  if (!table.empty() && !w.d.table) w.d.table = B.upload(table);  // user-supplied dense table
   if (!slot_of.empty()) w.d.slot_of = B.upload(slot_of);
 
 
@@ -865,26 +903,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     w.g.nrow = B.upload(nrow);
     const int32_t T = dd->kind == GMACO_DIST_TARGETS ? (int32_t)targets.size() : n;
     const int64_t fbw = (M + 31) / 32 + 1;
-    std::vector<uint2> fb((size_t)T * fbw, make_uint2(0, 0));
-    const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> pool;
-    for (int th = 0; th < nt; ++th)
-      pool.emplace_back([&, th] {
-        for (int32_t t = th; t < T; t += nt) {
-          const int64_t* dt = table.data() + (size_t)t * n;
-          uint2* out = fb.data() + (size_t)t * fbw;
-          for (int32_t s = 0; s < M; ++s) {
-            if (col[s] < 0) continue;
-            const int64_t dn = dt[col[s]];
-            if (dn == kInf) continue;
-            out[s >> 5].y |= 1u << (s & 31);
-            if (dn < dt[slot_from[s]]) out[s >> 5].x |= 1u << (s & 31);
-          }
-        }
-      });
-    for (auto& th : pool) th.join();
-    w.d.fbits = B.upload(fb);
+    uint2* fb = B.alloc_direct<uint2>((size_t)T * fbw);  // filled by k_fbits from the device table
     w.d.fbw = fbw;
+    B.flush();  // the kernel reads arena arrays (col, slot_from)
+    CK(build_fbits(w, T, fb, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    w.d.fbits = fb;
+
   }
   p.shard_lo = 0;
   p.shard_hi = V;

@@ -2406,6 +2406,99 @@ cudaError_t launch_pack(const PackDesc& d, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Distance service on the device: exact multi-target
+// shortest distances dist(x -> target) over the reversed graph, int64 mm.
+// Frontier Bellman-Ford: every (target, node) whose distance dropped is
+// relaxed along its in-edges with int64 atomicMin; a per-state in-queue flag
+// dedups the next frontier.  Shortest distances are unique, so the table is
+// identical to the reference's Dijkstra (net.cpp:359-437) whatever the
+// relaxation order.  Tables are destination-major [T][n].
+// ---------------------------------------------------------------------------
+__global__ void k_sssp_fill(int64_t* D, size_t total) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+    D[i] = kInf;
+}
+
+__global__ void k_sssp_seed(int64_t* D, const int32_t* dests, int32_t T, int32_t n, uint32_t* cur) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint32_t item = (uint32_t)t * (uint32_t)n + (uint32_t)dests[t];
+  D[item] = 0;
+  cur[t] = item;
+}
+
+__global__ void __launch_bounds__(256) k_sssp_relax(SsspArgs a, const uint32_t* cur, uint32_t count, uint32_t* nxt,
+                                                    uint32_t* nnxt) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const uint32_t item = cur[i];
+    const uint32_t t = item / (uint32_t)a.n, u = item - t * (uint32_t)a.n;
+    a.inq[item] = 0;  // before reading D: a later improvement re-queues the state
+    __threadfence();
+    const int64_t du = *((volatile int64_t*)(a.D + item));
+    int64_t* Drow = a.D + (size_t)t * a.n;
+    for (int32_t k = a.rptr[u]; k < a.rptr[u + 1]; ++k) {
+      const int32_t v = a.rsrc[k];
+      const int64_t nd = du + a.rlen[k];
+      if (nd < Drow[v]) {
+        const long long old = atomicMin(reinterpret_cast<long long*>(Drow + v), (long long)nd);
+        if (nd < old) __threadfence();  // pairs with the reader's flag-clear fence (store-buffering)
+        if (nd < old && atomicExch(a.inq + (size_t)t * a.n + v, 1u) == 0u) {
+          cg::coalesced_group g = cg::coalesced_threads();  // aggregated append
+          uint32_t base = 0;
+          if (g.thread_rank() == 0) base = atomicAdd(nnxt, (uint32_t)g.size());
+          base = g.shfl(base, 0);
+          nxt[base + g.thread_rank()] = t * (uint32_t)a.n + (uint32_t)v;
+        }
+      }
+    }
+  }
+}
+
+cudaError_t sssp_fill_seed(int64_t* D, size_t total, const int32_t* dests, int32_t T, int32_t n, uint32_t* cur,
+                           cudaStream_t st) {
+  k_sssp_fill<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(D, total);
+  k_sssp_seed<<<blocks_for(T, 256), 256, 0, st>>>(D, dests, T, n, cur);
+  return cudaGetLastError();
+}
+
+cudaError_t sssp_relax(const SsspArgs& a, const uint32_t* cur, uint32_t count, uint32_t* nxt, uint32_t* nnxt,
+                       cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<uint32_t>((count + 255) / 256, 148u * 8u);
+  k_sssp_relax<<<blocks, 256, 0, st>>>(a, cur, count, nxt, nnxt);
+  return cudaGetLastError();
+}
+
+// Progress-filter bitmaps from a device distance table (see DevDist::fbits).
+__global__ void k_fbits(const int64_t* D, int32_t n, int32_t T, const int32_t* col, const int32_t* from, int32_t M,
+                        int64_t fbw, uint2* fb) {
+  const size_t total = (size_t)T * fbw;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = idx / fbw;
+    const int64_t wd = (int64_t)(idx - t * fbw);
+    const int64_t* Dr = D + t * n;
+    uint2 out = make_uint2(0u, 0u);
+    for (int b = 0; b < 32; ++b) {
+      const int64_t s = wd * 32 + b;
+      if (s >= M) break;
+      const int32_t c = col[s];
+      if (c < 0) continue;
+      const int64_t dn = Dr[c];
+      if (dn == kInf) continue;
+      out.y |= 1u << b;
+      if (dn < Dr[from[s]]) out.x |= 1u << b;
+    }
+    fb[idx] = out;
+  }
+}
+
+cudaError_t build_fbits(const DevWorld& w, int32_t T, uint2* fb, cudaStream_t st) {
+  const size_t total = (size_t)T * w.d.fbw;
+  k_fbits<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(w.d.table, w.g.n, T, w.g.col,
+                                                                                      w.g.slot_from, w.g.M, w.d.fbw, fb);
+  return cudaGetLastError();
+}
+
 int queue_blocks(const DevWorld& w, int device) {
   if (!w.p.ant_queue) return 0;
   int per_sm = 0, sms = 0;

@@ -33,6 +33,20 @@ cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
 cudaError_t configure_grid_carveout(const DevWorld& w);
+// Device distance service (exact multi-target SSSP over the reversed graph).
+struct SsspArgs {
+  int32_t n;
+  const int32_t* rptr;  // [n+1] reversed CSR: in-edges of u
+  const int32_t* rsrc;  // [m] tail node of each in-edge
+  const int64_t* rlen;  // [m] its length (mm)
+  int64_t* D;           // [T][n] distances to each target
+  uint32_t* inq;        // [T][n] in-next-frontier flags
+};
+cudaError_t sssp_fill_seed(int64_t* D, size_t total, const int32_t* dests, int32_t T, int32_t n, uint32_t* cur,
+                           cudaStream_t st);
+cudaError_t sssp_relax(const SsspArgs& a, const uint32_t* cur, uint32_t count, uint32_t* nxt, uint32_t* nnxt,
+                       cudaStream_t st);
+cudaError_t build_fbits(const DevWorld& w, int32_t T, uint2* fb, cudaStream_t st);
 // Batched gather of device arrays into (mapped pinned) host memory.
 struct PackField {
   const void* src;
