@@ -18,6 +18,7 @@
 #ifndef GMACO_H_
 #define GMACO_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -283,6 +284,32 @@ int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
  * (begin, end of the stage-B walk; the rest of the step runs untimed), or
  * both (three events; each event node costs ~2-3 us of serialization). */
 int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms);
+
+/* ---- reference-schema network files --------------------
+ * load_network / load_network_file (R/src/net.cpp:112-175): parse
+ * {"nodes": [{"id","signalized","x"?,"y"?}], "edges": [{"id","from","to",
+ * "length_m","lanes"}]} with the reference's checks and messages (status 1),
+ * ids dense and sorted as the RoadNetwork ctor (net.cpp:38-98) leaves them;
+ * length_mm = llround(length_m * 1000) (net.cpp:34).  The opaque handle owns
+ * the parsed SoA arrays; gmaco_network_export copies them into caller buffers
+ * sized by gmaco_network_info (any pointer may be NULL). */
+typedef struct gmaco_network gmaco_network;
+int gmaco_network_parse(const char* text, size_t len, gmaco_network** out);
+int gmaco_network_load_file(const char* path, gmaco_network** out);
+int gmaco_network_info(const gmaco_network* net, int32_t* node_count, int32_t* edge_count);
+int gmaco_network_export(const gmaco_network* net, uint8_t* signalized, int32_t* edge_from, int32_t* edge_to,
+                         int64_t* edge_length_mm, int32_t* edge_lanes, double* x_m, double* y_m,
+                         uint8_t* has_position);
+void gmaco_network_free(gmaco_network* net);
+/* serialize_network / write_network_file (net.cpp:179-209): the same text as
+ * nlohmann::json::dump(2) of the reference document.  serialize: *len gets the
+ * text length; the text is written only when cap >= *len.  Positions are
+ * optional (NULL x/y: none; has_position NULL: all present). */
+int gmaco_network_serialize(const gmaco_graph_desc* g, const double* x_m, const double* y_m,
+                            const uint8_t* has_position, char* buf, size_t cap, size_t* len);
+int gmaco_network_write_file(const gmaco_graph_desc* g, const double* x_m, const double* y_m,
+                             const uint8_t* has_position, const char* path);
+const char* gmaco_network_last_error(void);
 
 const char* gmaco_last_error(const gmaco_engine* h);
 void gmaco_destroy(gmaco_engine* h);

@@ -117,6 +117,11 @@ def ref_lib():
         _sig(L, "ref_generate_city", C.c_int, C.c_int, C.c_int, C.c_int, u64, P(u8), P(i32), P(i32),
              P(i64), P(i32))
         _sig(L, "ref_validate_graph", C.c_int, P(abi.GraphDesc))
+        _sig(L, "ref_serialize_city", C.c_int, C.c_int, C.c_int, C.c_int, u64, C.c_char_p, C.c_size_t,
+             P(C.c_size_t))
+        _sig(L, "ref_serialize_desc", C.c_int, P(abi.GraphDesc), C.c_char_p, C.c_size_t, P(C.c_size_t))
+        _sig(L, "ref_load_network", C.c_int, C.c_char_p, C.c_size_t, P(i32), P(i32), P(u8), P(i32), P(i32),
+             P(i64), P(i32), P(f64), P(f64), P(u8))
         _sig(L, "ref_apsp", C.c_int, P(abi.GraphDesc), P(i64), P(i32))
         _sig(L, "ref_evaporate_one", i64, i64, P(abi.PheromoneParams))
         _sig(L, "ref_deposit_amount", i64, i64, P(abi.PheromoneParams))
@@ -405,6 +410,51 @@ def ref_city(nodes, links, lanes=3, seed=20250810):
     if rc:
         raise OracleError(rc, L.ref_last_error().decode())
     return Network(nodes, sig, frm, to, ln, la)
+
+
+def _ref_text(call):
+    L = ref_lib()
+    need = C.c_size_t()
+    rc = call(None, 0, C.byref(need))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    buf = C.create_string_buffer(need.value)
+    rc = call(buf, need.value, C.byref(need))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return buf.raw[:need.value].decode()
+
+
+def ref_serialize_city(nodes, links, lanes=3, seed=20250810) -> str:
+    """serialize_network (net.cpp:179-200) of the reference's generate_city."""
+    L = ref_lib()
+    return _ref_text(lambda b, c, n: L.ref_serialize_city(nodes, links, lanes, seed, b, c, n))
+
+
+def ref_serialize(net) -> str:
+    """serialize_network of a descriptor network (reference code)."""
+    L = ref_lib()
+    return _ref_text(lambda b, c, n: L.ref_serialize_desc(C.byref(net.desc()), b, c, n))
+
+
+def ref_load_network(text: str):
+    """load_network (net.cpp:112-168) by the reference: (status, message or
+    dict of SoA arrays in id order)."""
+    L = ref_lib()
+    raw = text.encode()
+    n, m = C.c_int32(), C.c_int32()
+    rc = L.ref_load_network(raw, len(raw), C.byref(n), C.byref(m), None, None, None, None, None, None, None, None)
+    if rc:
+        return rc, L.ref_last_error().decode()
+    n, m = n.value, m.value
+    a = dict(signalized=np.zeros(n, np.uint8), edge_from=np.zeros(m, np.int32), edge_to=np.zeros(m, np.int32),
+             edge_length_mm=np.zeros(m, np.int64), edge_lanes=np.zeros(m, np.int32), x=np.zeros(n, np.float64),
+             y=np.zeros(n, np.float64), has_position=np.zeros(n, np.uint8))
+    L.ref_load_network(raw, len(raw), C.byref(C.c_int32()), C.byref(C.c_int32()), abi.ptr(a["signalized"], u8),
+                       abi.ptr(a["edge_from"], i32), abi.ptr(a["edge_to"], i32), abi.ptr(a["edge_length_mm"], i64),
+                       abi.ptr(a["edge_lanes"], i32), abi.ptr(a["x"], f64), abi.ptr(a["y"], f64),
+                       abi.ptr(a["has_position"], u8))
+    return 0, a
 
 
 def results_identical(a, b) -> bool:

@@ -238,6 +238,53 @@ int ref_generate_city(int nodes, int links, int lanes, uint64_t seed, uint8_t* s
   })
 }
 
+// serialize_network (net.cpp:179-200) of a generated city (which carries
+// node positions): *len = text length, written when cap >= *len.
+int ref_serialize_city(int nodes, int links, int lanes, uint64_t seed, char* buf, size_t cap, size_t* len) {
+  GUARD({
+    const std::string s = serialize_network(generate_city(nodes, links, lanes, seed));
+    *len = s.size();
+    if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    return 0;
+  })
+}
+
+// serialize_network of a descriptor network (no positions).
+int ref_serialize_desc(const gmaco_graph_desc* g, char* buf, size_t cap, size_t* len) {
+  GUARD({
+    const std::string s = serialize_network(to_network(g));
+    *len = s.size();
+    if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    return 0;
+  })
+}
+
+// load_network (net.cpp:112-168): sizes, then (arrays non-null) the SoA.
+int ref_load_network(const char* text, size_t len, int32_t* n_out, int32_t* m_out, uint8_t* signalized,
+                     int32_t* from, int32_t* to, int64_t* len_mm, int32_t* lanes_out, double* x, double* y,
+                     uint8_t* has_pos) {
+  GUARD({
+    RoadNetwork net = load_network(std::string(text, len));
+    *n_out = net.node_count();
+    *m_out = net.edge_count();
+    if (signalized)
+      for (const RoadNode& nd : net.nodes()) {
+        signalized[nd.id] = nd.signalized;
+        if (x) x[nd.id] = nd.x_m;
+        if (y) y[nd.id] = nd.y_m;
+        if (has_pos) has_pos[nd.id] = nd.has_position;
+      }
+    if (from)
+      for (const RoadEdge& e : net.edges()) {
+        from[e.id] = e.from;
+        to[e.id] = e.to;
+        len_mm[e.id] = e.length_mm;
+        lanes_out[e.id] = e.lanes;
+      }
+    return 0;
+  })
+}
+
 // Validates through the RoadNetwork constructor (net.cpp:38-98).
 int ref_validate_graph(const gmaco_graph_desc* g) {
   GUARD({

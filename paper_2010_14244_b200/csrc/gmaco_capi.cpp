@@ -378,6 +378,21 @@ std::vector<T> download(const T* d, size_t n) {
 }  // namespace
 }  // namespace gmaco
 
+namespace gmaco {
+// RoadNetwork ctor checks (net.cpp:38-98) on a descriptor, for the
+// reference-schema loader / writer (netio.cpp).
+bool validate_graph_desc(const gmaco_graph_desc* d, std::string* err) {
+  try {
+    HostGraph g;
+    build_graph(d, g);
+    return true;
+  } catch (const ValidationError& e) {
+    if (err) *err = e.what();
+    return false;
+  }
+}
+}  // namespace gmaco
+
 using namespace gmaco;
 
 struct gmaco_engine {

@@ -50,6 +50,15 @@ SIGNATURES = {
     "gmaco_step_split": (C.c_int, C.c_void_p, i32),
     "gmaco_exchange_export": (C.c_int, C.c_void_p, P(i32), P(i64)),
     "gmaco_exchange_import": (C.c_int, C.c_void_p, P(i32), P(i64)),
+    "gmaco_network_parse": (C.c_int, C.c_char_p, C.c_size_t, P(C.c_void_p)),
+    "gmaco_network_load_file": (C.c_int, C.c_char_p, P(C.c_void_p)),
+    "gmaco_network_info": (C.c_int, C.c_void_p, P(i32), P(i32)),
+    "gmaco_network_export": (C.c_int, C.c_void_p, P(u8), P(i32), P(i32), P(i64), P(i32), P(f64), P(f64), P(u8)),
+    "gmaco_network_free": (None, C.c_void_p),
+    "gmaco_network_serialize": (C.c_int, P(abi.GraphDesc), P(f64), P(f64), P(u8), C.c_char_p, C.c_size_t,
+                                P(C.c_size_t)),
+    "gmaco_network_write_file": (C.c_int, P(abi.GraphDesc), P(f64), P(f64), P(u8), C.c_char_p),
+    "gmaco_network_last_error": (C.c_char_p,),
     "gmaco_last_error": (C.c_char_p, C.c_void_p),
     "gmaco_destroy": (None, C.c_void_p),
 }

@@ -182,3 +182,81 @@ def random_geometric(nodes: int, k: int = 3, lanes: int = 3, seed: int = 2025081
         edge_length_mm=np.repeat(length, 2),
         edge_lanes=np.full(2 * npairs, lanes, dtype=np.int32),
     )
+
+
+# ---- reference-schema JSON (load_network / serialize_network, net.cpp:112-209) ----
+
+def _net_check(L, rc):
+    if rc != 0:
+        from .engine import EngineError
+        raise EngineError(rc, L.gmaco_network_last_error().decode())
+
+
+def _from_handle(L, h) -> "Network":
+    n, m = C.c_int32(), C.c_int32()
+    L.gmaco_network_info(h, C.byref(n), C.byref(m))
+    n, m = n.value, m.value
+    sig = np.zeros(n, np.uint8)
+    frm, to, lanes = np.zeros(m, np.int32), np.zeros(m, np.int32), np.zeros(m, np.int32)
+    ln = np.zeros(m, np.int64)
+    x, y, hp = np.zeros(n, np.float64), np.zeros(n, np.float64), np.zeros(n, np.uint8)
+    _net_check(L, L.gmaco_network_export(h, abi.ptr(sig, C.c_uint8), abi.ptr(frm, C.c_int32), abi.ptr(to, C.c_int32),
+                                         abi.ptr(ln, C.c_int64), abi.ptr(lanes, C.c_int32), abi.ptr(x, C.c_double),
+                                         abi.ptr(y, C.c_double), abi.ptr(hp, C.c_uint8)))
+    net = Network(node_count=n, signalized=sig, edge_from=frm, edge_to=to, edge_length_mm=ln, edge_lanes=lanes)
+    net.positions = (x, y, hp) if hp.any() else None
+    return net
+
+
+def parse_json(text: str) -> "Network":
+    """load_network (net.cpp:112-168): a reference-schema network from JSON
+    text, parsed natively by the engine library (gmaco_network_parse)."""
+    from .engine import load
+    L = load()
+    h = C.c_void_p()
+    raw = text.encode()
+    _net_check(L, L.gmaco_network_parse(raw, len(raw), C.byref(h)))
+    try:
+        return _from_handle(L, h)
+    finally:
+        L.gmaco_network_free(h)
+
+
+def load_json(path: str) -> "Network":
+    """load_network_file (net.cpp:170-176) via gmaco_network_load_file."""
+    from .engine import load
+    L = load()
+    h = C.c_void_p()
+    _net_check(L, L.gmaco_network_load_file(path.encode(), C.byref(h)))
+    try:
+        return _from_handle(L, h)
+    finally:
+        L.gmaco_network_free(h)
+
+
+def _pos_args(net):
+    pos = getattr(net, "positions", None)
+    if pos is None:
+        return None, None, None
+    x, y, hp = (np.ascontiguousarray(a) for a in pos)
+    return abi.ptr(x, C.c_double), abi.ptr(y, C.c_double), abi.ptr(hp, C.c_uint8)
+
+
+def serialize_json(net: "Network") -> str:
+    """serialize_network (net.cpp:179-200): the reference's dump(2) text."""
+    from .engine import load
+    L = load()
+    px, py, ph = _pos_args(net)
+    need = C.c_size_t()
+    _net_check(L, L.gmaco_network_serialize(C.byref(net.desc()), px, py, ph, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _net_check(L, L.gmaco_network_serialize(C.byref(net.desc()), px, py, ph, buf, need.value, C.byref(need)))
+    return buf.raw[:need.value].decode()
+
+
+def save_json(net: "Network", path: str) -> None:
+    """write_network_file (net.cpp:202-206)."""
+    from .engine import load
+    L = load()
+    px, py, ph = _pos_args(net)
+    _net_check(L, L.gmaco_network_write_file(C.byref(net.desc()), px, py, ph, path.encode()))
