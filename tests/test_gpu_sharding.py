@@ -52,6 +52,16 @@ def test_host_mediated_shards_equal_unsharded(nshards):
         for e in shards:
             assert same(e, single) is None, (k, same(e, single))
     assert sum(e.counters().ant_steps for e in shards) == single.counters().ant_steps
+    # run to completion: every rank must agree on the step count and on
+    # finished() (the NCCL path relies on it: no rank may stop early)
+    while not single.finished():
+        step()
+        single.step(1)
+        for e in shards:
+            assert e.current_step() == single.current_step()
+            assert e.finished() == single.finished()
+        assert sum(e.counters().decisions for e in shards) == single.counters().decisions
+    assert O.results_identical(shards[0].collect(), single.collect())
 
 
 def test_mixed_engine_and_oracle_shards():
@@ -84,3 +94,49 @@ def test_nccl_exchange_world1_equals_unsharded():
     single.step(6)
     assert same(e, single) is None
     assert e.counters().ant_steps == single.counters().ant_steps
+
+
+def _walker_world(kind):
+    """(net, cfg, dist factory, env) per stage-B walker kind."""
+    from test_gpu_parity import _hub_graph, _rgg_targets
+    prod = lambda V, ants, steps: abi.colony_production(abi.default_config(
+        algorithm="colony", controller="preemptive", vehicle_count=V, seed=9, max_steps=steps), ants=ants)
+    if kind == "lattice-multiword":
+        net = networks.grid(40, 40, signals="interior")
+        return net, prod(240, 64, 30), net.grid_distance, {}
+    if kind in ("queue", "block"):
+        net, _, tgt = _rgg_targets(3000, 12, 77)
+        cfg = prod(300, 16, 30)
+        cfg.colony.max_hops = 512
+        make = lambda: abi.DistanceDesc(kind=abi.DIST_TARGETS, targets=abi.ptr(tgt, __import__("ctypes").c_int32),
+                                        target_count=len(tgt))
+        return net, cfg, make, ({"GMACO_NO_QUEUE": "1"} if kind == "block" else {}), tgt
+    if kind == "generic":
+        net = _hub_graph(20)
+        return net, prod(200, 32, 30), lambda: abi.DistanceDesc(kind=abi.DIST_DENSE), {}
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["lattice-multiword", "queue", "block", "generic"])
+def test_host_mediated_shards_every_walker(kind, monkeypatch):
+    """Sharded stage B on each walker (prologue / queue / epilogue decision
+    records included) equals the unsharded engine, step by step."""
+    spec = _walker_world(kind)
+    net, cfg, dist, env = spec[:4]
+    keep = spec[4:]  # target arrays referenced by the descriptors
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    single = Engine(net, cfg, dist())
+    shards = []
+    for r in range(3):
+        e = Engine(net, cfg, dist())
+        e.set_shard(*sharding.shard_bounds(cfg.vehicle_count, 3, r))
+        shards.append(e)
+    step = sharding.local_transport(shards)
+    for k in range(6):
+        step()
+        single.step(1)
+        for e in shards:
+            assert same(e, single) is None, (kind, k, same(e, single))
+    assert sum(e.counters().ant_steps for e in shards) == single.counters().ant_steps
+    del keep
