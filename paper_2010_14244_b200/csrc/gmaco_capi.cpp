@@ -289,19 +289,35 @@ struct DevBuffers {
   // (a later flush of the arena must never overwrite them).
   template <class T>
   T* alloc_direct(size_t n) {
+    return static_cast<T*>(raw_alloc(std::max<size_t>(n, 1) * sizeof(T)));
+  }
+  // Stream-ordered allocations from the device's default pool, which keeps
+  // up to kPoolKeep of freed memory: engines created one after another (the
+  // bench legs, the tests) reuse it instead of paying cudaMalloc per array.
+  static constexpr uint64_t kPoolKeep = uint64_t(4) << 30;
+  void* raw_alloc(size_t bytes) {
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (configured_dev != dev) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      configured_dev = dev;
+    }
     void* p = nullptr;
-    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMallocAsync(&p, bytes, stream));
+    CK(cudaStreamSynchronize(stream));  // usable by any stream / host call right away
     ptrs.push_back(p);
-    return static_cast<T*>(p);
+    return p;
   }
   template <class T>
   T* alloc(size_t n) {
     const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
     if (arena && bytes <= kArenaMax) return static_cast<T*>(carve(bytes, nullptr));
-    void* p = nullptr;
-    CK(cudaMalloc(&p, bytes));
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
+    return static_cast<T*>(raw_alloc(bytes));
   }
   template <class T>
   T* upload(const std::vector<T>& h) {
@@ -342,17 +358,24 @@ struct DevBuffers {
     for (auto& ch : chunks) ch.shadow.reset();
     arena = false;
   }
-  ~DevBuffers() {
-    for (void* p : ptrs) cudaFree(p);
-    for (auto& ch : chunks) cudaFree(ch.dev);
+  // Back to the pool, ordered after the owner's work on `stream` (call
+  // before that stream is destroyed).
+  void release() {
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
+    for (auto& ch : chunks) cudaFreeAsync(ch.dev, stream);
+    if (!ptrs.empty() || !chunks.empty()) cudaStreamSynchronize(stream);
+    ptrs.clear();
+    chunks.clear();
   }
+  ~DevBuffers() { release(); }
 
  private:
   void* carve(size_t bytes, const void*) {
     const size_t need = (bytes + kAlign - 1) & ~(kAlign - 1);
     if (chunks.empty() || chunks.back().used + need > kChunk) {
       Chunk ch;
-      CK(cudaMalloc(&ch.dev, kChunk));
+      ch.dev = static_cast<char*>(raw_alloc(kChunk));
+      ptrs.pop_back();  // owned by the chunk list
       ch.shadow.reset(new char[kChunk]);
       chunks.push_back(std::move(ch));
     }
@@ -455,6 +478,7 @@ struct gmaco_engine {
     PinnedPool::give(ctl_host);
     // stop_host lives inside the ctl_host pinned block
     PinnedPool::give(stage);
+    buf.release();  // stream-ordered frees need the stream alive
     if (stream) cudaStreamDestroy(stream);
     destroy_comm();
   }
