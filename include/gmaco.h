@@ -250,6 +250,14 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau_micros);
 int gmaco_get_occupancy(gmaco_engine* h, int32_t* occupancy /* [edge_count] */);
 int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* view);
 int gmaco_get_signals(gmaco_engine* h, const gmaco_signal_view* view, int64_t queue_cap);
+/* Double-buffered vehicle readback: gmaco_vehicles_enqueue snapshots the
+ * fields a view requests (non-NULL pointers; their values are not read) of
+ * the state after every step enqueued so far into internal pinned slot 0 or
+ * 1, without waiting; gmaco_vehicles_wait blocks for that snapshot only and
+ * copies it into `view` (same field set).  A caller reads every step's result
+ * while the next step already runs (gmaco_step with executed == NULL). */
+int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot);
+int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view* view);
 int gmaco_signal_count(gmaco_engine* h, int32_t* out);
 int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out);
 int gmaco_current_step(gmaco_engine* h, int64_t* out);

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <tuple>
 #include <unordered_map>
 #include <mutex>
 #include <cstdio>
@@ -437,6 +438,15 @@ struct gmaco_engine {
   bool pending = false;       // steps enqueued without a host sync
   void* stage = nullptr;      // pinned staging for batched device->host reads
   size_t stage_bytes = 0;
+  // double-buffered readback slots (gmaco_vehicles_enqueue / _wait)
+  struct ReadSlot {
+    void* buf = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+    std::vector<std::pair<size_t, size_t>> fields;  // (staging offset, bytes) per requested field, view order
+    size_t oe_off = 0;
+    bool on_edge = false, armed = false;
+  } rslot[2];
   StepResources res;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph_big = nullptr, graph_one = nullptr;
@@ -478,6 +488,10 @@ struct gmaco_engine {
     PinnedPool::give(ctl_host);
     // stop_host lives inside the ctl_host pinned block
     PinnedPool::give(stage);
+    for (auto& s : rslot) {
+      PinnedPool::give(s.buf);
+      if (s.done) cudaEventDestroy(s.done);
+    }
     buf.release();  // stream-ordered frees need the stream alive
     if (stream) cudaStreamDestroy(stream);
     destroy_comm();
@@ -1663,6 +1677,92 @@ int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
     }
   }, /*stream_ordered=*/true);
 }
+// The requested vehicle fields of a view, in declaration order:
+// (user destination, device source, element bytes).
+static std::vector<std::tuple<void*, const void*, size_t>> vehicle_fields(const gmaco_engine* h,
+                                                                          const gmaco_vehicle_view* v) {
+  const DevVehicles& d = h->w.v;
+  std::vector<std::tuple<void*, const void*, size_t>> f;
+  auto add = [&](void* dst, const void* src, size_t e) {
+    if (dst) f.emplace_back(dst, src, e);
+  };
+  add(v->origin, d.origin, 4);
+  add(v->dest, d.dest, 4);
+  add(v->advance_mm, d.advance, 8);
+  add(v->state, d.state, 1);
+  add(v->at_node, d.at_node, 4);
+  add(v->progress_mm, d.progress, 8);
+  add(v->overshoot_mm, d.overshoot, 8);
+  add(v->queued_phase, d.queued_phase, 4);
+  add(v->queue_joined_step, d.joined, 8);
+  add(v->depart_step, d.depart, 8);
+  add(v->arrive_step, d.arrive, 8);
+  add(v->latency_debt_us, d.latency_debt, 8);
+  add(v->driving_steps, d.driving, 8);
+  add(v->queued_steps, d.queued, 8);
+  add(v->latency_steps, d.lat_steps, 8);
+  add(v->decisions, d.decisions, 4);
+  add(v->deviations, d.deviations, 4);
+  add(v->path_length_mm, d.path_len_mm, 8);
+  return f;
+}
+
+int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
+  if (!h || !fields || slot < 0 || slot > 1) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    auto& rs = h->rslot[slot];
+    const size_t V = h->w.p.V;
+    const auto f = vehicle_fields(h, fields);
+    size_t total = 0;
+    rs.fields.clear();
+    for (const auto& t : f) {
+      rs.fields.emplace_back(total, V * std::get<2>(t));
+      total += (V * std::get<2>(t) + 15) & ~size_t(15);
+    }
+    rs.on_edge = fields->on_edge != nullptr;
+    rs.oe_off = total;
+    if (rs.on_edge) total += V * 4;
+    total = std::max<size_t>(total, 16);
+    if (rs.bytes < total) {
+      PinnedPool::give(rs.buf);
+      rs.buf = PinnedPool::take(total);
+      rs.bytes = total;
+    }
+    if (!rs.done) CK(cudaEventCreateWithFlags(&rs.done, cudaEventDisableTiming));
+    char* dev = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), rs.buf, 0));
+    PackDesc pd;
+    for (size_t i = 0; i < f.size(); ++i) pd.f[pd.n++] = PackField{std::get<1>(f[i]), dev + rs.fields[i].first,
+                                                                   rs.fields[i].second};
+    if (rs.on_edge) pd.f[pd.n++] = PackField{h->w.v.on_edge, dev + rs.oe_off, V * 4};
+    CK(launch_pack(pd, h->stream));
+    CK(cudaEventRecord(rs.done, h->stream));
+    rs.armed = true;
+  }, /*stream_ordered=*/true);
+}
+
+int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view* view) {
+  if (!h || !view || slot < 0 || slot > 1) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    auto& rs = h->rslot[slot];
+    if (!rs.armed) throw ValidationError("vehicles_wait: no snapshot enqueued in this slot");
+    const auto f = vehicle_fields(h, view);
+    if (f.size() != rs.fields.size() || (view->on_edge != nullptr) != rs.on_edge)
+      throw ValidationError("vehicles_wait: view fields differ from the enqueued snapshot");
+    CK(cudaEventSynchronize(rs.done));  // only this snapshot, not later steps
+    const char* st = static_cast<const char*>(rs.buf);
+    for (size_t i = 0; i < f.size(); ++i) std::memcpy(std::get<0>(f[i]), st + rs.fields[i].first, rs.fields[i].second);
+    if (rs.on_edge) {
+      const int32_t* oe = reinterpret_cast<const int32_t*>(st + rs.oe_off);
+      for (size_t i = 0; i < (size_t)h->w.p.V; ++i) view->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
+    }
+    if (view->speed_mps)
+      for (size_t i = 0; i < (size_t)h->w.p.V; ++i)
+        view->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+    rs.armed = false;
+  }, /*stream_ordered=*/true);
+}
+
 int gmaco_signal_count(gmaco_engine* h, int32_t* out) {
   if (!h || !out) return GMACO_EVALIDATION;
   *out = h->S;

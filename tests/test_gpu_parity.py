@@ -433,3 +433,33 @@ def test_colony_wide_rows(hub_degree, mode, monkeypatch):
     for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
         assert getattr(a, f) == getattr(b, f), f
     assert O.results_identical(gpu.run(), cpu.run())
+
+
+def test_double_buffered_readback_every_step():
+    """gmaco_vehicles_enqueue / _wait: each step's snapshot (taken while the
+    next step is already enqueued) equals the oracle's state at that step."""
+    import ctypes as C
+    net = networks.grid(10, 10, signals="all")
+    cfg = abi.colony_production(_cfg("colony", 150, 4, max_steps=30), ants=32)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    V = cfg.vehicle_count
+    bufs = [dict(state=np.zeros(V, np.uint8), on_edge=np.zeros(V, np.int32), progress_mm=np.zeros(V, np.int64),
+                 decisions=np.zeros(V, np.int32)) for _ in range(2)]
+    views = [abi.VehicleView(state=abi.ptr(b["state"], C.c_uint8), on_edge=abi.ptr(b["on_edge"], C.c_int32),
+                             progress_mm=abi.ptr(b["progress_mm"], C.c_int64),
+                             decisions=abi.ptr(b["decisions"], C.c_int32)) for b in bufs]
+    for k in range(14):
+        gpu.step(1, count=False)
+        gpu.vehicles_enqueue(views[k % 2], k % 2)
+        if k:
+            gpu.vehicles_wait((k - 1) % 2, views[(k - 1) % 2])
+            cpu.step(1)
+            ref = cpu.vehicles()
+            for f, arr in bufs[(k - 1) % 2].items():
+                assert np.array_equal(arr, ref[f]), (k, f)
+    gpu.vehicles_wait(13 % 2, views[13 % 2])
+    cpu.step(1)
+    ref = cpu.vehicles()
+    for f, arr in bufs[13 % 2].items():
+        assert np.array_equal(arr, ref[f]), f
