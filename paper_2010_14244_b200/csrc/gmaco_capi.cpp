@@ -678,7 +678,7 @@ void ensure_device(gmaco_engine* h) {
 }
 
 // Exact distances dist(x -> dests[t]) for every node x on the device
-// (all_pairs_distances / dijkstra_to semantics, net.cpp:359-437): returns the
+// (all_pairs_distances / dijkstra_to results, net.cpp:359-437): returns the
 // device table [T][n] (owned by B) and copies it to `host` for setup (spawn).
 int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::vector<int32_t>& dests,
                                std::vector<int64_t>& host) {

@@ -1418,9 +1418,11 @@ __device__ __forceinline__ size_t grid_staged_bytes_dev(const DevWorld& w) {
 //   kTourReplay  — the winner re-walks (counter RNG) into v.plan;
 //   kTourScratch — every ant writes its slots to v.scratch, the plan is the
 //                  winner's row;
-//   kTourBits    — walks of <= 64 hops keep one bit per hop (vertical or
-//                  horizontal move) in a register; the winner's tour is
-//                  rebuilt arithmetically into v.plan.  No per-hop stores.
+//   kTourBits    — one bit per hop (vertical or horizontal move), 64 hops
+//                  per word in a register, full words flushed to SMEM
+//                  (bit_words per ant); the winner's tour is rebuilt
+//                  arithmetically (prefix popcounts) into v.plan.  No
+//                  per-hop global stores.
 enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 
 // kOneVeh: the CTA holds exactly one vehicle's colony (threads == K, K a
