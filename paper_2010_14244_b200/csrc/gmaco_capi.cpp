@@ -309,11 +309,18 @@ struct DevBuffers {
       configured_dev = dev;
     }
     void* p = nullptr;
+    if (bytes >= kPoolMax) {  // huge (tour scratch, distance tables): plain allocation, not pooled
+      CK(cudaMalloc(&p, bytes));
+      big.push_back(p);
+      return p;
+    }
     CK(cudaMallocAsync(&p, bytes, stream));
     CK(cudaStreamSynchronize(stream));  // usable by any stream / host call right away
     ptrs.push_back(p);
     return p;
   }
+  static constexpr size_t kPoolMax = size_t(256) << 20;
+  std::vector<void*> big;
   template <class T>
   T* alloc(size_t n) {
     const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
@@ -364,9 +371,11 @@ struct DevBuffers {
   void release() {
     for (void* p : ptrs) cudaFreeAsync(p, stream);
     for (auto& ch : chunks) cudaFreeAsync(ch.dev, stream);
-    if (!ptrs.empty() || !chunks.empty()) cudaStreamSynchronize(stream);
+    if (!ptrs.empty() || !chunks.empty() || !big.empty()) cudaStreamSynchronize(stream);
+    for (void* p : big) cudaFree(p);
     ptrs.clear();
     chunks.clear();
+    big.clear();
   }
   ~DevBuffers() { release(); }
 
@@ -561,17 +570,16 @@ struct DistHost {  // host view of the distance service (spawn reachability)
   int kind = 0;
   int32_t n = 0, cols = 0;
   int64_t grid_len = 0;
-  const std::vector<int64_t>* table = nullptr;  // [slot*n + x]
+  // table kinds: reach[x * reach_words + t/64] bit t%64 = dist(x, row t) != inf
+  const std::vector<uint64_t>* reach = nullptr;
+  int64_t reach_words = 0;
   const std::vector<int32_t>* slot_of = nullptr;
-  int64_t dist(int32_t x, int32_t dest) const {
-    if (kind == GMACO_DIST_GRID) {
-      const int32_t rx = x / cols, cx = x % cols, rd = dest / cols, cd = dest % cols;
-      return (int64_t)(std::abs(rx - rd) + std::abs(cx - cd)) * grid_len;
-    }
-    const int32_t s = slot_of ? (*slot_of)[dest] : dest;
-    return s < 0 ? kInf : (*table)[(size_t)s * n + x];
+  bool reachable(int32_t u, int32_t v) const {
+    if (kind == GMACO_DIST_GRID) return true;  // a validated lattice is strongly connected
+    const int32_t s = slot_of ? (*slot_of)[v] : v;
+    if (s < 0) return false;
+    return ((*reach)[(size_t)u * reach_words + (s >> 6)] >> (s & 63)) & 1u;
   }
-  bool reachable(int32_t u, int32_t v) const { return dist(u, v) != kInf; }
 };
 
 Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
@@ -681,7 +689,7 @@ void ensure_device(gmaco_engine* h) {
 // (all_pairs_distances / dijkstra_to results, net.cpp:359-437): returns the
 // device table [T][n] (owned by B) and copies it to `host` for setup (spawn).
 int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::vector<int32_t>& dests,
-                               std::vector<int64_t>& host) {
+                               std::vector<uint64_t>& reach, int64_t& reach_words) {
   const int32_t n = g.n, T = (int32_t)dests.size();
   const size_t total = (size_t)T * n;
   if (total >= (size_t(1) << 32)) throw ValidationError("distance table exceeds 2^32 entries");
@@ -722,9 +730,15 @@ int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::v
   if (pt.on) std::fprintf(stderr, "[gmaco create] sssp: %d rounds, %zu state relaxations (%.2f per state)\n", iters,
                           relaxed, (double)relaxed / (double)total);
   pt.mark("sssp rounds");
-  host.resize(total);
-  CK(cudaMemcpy(host.data(), a.D, total * 8, cudaMemcpyDeviceToHost));
-  pt.mark("table download");
+  // spawn needs reachability only: a per-node bitmap over the table rows
+  // (n * ceil(T/64) words) instead of the whole int64 table
+  reach_words = (T + 63) / 64;
+  uint64_t* rb = tmp.alloc<uint64_t>((size_t)n * reach_words);
+  CK(build_reach_bits(a.D, T, n, reach_words, rb, h->stream));
+  reach.resize((size_t)n * reach_words);
+  CK(cudaMemcpyAsync(reach.data(), rb, reach.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  pt.mark("reachability bitmap");
   return a.D;
 }
 
@@ -753,22 +767,29 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   DistHost dh;
   dh.kind = dd->kind;
   dh.n = n;
-  std::vector<int64_t> table;
+  std::vector<int64_t> table;  // user-supplied dense table only
+  std::vector<uint64_t> reach;
   std::vector<int32_t> slot_of, targets;
   w.d.kind = dd->kind == GMACO_DIST_GRID ? 1 : 0;
   w.d.n = n;
   if (dd->kind == GMACO_DIST_DENSE) {
-    table.resize((size_t)n * n);
     if (dd->dist_mm) {
+      table.resize((size_t)n * n);
+      dh.reach_words = (n + 63) / 64;
+      reach.assign((size_t)n * dh.reach_words, 0);
       for (int32_t u = 0; u < n; ++u)
-        for (int32_t v = 0; v < n; ++v) table[(size_t)v * n + u] = dd->dist_mm[(size_t)u * n + v];
+        for (int32_t v = 0; v < n; ++v) {
+          const int64_t dv = dd->dist_mm[(size_t)u * n + v];
+          table[(size_t)v * n + u] = dv;
+          if (dv != kInf) reach[(size_t)u * dh.reach_words + (v >> 6)] |= uint64_t(1) << (v & 63);
+        }
     } else {  // all_pairs_distances (net.cpp:419-437): every node a destination, on the device
       ensure_device(h);
       std::vector<int32_t> all(n);
       for (int32_t d = 0; d < n; ++d) all[d] = d;
-      w.d.table = device_distance_table(h, g, all, table);
+      w.d.table = device_distance_table(h, g, all, reach, dh.reach_words);
     }
-    dh.table = &table;
+    dh.reach = &reach;
   } else if (dd->kind == GMACO_DIST_GRID) {
     const int32_t R = dd->grid_rows, Cc = dd->grid_cols;
     if (R < 2 || Cc < 2 || (int64_t)R * Cc != n)
@@ -797,8 +818,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       slot_of[x] = t;
     }
     ensure_device(h);
-    w.d.table = device_distance_table(h, g, targets, table);
-    dh.table = &table;
+    w.d.table = device_distance_table(h, g, targets, reach, dh.reach_words);
+    dh.reach = &reach;
     dh.slot_of = &slot_of;
   } else {
     throw ValidationError(fmt("unknown distance kind %d", dd->kind));

@@ -2471,6 +2471,29 @@ cudaError_t sssp_relax(const SsspArgs& a, const uint32_t* cur, uint32_t count, u
   return cudaGetLastError();
 }
 
+// Reachability bitmap of a distance table for the host's spawn:
+// out[x * words + t/64] bit t%64 = D[t][x] != inf.  Threads run over x, so
+// the loads of a table row are coalesced.
+__global__ void k_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t words, uint64_t* out) {
+  const int64_t total = (int64_t)n * words;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t wd = i / n, x = i - wd * n;
+    uint64_t bits = 0;
+    for (int b = 0; b < 64; ++b) {
+      const int64_t t = wd * 64 + b;
+      if (t >= T) break;
+      if (D[t * n + x] != kInf) bits |= uint64_t(1) << b;
+    }
+    out[x * words + wd] = bits;
+  }
+}
+
+cudaError_t build_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t words, uint64_t* out, cudaStream_t st) {
+  const int64_t total = (int64_t)n * words;
+  k_reach_bits<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(D, T, n, words, out);
+  return cudaGetLastError();
+}
+
 // Progress-filter bitmaps from a device distance table (see DevDist::fbits).
 __global__ void k_fbits(const int64_t* D, int32_t n, int32_t T, const int32_t* col, const int32_t* from, int32_t M,
                         int64_t fbw, uint2* fb) {
