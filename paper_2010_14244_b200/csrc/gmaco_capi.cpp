@@ -708,27 +708,23 @@ int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::v
   a.D = B.alloc_direct<int64_t>(total);  // written by kernels before the arena seal
   a.inq = tmp.alloc<uint32_t>(total);
   CK(cudaMemsetAsync(a.inq, 0, total * 4, h->stream));
-  uint32_t* q[2] = {tmp.alloc<uint32_t>(total), tmp.alloc<uint32_t>(total)};
-  uint32_t* cnt = tmp.alloc<uint32_t>(2);
+  // near in/out and far cur/next lists (a state is in at most one list: inq)
+  uint32_t* q[4] = {tmp.alloc<uint32_t>(total), tmp.alloc<uint32_t>(total), tmp.alloc<uint32_t>(total),
+                    tmp.alloc<uint32_t>(total)};
+  uint32_t* cnt = tmp.alloc<uint32_t>(4);
   const int32_t* ddests = tmp.upload(dests);
   CK(sssp_fill_seed(a.D, total, ddests, T, n, q[0], h->stream));
   CK(cudaStreamSynchronize(h->stream));
   pt.mark("sssp setup (reverse CSR, alloc)");
-  uint32_t count = (uint32_t)T, host_cnt = 0;
-  int cur = 0, iters = 0;
-  size_t relaxed = 0;
-  while (count) {
-    ++iters;
-    relaxed += count;
-    CK(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, h->stream));
-    CK(sssp_relax(a, q[cur], count, q[cur ^ 1], cnt + (cur ^ 1), h->stream));
-    CK(cudaMemcpyAsync(&host_cnt, cnt + (cur ^ 1), 4, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    count = host_cnt;
-    cur ^= 1;
-  }
-  if (pt.on) std::fprintf(stderr, "[gmaco create] sssp: %d rounds, %zu state relaxations (%.2f per state)\n", iters,
-                          relaxed, (double)relaxed / (double)total);
+  // every round inside one persistent cooperative kernel (k_sssp_coop)
+  // near/far threshold step: a few mean edge lengths (GMACO_SSSP_DELTA overrides, in edge lengths)
+  int64_t lsum = 0;
+  for (int32_t e = 0; e < g.m; ++e) lsum += g.len[e];
+  const double mult = std::getenv("GMACO_SSSP_DELTA") ? std::atof(std::getenv("GMACO_SSSP_DELTA")) : 32.0;
+  const int64_t delta = std::max<int64_t>(1, (int64_t)(mult * (double)lsum / std::max(1, g.m)));
+  CK(cudaMemsetAsync(cnt, 0, 16, h->stream));
+  CK(sssp_run_coop(a, q, cnt, (uint32_t)T, delta, h->device, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   pt.mark("sssp rounds");
   // spawn needs reachability only: a per-node bitmap over the table rows
   // (n * ceil(T/64) words) instead of the whole int64 table

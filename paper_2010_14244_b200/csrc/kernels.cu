@@ -2430,44 +2430,107 @@ __global__ void k_sssp_seed(int64_t* D, const int32_t* dests, int32_t T, int32_t
   cur[t] = item;
 }
 
-__global__ void __launch_bounds__(256) k_sssp_relax(SsspArgs a, const uint32_t* cur, uint32_t count, uint32_t* nxt,
-                                                    uint32_t* nnxt) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-    const uint32_t item = cur[i];
-    const uint32_t t = item / (uint32_t)a.n, u = item - t * (uint32_t)a.n;
-    a.inq[item] = 0;  // before reading D: a later improvement re-queues the state
-    __threadfence();
-    const int64_t du = *((volatile int64_t*)(a.D + item));
-    int64_t* Drow = a.D + (size_t)t * a.n;
-    for (int32_t k = a.rptr[u]; k < a.rptr[u + 1]; ++k) {
-      const int32_t v = a.rsrc[k];
-      const int64_t nd = du + a.rlen[k];
-      if (nd < Drow[v]) {
-        const long long old = atomicMin(reinterpret_cast<long long*>(Drow + v), (long long)nd);
-        if (nd < old) __threadfence();  // pairs with the reader's flag-clear fence (store-buffering)
-        if (nd < old && atomicExch(a.inq + (size_t)t * a.n + v, 1u) == 0u) {
-          cg::coalesced_group g = cg::coalesced_threads();  // aggregated append
-          uint32_t base = 0;
-          if (g.thread_rank() == 0) base = atomicAdd(nnxt, (uint32_t)g.size());
-          base = g.shfl(base, 0);
-          nxt[base + g.thread_rank()] = t * (uint32_t)a.n + (uint32_t)v;
+// All rounds in one persistent cooperative launch, near/far ordered
+// (delta-stepping without per-bucket lists): states whose new distance is
+// <= T go to the near frontier, others to a far pile; when the near frontier
+// empties, T grows by delta and the far pile is split (entries already at
+// <= T move to near, the rest are compacted).  Exactness does not depend on
+// delta or on the processing order: every improvement is still relaxed.
+// Lists: q[0]/q[1] near in/out, q[2]/q[3] far cur/next; cnt[0..3] their sizes.
+__device__ __forceinline__ void sssp_append(uint32_t* list, uint32_t* n, uint32_t item) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  uint32_t base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(n, (uint32_t)g.size());
+  base = g.shfl(base, 0);
+  list[base + g.thread_rank()] = item;
+}
+
+__global__ void __launch_bounds__(256) k_sssp_coop(SsspArgs a, uint32_t* q0, uint32_t* q1, uint32_t* q2,
+                                                   uint32_t* q3, uint32_t* cnt, uint32_t count, int64_t delta) {
+  cg::grid_group grid = cg::this_grid();
+  uint32_t* nl[2] = {q0, q1};
+  uint32_t* fl[2] = {q2, q3};
+  int cur = 0, fcur = 0;
+  int64_t T = delta;
+  uint32_t nfar = 0;
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
+  for (;;) {
+    if (count) {
+      const uint32_t* in = nl[cur];
+      for (uint32_t i = gtid; i < count; i += gsz) {
+        const uint32_t item = in[i];
+        const uint32_t t = item / (uint32_t)a.n, u = item - t * (uint32_t)a.n;
+        a.inq[item] = 0;
+        __threadfence();
+        const int64_t du = *((volatile int64_t*)(a.D + item));
+        int64_t* Drow = a.D + (size_t)t * a.n;
+        for (int32_t k = a.rptr[u]; k < a.rptr[u + 1]; ++k) {
+          const int32_t v = a.rsrc[k];
+          const int64_t nd = du + a.rlen[k];
+          if (nd < Drow[v]) {
+            const long long old = atomicMin(reinterpret_cast<long long*>(Drow + v), (long long)nd);
+            if (nd < old) __threadfence();
+            if (nd < old && atomicExch(a.inq + (size_t)t * a.n + v, 1u) == 0u) {
+              const uint32_t it = t * (uint32_t)a.n + (uint32_t)v;
+              if (nd <= T)
+                sssp_append(nl[cur ^ 1], cnt + (cur ^ 1), it);
+              else
+                sssp_append(fl[fcur], cnt + 2 + fcur, it);
+            }
+          }
         }
       }
+      grid.sync();
+      if (grid.thread_rank() == 0) cnt[cur] = 0;
+      count = *((volatile uint32_t*)(cnt + (cur ^ 1)));
+      nfar = *((volatile uint32_t*)(cnt + 2 + fcur));
+      grid.sync();
+      cur ^= 1;
+      continue;
     }
+    if (!nfar) break;  // both frontiers empty: done
+    // near frontier empty: raise the threshold and split the far pile
+    T += delta;
+    const uint32_t* fin = fl[fcur];
+    for (uint32_t i = gtid; i < nfar; i += gsz) {
+      const uint32_t item = fin[i];
+      if (*((volatile int64_t*)(a.D + item)) <= T)
+        sssp_append(nl[cur], cnt + cur, item);
+      else
+        sssp_append(fl[fcur ^ 1], cnt + 2 + (fcur ^ 1), item);
+    }
+    grid.sync();
+    if (grid.thread_rank() == 0) cnt[2 + fcur] = 0;
+    count = *((volatile uint32_t*)(cnt + cur));
+    nfar = *((volatile uint32_t*)(cnt + 2 + (fcur ^ 1)));
+    grid.sync();
+    fcur ^= 1;
   }
+}
+
+cudaError_t sssp_run_coop(const SsspArgs& a, uint32_t* const* q, uint32_t* cnt, uint32_t count, int64_t delta,
+                          int device, cudaStream_t st) {
+  int per_sm = 0, sms = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sssp_coop, 256, 0);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)std::max(1, per_sm * sms));
+  lc.blockDim = dim3(256);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, k_sssp_coop, a, q[0], q[1], q[2], q[3], cnt, count, delta);
 }
 
 cudaError_t sssp_fill_seed(int64_t* D, size_t total, const int32_t* dests, int32_t T, int32_t n, uint32_t* cur,
                            cudaStream_t st) {
   k_sssp_fill<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(D, total);
   k_sssp_seed<<<blocks_for(T, 256), 256, 0, st>>>(D, dests, T, n, cur);
-  return cudaGetLastError();
-}
-
-cudaError_t sssp_relax(const SsspArgs& a, const uint32_t* cur, uint32_t count, uint32_t* nxt, uint32_t* nnxt,
-                       cudaStream_t st) {
-  const unsigned blocks = (unsigned)std::min<uint32_t>((count + 255) / 256, 148u * 8u);
-  k_sssp_relax<<<blocks, 256, 0, st>>>(a, cur, count, nxt, nnxt);
   return cudaGetLastError();
 }
 
