@@ -463,3 +463,40 @@ def test_double_buffered_readback_every_step():
     ref = cpu.vehicles()
     for f, arr in bufs[13 % 2].items():
         assert np.array_equal(arr, ref[f]), f
+
+
+COLONY_OPTIONS = [
+    dict(congestion=0, deposit=abi.DEPOSIT_BEST_TOUR, congestion_evaporation=0, replan_all=0),
+    dict(congestion=1, deposit=abi.DEPOSIT_COMPLETION, congestion_evaporation=1, replan_all=1),
+    dict(congestion=1, deposit=abi.DEPOSIT_BEST_TOUR, congestion_evaporation=0, replan_all=1, hop_limit=5),
+    dict(congestion=0, deposit=abi.DEPOSIT_BEST_TOUR, congestion_evaporation=1, replan_all=0, hop_limit=3),
+    dict(congestion=1, deposit=abi.DEPOSIT_NONE, congestion_evaporation=1, replan_all=1),
+]
+
+
+@pytest.mark.parametrize("opts", range(len(COLONY_OPTIONS)))
+@pytest.mark.parametrize("graph", ["lattice", "rgg"])
+def test_colony_option_matrix(graph, opts):
+    """Colony switches (congestion, deposit kind, congestion evaporation,
+    replan_all, hop_limit) on the lattice walker and the ant-queue walker."""
+    if graph == "lattice":
+        net = networks.grid(14, 14, signals="all")
+        dist_factory = net.grid_distance
+        keep = None
+    else:
+        net, dist, keep = _rgg_targets(2500, 10, 41)
+        dist_factory = lambda: dist
+    cfg = abi.colony_production(_cfg("colony", 250, 31, max_steps=45), ants=32)
+    for kk, vv in COLONY_OPTIONS[opts].items():
+        setattr(cfg.colony, kk, vv)
+    cfg.colony.max_hops = 512
+    gpu = Engine(net, cfg, dist_factory())
+    cpu = O.PortWorld(net, cfg, dist_factory())
+    for k in (1, 4, 9):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, f"{graph} opts {opts}")
+        for vid in range(0, 250, 4):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    assert O.results_identical(gpu.run(), cpu.run())
+    del keep
