@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C4 (1M-node road graph) secondary measurement of the default C2 run")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
                     help="BASELINE.json config (c2 = the metric's single-GPU config, the default)")
@@ -138,6 +140,42 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def secondary_c4(peak, peak_src, steps=10, warmup=3):
+    """C4 (the north star's 100k-vehicle road-graph config) on the same GPU:
+    the HBM-bound ant-queue walker beside the latency-bound C2 headline.
+    Same rules as the headline: L2 flushed before each iteration, CUDA events
+    (three per iteration here: begin, walk end, step end)."""
+    from paper_2010_14244_b200 import workloads
+    from paper_2010_14244_b200.engine import Engine
+    net, cfg, dist, keep = workloads.c4(seed=1, max_steps=warmup + steps + 1)
+    e = Engine(net, cfg, dist)
+    e.step(warmup)
+    c0 = e.counters()
+    walk, stepms = e.bench_steps(steps, L2_FLUSH_BYTES, "both")
+    c1 = e.counters()
+    e.close()
+    del keep
+    ant_steps = c1.ant_steps - c0.ant_steps
+    alg = c1.walk_bytes - c0.walk_bytes
+    walk_s = float(walk.sum()) / 1e3
+    achieved = alg / walk_s / 1e9 if walk_s > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as f:
+            traffic = json.load(f)["c4"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
+    return {"workload": "C4: " + workloads.DESCRIPTIONS["c4"], "metric": "ant-steps/sec",
+            "value": ant_steps / (float(stepms.sum()) / 1e3), "unit": "ant-steps/s",
+            "ms_per_step": float(stepms.mean()), "iterations_timed": steps,
+            "vehicle_routes_per_sec": (c1.vehicle_routes - c0.vehicle_routes) / (float(stepms.sum()) / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_colony_q (ant-queue walk; pro/epi kernels inside the timed walk)",
+                         "algorithmic_bytes_per_launch": alg / steps,
+                         "avg_launch_us": walk_s / steps * 1e6}}
 
 
 def measured_peak():
@@ -448,6 +486,8 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
         "completed_vehicles_e2e": completed,
     }
+    if world == 1 and not args.no_secondary and args.config == "c2":
+        line["secondary"] = secondary_c4(peak, peak_src)
     if world == 1 and not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     eng.close()
