@@ -236,7 +236,207 @@ struct Net {
   std::vector<int64_t> len;
 };
 
-Net build_net(const std::string& text) {
+struct NodeRec {
+  int64_t id;
+  bool sig, pos;
+  double x, y;
+};
+struct EdgeRec {
+  int64_t id, from, to, len;
+  int64_t lanes;
+};
+
+// Fast path for well-formed documents of the common shape: top-level
+// "nodes" / "edges" arrays of objects with known keys (each at most once),
+// escape-free keys, plain numeric literals.  Fills the records directly (no
+// DOM) and returns false on anything else — the exact DOM parser then runs
+// and produces the reference's behaviour and messages.
+struct Fast {
+  const char* p;
+  const char* e;
+  void ws() {
+    while (p < e && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+  }
+  bool lit(char c) {
+    ws();
+    if (p < e && *p == c) {
+      ++p;
+      return true;
+    }
+    return false;
+  }
+  bool key(const char*& k, size_t& kl) {  // escape-free string, then ':'
+    ws();
+    if (p >= e || *p != '"') return false;
+    const char* s = ++p;
+    while (p < e && *p != '"') {
+      if (*p == '\\' || (unsigned char)*p < 0x20) return false;
+      ++p;
+    }
+    if (p >= e) return false;
+    k = s;
+    kl = (size_t)(p - s);
+    ++p;
+    return lit(':');
+  }
+  // JSON number literal: integer (no fraction/exponent) or float
+  bool number(bool& is_int, int64_t& iv, double& dv) {
+    ws();
+    const char* s = p;
+    if (p < e && *p == '-') ++p;
+    if (p >= e || *p < '0' || *p > '9') return false;
+    if (*p == '0' && p + 1 < e && p[1] >= '0' && p[1] <= '9') return false;  // leading zero: let the DOM parser report
+    while (p < e && *p >= '0' && *p <= '9') ++p;
+    is_int = true;
+    if (p < e && *p == '.') {
+      is_int = false;
+      ++p;
+      if (p >= e || *p < '0' || *p > '9') return false;
+      while (p < e && *p >= '0' && *p <= '9') ++p;
+    }
+    if (p < e && (*p == 'e' || *p == 'E')) {
+      is_int = false;
+      ++p;
+      if (p < e && (*p == '+' || *p == '-')) ++p;
+      if (p >= e || *p < '0' || *p > '9') return false;
+      while (p < e && *p >= '0' && *p <= '9') ++p;
+    }
+    if (is_int) {
+      const auto r = std::from_chars(s, p, iv);
+      if (r.ec != std::errc() || r.ptr != p) return false;  // out of int64 range: DOM path
+      dv = (double)iv;
+    } else {
+      const auto r = std::from_chars(s, p, dv);
+      if (r.ec != std::errc() || r.ptr != p) return false;
+    }
+    return true;
+  }
+  bool boolean(bool& b) {
+    ws();
+    if (e - p >= 4 && !std::memcmp(p, "true", 4)) {
+      b = true;
+      p += 4;
+      return true;
+    }
+    if (e - p >= 5 && !std::memcmp(p, "false", 5)) {
+      b = false;
+      p += 5;
+      return true;
+    }
+    return false;
+  }
+  static bool is(const char* k, size_t kl, const char* name) {
+    return std::strlen(name) == kl && !std::memcmp(k, name, kl);
+  }
+  bool node(NodeRec& r) {
+    if (!lit('{')) return false;
+    unsigned seen = 0;
+    bool have_x = false, have_y = false;
+    r = NodeRec{0, false, false, 0.0, 0.0};
+    if (lit('}')) return false;  // no id: DOM path reports
+    do {
+      const char* k;
+      size_t kl;
+      if (!key(k, kl)) return false;
+      bool isi;
+      int64_t iv;
+      double dv;
+      if (is(k, kl, "id")) {
+        if (seen & 1 || !number(isi, iv, dv) || !isi) return false;
+        r.id = (int64_t)(int32_t)iv;
+        seen |= 1;
+      } else if (is(k, kl, "signalized")) {
+        if (seen & 2 || !boolean(r.sig)) return false;
+        seen |= 2;
+      } else if (is(k, kl, "x")) {
+        if (seen & 4 || !number(isi, iv, dv)) return false;
+        r.x = dv;
+        have_x = true;
+        seen |= 4;
+      } else if (is(k, kl, "y")) {
+        if (seen & 8 || !number(isi, iv, dv)) return false;
+        r.y = dv;
+        have_y = true;
+        seen |= 8;
+      } else {
+        return false;
+      }
+    } while (lit(','));
+    if (!lit('}')) return false;
+    if ((seen & 3) != 3 || have_x != have_y) return false;
+    r.pos = have_x;
+    return true;
+  }
+  bool edge(EdgeRec& r) {
+    if (!lit('{')) return false;
+    unsigned seen = 0;
+    r = EdgeRec{};
+    if (lit('}')) return false;
+    do {
+      const char* k;
+      size_t kl;
+      if (!key(k, kl)) return false;
+      bool isi;
+      int64_t iv;
+      double dv;
+      int bit;
+      if (is(k, kl, "id")) bit = 0;
+      else if (is(k, kl, "from")) bit = 1;
+      else if (is(k, kl, "to")) bit = 2;
+      else if (is(k, kl, "length_m")) bit = 3;
+      else if (is(k, kl, "lanes")) bit = 4;
+      else return false;
+      if (seen & (1u << bit) || !number(isi, iv, dv)) return false;
+      seen |= 1u << bit;
+      switch (bit) {
+        case 0: if (!isi) return false; r.id = (int32_t)iv; break;
+        case 1: if (!isi) return false; r.from = (int32_t)iv; break;
+        case 2: if (!isi) return false; r.to = (int32_t)iv; break;
+        case 3: r.len = std::llround(dv * 1000.0); break;  // meters_to_mm, net.cpp:34
+        case 4: if (!isi) return false; r.lanes = (int32_t)iv; break;
+      }
+    } while (lit(','));
+    if (!lit('}')) return false;
+    return seen == 31u;
+  }
+  template <class Rec, class F>
+  bool array(std::vector<Rec>& out, F&& one) {
+    if (!lit('[')) return false;
+    if (lit(']')) return true;
+    do {
+      out.emplace_back();
+      if (!one(out.back())) return false;
+    } while (lit(','));
+    return lit(']');
+  }
+};
+
+bool fast_parse(const std::string& text, std::vector<NodeRec>& nodes, std::vector<EdgeRec>& edges) {
+  Fast f{text.data(), text.data() + text.size()};
+  if (!f.lit('{')) return false;
+  bool hn = false, he = false;
+  do {
+    const char* k;
+    size_t kl;
+    if (!f.key(k, kl)) return false;
+    if (Fast::is(k, kl, "nodes") && !hn) {
+      nodes.reserve(text.size() / 160);
+      if (!f.array(nodes, [&](NodeRec& r) { return f.node(r); })) return false;
+      hn = true;
+    } else if (Fast::is(k, kl, "edges") && !he) {
+      edges.reserve(text.size() / 120);
+      if (!f.array(edges, [&](EdgeRec& r) { return f.edge(r); })) return false;
+      he = true;
+    } else {
+      return false;
+    }
+  } while (f.lit(','));
+  if (!f.lit('}')) return false;
+  f.ws();
+  return f.p == f.e && hn && he;
+}
+
+void dom_parse(const std::string& text, std::vector<NodeRec>& nodes, std::vector<EdgeRec>& edges) {
   Parser ps{text.data(), text.data() + text.size(), text.data()};
   Val doc;
   ps.parse(doc);
@@ -247,23 +447,12 @@ Net build_net(const std::string& text) {
   const Val* jn = doc.get("nodes");
   const Val* je = doc.get("edges");
   if (!jn || !je) throw NetValidation("network document requires \"nodes\" and \"edges\"");
-  struct Node {
-    int64_t id;
-    bool sig, pos;
-    double x, y;
-  };
-  struct Edge {
-    int64_t id, from, to, len;
-    int64_t lanes;
-  };
-  std::vector<Node> nodes;
-  std::vector<Edge> edges;
   for (const Val& v : jn->arr) {  // net.cpp:123-141
     if (v.kind != Val::Obj) throw NetValidation("node entries must be objects");
     reject_unknown(v, {"id", "signalized", "x", "y"}, "node entry");
     const Val* id = v.get("id");
     if (!id || id->kind != Val::Int) throw NetValidation("node entry missing integer \"id\"");
-    Node nd{(int64_t)(int32_t)id->i, false, false, 0.0, 0.0};
+    NodeRec nd{(int64_t)(int32_t)id->i, false, false, 0.0, 0.0};
     const Val* sg = v.get("signalized");
     if (!sg || sg->kind != Val::Bool)
       throw NetValidation("node " + std::to_string(nd.id) + " missing boolean \"signalized\"");
@@ -283,7 +472,7 @@ Net build_net(const std::string& text) {
     reject_unknown(v, {"id", "from", "to", "length_m", "lanes"}, "edge entry");
     for (const char* k : {"id", "from", "to", "length_m", "lanes"})
       if (!v.get(k)) throw NetValidation("edge entry missing \"" + std::string(k) + "\"");
-    Edge e{};
+    EdgeRec e{};
     e.id = (int32_t)v.get("id")->as_int();
     e.from = (int32_t)v.get("from")->as_int();
     e.to = (int32_t)v.get("to")->as_int();
@@ -295,18 +484,22 @@ Net build_net(const std::string& text) {
     e.lanes = (int32_t)ln->i;
     edges.push_back(e);
   }
-  // RoadNetwork ctor (net.cpp:38-98): dense ids, then per-edge checks in input order
+}
+
+// RoadNetwork ctor (net.cpp:38-98): dense ids, then per-edge checks in input
+// order; the SoA arrays in id order.
+Net finish_net(const std::vector<NodeRec>& nodes, const std::vector<EdgeRec>& edges) {
   const int64_t n = (int64_t)nodes.size(), m = (int64_t)edges.size();
   if (n == 0) throw NetValidation("network has no nodes");
   std::vector<char> seen(n, 0);
-  for (const Node& nd : nodes) {
+  for (const NodeRec& nd : nodes) {
     if (nd.id < 0 || nd.id >= n)
       throw NetValidation("node id " + std::to_string(nd.id) + " out of dense range 0.." + std::to_string(n - 1));
     if (seen[nd.id]) throw NetValidation("duplicate node id " + std::to_string(nd.id));
     seen[nd.id] = 1;
   }
   std::vector<char> eseen(m, 0);
-  for (const Edge& e : edges) {
+  for (const EdgeRec& e : edges) {
     if (e.id < 0 || e.id >= m)
       throw NetValidation("edge id " + std::to_string(e.id) + " out of dense range 0.." + std::to_string(m - 1));
     if (eseen[e.id]) throw NetValidation("duplicate edge id " + std::to_string(e.id));
@@ -324,7 +517,7 @@ Net build_net(const std::string& text) {
   out.has_pos.resize(n);
   out.x.resize(n);
   out.y.resize(n);
-  for (const Node& nd : nodes) {
+  for (const NodeRec& nd : nodes) {
     out.sig[nd.id] = nd.sig;
     out.has_pos[nd.id] = nd.pos;
     out.x[nd.id] = nd.x;
@@ -334,7 +527,7 @@ Net build_net(const std::string& text) {
   out.to.resize(m);
   out.len.resize(m);
   out.lanes.resize(m);
-  for (const Edge& e : edges) {
+  for (const EdgeRec& e : edges) {
     out.from[e.id] = (int32_t)e.from;
     out.to[e.id] = (int32_t)e.to;
     out.len[e.id] = e.len;
@@ -351,6 +544,17 @@ Net build_net(const std::string& text) {
   std::string verr;  // duplicate edges between a node pair (net.cpp:87-96)
   if (!gmaco::validate_graph_desc(&d, &verr)) throw NetValidation(verr);
   return out;
+}
+
+Net build_net(const std::string& text) {
+  std::vector<NodeRec> nodes;
+  std::vector<EdgeRec> edges;
+  if (!fast_parse(text, nodes, edges)) {  // anything unusual: the exact DOM parser
+    nodes.clear();
+    edges.clear();
+    dom_parse(text, nodes, edges);
+  }
+  return finish_net(nodes, edges);
 }
 
 // nlohmann::json::dump number format: shortest round-trip digits, ".0" on
