@@ -29,9 +29,27 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# NCCL's banner / warnings go to stderr: stdout carries exactly one JSON line
-os.environ.setdefault("NCCL_DEBUG", "WARN")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_RESULT_FD = None
+
+
+def isolate_stdout() -> None:
+    """stdout carries exactly one JSON line: fd 1 is pointed at stderr for
+    the whole run (NCCL banners, CUDA / library prints land there) and the
+    result line goes to the saved original stdout (emit())."""
+    global _RESULT_FD
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+def emit(obj) -> None:
+    text = json.dumps(obj) + "\n"
+    if _RESULT_FD is None:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, text.encode())
 
 import numpy as np  # noqa: E402
 
@@ -221,7 +239,7 @@ def run_reference(args, rank, world):
         return
     from oracle import oracle as O
     if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"})
         return
     threads = os.cpu_count() or 1
     smp = RefSampler(threads)
@@ -246,7 +264,7 @@ def run_reference(args, rank, world):
                                    f"next_node_aco tours on {threads} std::threads + sequential_step"},
         "e2e": {"value": value, "unit": "ant-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def cpu_baseline(seconds):
@@ -491,12 +509,13 @@ def run_ours(args, rank, world, local):
     if world == 1 and not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     eng.close()
-    print(json.dumps(line))
+    emit(line)
     if dist:
         dist.destroy_process_group()
 
 
 def main():
+    isolate_stdout()
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":

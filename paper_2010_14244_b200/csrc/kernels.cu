@@ -2132,27 +2132,29 @@ __global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
     v.state[vid] = kRetired;
 }
 
-// colony mode: remote vehicles' decisions, then their motion (E2) and the
+// colony mode: a remote vehicle's decision, then its motion (E2) and the
 // next step's counts, exactly as the walk kernel does for its own shard
+__device__ __forceinline__ void apply_remote_one(const DevWorld& w, int32_t vid, long long& act, long long& unf) {
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  if (v.state[vid] == kPending && v.depart[vid] == step) {
+    v.state[vid] = kAtNode;
+    v.at_node[vid] = v.origin[vid];
+  }
+  const int32_t rec = v.dec_rec[vid];
+  if (rec >= 0)
+    take_edge(w, vid, rec, false, v.at_node[vid]);
+  else if (rec == -2)
+    v.state[vid] = kRetired;
+  veh_move(w, vid, act, unf);
+}
+
 __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
   if (skip_step(w.ctl)) return;
   __shared__ long long red[32];
   const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
   long long act = 0, unf = 0;
-  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) {
-    const DevVehicles& v = w.v;
-    const int64_t step = w.ctl->step;
-    if (v.state[vid] == kPending && v.depart[vid] == step) {
-      v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
-    }
-    const int32_t rec = v.dec_rec[vid];
-    if (rec >= 0)
-      take_edge(w, vid, rec, false, v.at_node[vid]);
-    else if (rec == -2)
-      v.state[vid] = kRetired;
-    veh_move(w, vid, act, unf);
-  }
+  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) apply_remote_one(w, vid, act, unf);
   act = block_sum(act, red);
   unf = block_sum(unf, red);
   if (threadIdx.x == 0) {
@@ -2180,6 +2182,20 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const DevParams& p = w.p;
   if (kFusedMotion) {
+    if (p.sharded) {
+      // other ranks' vehicles (their decision records arrived with the
+      // exchange): activation, decision bookkeeping, then motion — what the
+      // walk kernel did for this rank's shard (k_apply_remote_move, folded
+      // in to save a kernel boundary per step)
+      long long act = 0, unf = 0;
+      for (int64_t vid = gtid; vid < p.V; vid += gstride)
+        if (!(vid >= p.shard_lo && vid < p.shard_hi)) apply_remote_one(w, (int32_t)vid, act, unf);
+      act = block_sum(act, red);
+      if (threadIdx.x == 0 && act) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)act);
+      unf = block_sum(unf, red);
+      if (threadIdx.x == 0 && unf) atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unf);
+      grid.sync();
+    }
     // colony mode: E2 already ran inside the walk kernel, so one pass per
     // signal does C, D, E1 (pops the FIFO head) and E3 (appends this step's
     // arrivals after it) — the reference order for each queue
@@ -2682,9 +2698,10 @@ tail:
       cudaError_t e = r.exchange(r.exchange_ctx, st);
       if (e != cudaSuccess) return e;
     }
-    if (fused)
+    const bool coop_tail = r.coop_blocks > 0 && !w.p.need_positions;
+    if (fused && !coop_tail)  // (the cooperative tail applies remote vehicles itself)
       k_apply_remote_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
-    else
+    else if (!fused)
       k_apply_remote<<<blocks_for(V, 256), 256, 0, st>>>(w);
   }
   if (r.coop_blocks > 0 && !w.p.need_positions) {
@@ -2725,7 +2742,8 @@ tail:
 int kernels_per_step(const DevWorld& w, const StepResources& r) {
   int k = 1;                 // stage-B walk / decide
   if (w.p.ant_queue) k += 2; // k_colony_pro + k_colony_epi around k_colony_q
-  if (w.p.sharded) k += 1;   // k_apply_remote
+  if (w.p.sharded && !(w.p.algorithm == 4 && r.coop_blocks > 0 && !w.p.need_positions))
+    k += 1;  // k_apply_remote[_move] (folded into the cooperative colony tail otherwise)
   if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
   if (w.p.S > 0) k += 2;     // k_signals, k_e3
   if (w.p.algorithm != 4) k += 1;  // k_move (colony walks run E2 themselves)
