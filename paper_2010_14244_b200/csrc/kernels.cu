@@ -1567,13 +1567,14 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       const double wr = W[xb + ob];  // in-row (a hole reads 0.0); used only when two
       const double wb = two ? wr : 0.0;
       const double total = __dadd_rn(wa, wb);  // + exact 0.0 for a single candidate
-      const double pt = __dmul_rn(u, total), u2 = __dmul_rn(u, 2.0);
+      const double pt = __dmul_rn(u, total);
       // routing.cpp:100-113: total <= 0 or non-finite picks uniformly
-      // (floor(u*2) >= 1 takes the second), else the first candidate iff
+      // (floor(u*2) >= 1 takes the second; u = (bits>>11)*2^-53 exactly, so
+      // u*2 >= 1 iff bit 63 is set), else the first candidate iff
       // u*total < wa (default: the last candidate)
-      const unsigned bad = (unsigned)!(total > 0.0) |
-                           (unsigned)(__double_as_longlong(fabs(total)) >= 0x7ff0000000000000ll);
-      const unsigned tb = (unsigned)two & ((bad & (unsigned)(u2 >= 1.0)) | (~bad & (unsigned)!(pt < wa)));
+      const unsigned bad = (unsigned)!((total > 0.0) & (total <= 1.7976931348623157e308));
+      const unsigned hi = (unsigned)(bits >> 63);
+      const unsigned tb = (unsigned)two & ((bad & hi) | (~bad & (unsigned)!(pt < wa)));
       const unsigned mv = tb ? (unsigned)!a_is_v : (unsigned)a_is_v;
       const int32_t s = xb + (mv ? off_v : off_h);
       cost += kSmem ? (int64_t)Cst32[s] : Cst[s];
