@@ -1423,6 +1423,58 @@ __device__ __forceinline__ size_t grid_staged_bytes_dev(const DevWorld& w) {
 //                  (bit_words per ant); the winner's tour is rebuilt
 //                  arithmetically (prefix popcounts) into v.plan.  No
 //                  per-hop global stores.
+// degree_sum and two-candidate counters of a monotone lattice walk from its
+// move bits (hop i: word i/64, bit 63-(i%64); 1 = vertical), equal to summing
+// per hop: rows change only on vertical moves, so the hops standing on the
+// start row are those before the first vertical move and the hops on the
+// final row those after the last one (a hop counts the node it departs from,
+// so the first vertical move still stands on the start row; rows strictly
+// between are interior);
+// columns likewise with horizontal moves.  A hop has two candidates while
+// both vertical and horizontal distance remain: hop i <= the index of the
+// RV-th vertical and of the RH-th horizontal move (n when not made).
+__device__ __forceinline__ void walk_counters_from_bits(const unsigned long long* wb, int32_t n, int32_t RV,
+                                                        int32_t RH, int32_t rx, int32_t cx, int32_t dr, int32_t dc,
+                                                        int32_t rows, int32_t cols, int32_t& idegs,
+                                                        int32_t& n_two) {
+  if (n <= 0) return;
+  int32_t nv = 0, fv = -1, lv = -1, fh = -1, lh = -1;
+  const int32_t words = (n + 63) >> 6;
+  for (int32_t j = 0; j < words; ++j) {
+    const unsigned long long wv = wb[j];
+    const int32_t valid = min(64, n - 64 * j);
+    const unsigned long long mask = valid == 64 ? ~0ull : (~0ull << (64 - valid));
+    const unsigned long long wh = ~wv & mask;
+    nv += __popcll(wv);
+    if (wv) {
+      if (fv < 0) fv = 64 * j + __clzll(wv);
+      lv = 64 * j + 63 - (__ffsll((long long)wv) - 1);
+    }
+    if (wh) {
+      if (fh < 0) fh = 64 * j + __clzll(wh);
+      lh = 64 * j + 63 - (__ffsll((long long)wh) - 1);
+    }
+  }
+  const int32_t nh = n - nv;
+  auto border_r = [&](int32_t r) { return (r == 0) + (r == rows - 1); };
+  auto border_c = [&](int32_t c) { return (c == 0) + (c == cols - 1); };
+  int32_t sub = 0;
+  if (nv == 0) {
+    sub += n * border_r(rx);
+  } else {
+    sub += (fv + 1) * border_r(rx) + (n - 1 - lv) * border_r(rx + dr * nv);  // hop fv departs from row rx
+  }
+  if (nh == 0) {
+    sub += n * border_c(cx);
+  } else {
+    sub += (fh + 1) * border_c(cx) + (n - 1 - lh) * border_c(cx + dc * nh);
+  }
+  idegs += 4 * n - sub;
+  const int32_t cv = RV == 0 ? 0 : (nv >= RV ? lv + 1 : n);  // nv == RV: the RV-th vertical move is the last
+  const int32_t chh = RH == 0 ? 0 : (nh >= RH ? lh + 1 : n);
+  n_two += min(cv, chh);
+}
+
 enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 
 // kOneVeh: the CTA holds exactly one vehicle's colony (threads == K, K a
@@ -1586,12 +1638,14 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
           hb = 0;
         }
       }
-      // out-degree of x on the validated full lattice (degree_sum counter)
-      idegs += (rr > 0) + (rr < rows - 1) + (cq > 0) + (cq < cols - 1);
-      n_two += two;
+      if (kTour != kTourBits) {  // move-bit walks derive both counters after the walk
+        // out-degree of x on the validated full lattice (degree_sum counter)
+        idegs += (rr > 0) + (rr < rows - 1) + (cq > 0) + (cq < cols - 1);
+        n_two += two;
+        rr += mv ? dr : 0;
+        cq += mv ? 0 : dc;
+      }
       x += mv ? step_v : step_h;
-      rr += mv ? dr : 0;
-      cq += mv ? 0 : dc;
       rem_v -= mv;
       rem_h -= mv ^ 1u;
     };
@@ -1615,12 +1669,16 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       }
       if (n & 1) hop(((uint64_t)cur.x << 32) | cur.y);
     }
+    if (kTour == kTourBits) {
+      if (hb) bits_w[threadIdx.x * nw + wj] = mbits << (64 - hb);  // left-aligned
+      walk_counters_from_bits(bits_w + threadIdx.x * nw, n, abs(rd - rx), abs(cd - cx), rx, cx, dr, dc, rows, cols,
+                              idegs, n_two);
+    }
     if (capped) cost = kInf;
     hops = n;
     steps = n;
     degs = idegs;
     cands = n + n_two;
-    if (kTour == kTourBits && hb) bits_w[threadIdx.x * nw + wj] = mbits << (64 - hb);  // left-aligned
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
     if (kTour == kTourBits && (K & 31) == 0) {
