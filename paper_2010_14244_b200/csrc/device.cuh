@@ -142,6 +142,7 @@ struct DevVehicles {
   int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
   int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)
   int32_t* plan_ant;            // winning ant per vehicle (scratch mode)
+  const int32_t* walk_order;    // lattice walker: walk slot -> vehicle (walk-length balanced), or nullptr
   // ant-queue walker (general graphs, scratch mode): per-vehicle walk start
   // (-1 = not walking), deciding flag, packed (cost, ant) argmin key, the
   // walking-vehicle list the queue indexes, and per-ant hop counts

@@ -1117,6 +1117,38 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
   dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
   dv.plan_ant = B.filled<int32_t>(V, 0);
+  if (lattice_walker && !std::getenv("GMACO_NO_ORDER")) {
+    // Walk-length balance: vehicles sorted by origin->destination Manhattan
+    // distance, dealt round-robin over the CTAs so every CTA (and SM) holds a
+    // mix of long and short colonies; results do not depend on the order.
+    const int32_t Cc = dd->grid_cols;
+    std::vector<int32_t> ord(V);
+    for (int32_t i = 0; i < V; ++i) ord[i] = i;
+    auto dist = [&](int32_t i) {
+      const int32_t o = sp.origin[i], t = sp.dest[i];
+      return std::abs(o / Cc - t / Cc) + std::abs(o % Cc - t % Cc);
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return dist(a) > dist(b); });
+    // vehicles per CTA of the launch (launch_step): staged tables pack 256/K;
+    // otherwise one vehicle per CTA when K fills whole warps (then the order
+    // is longest-first: CTAs start in index order, LPT packing of the waves)
+    const int32_t K = std::max(1, c.colony.ants);
+    const int32_t vpb = grid_smem_bytes(w) ? std::max(1, 256 / K) : ((K % 32 == 0) ? 1 : std::max(1, 256 / K));
+    const int32_t ctas = (V + vpb - 1) / vpb;
+    // rank r (0 = longest) -> CTA r % ctas, lane r / ctas
+    std::vector<int32_t> order(V, -1);
+    for (int32_t r = 0; r < V; ++r) {
+      const int32_t s = (r % ctas) * vpb + r / ctas;
+      order[s < V ? s : r] = ord[r];
+    }
+    bool ok = true;  // a permutation of 0..V-1 (falls back to identity otherwise)
+    std::vector<char> seen(V, 0);
+    for (int32_t s = 0; s < V; ++s) {
+      if (order[s] < 0 || seen[order[s]]) ok = false;
+      else seen[order[s]] = 1;
+    }
+    if (ok) dv.walk_order = B.upload(order);
+  }
   p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE") && (ell == 8 || align4);
   if (p.ant_queue) {
     // slot records {weight (double), head node, head row (first/4) << 5 | degree}
@@ -1417,6 +1449,7 @@ void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
   w.p.shard_lo = lo;
   w.p.shard_hi = hi;
   w.p.sharded = 1;
+  w.v.walk_order = nullptr;  // a rank walks exactly its own vehicle range
   h->reset_graphs();
 }
 

@@ -1502,8 +1502,9 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
   const int ant = threadIdx.x - lv * K;
-  const int32_t vid = w.p.shard_lo + blockIdx.x * vpb + lv;
-  const bool live = lv < vpb && vid < w.p.shard_hi;
+  const int32_t slot = w.p.shard_lo + blockIdx.x * vpb + lv;  // walk slot; the vehicle via the balance order
+  const bool live = lv < vpb && slot < w.p.shard_hi;
+  const int32_t vid = (w.v.walk_order && live) ? w.v.walk_order[slot] : slot;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
   const double* __restrict__ W = w.weight;

@@ -32,6 +32,8 @@ int kernels_per_step(const DevWorld& w, const StepResources& r);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
+// Lattice walker: bytes of tables staged in SMEM per CTA (0: not staged).
+size_t grid_smem_bytes(const DevWorld& w);
 cudaError_t configure_grid_carveout(const DevWorld& w);
 // Device distance service (exact multi-target SSSP over the reversed graph).
 struct SsspArgs {
