@@ -45,10 +45,15 @@ struct DevDist {
   const int64_t* table;    // [slot * n + x] = dist(x, dest of slot), kInf unreachable
   const int32_t* slot_of;  // node -> table row (targets), nullptr = identity (dense)
   // Progress-filter bitmaps (general-graph walker): per table row t and slot
-  // word, {closer, reach} bits of slot s = dist_t(col[s]) < dist_t(from[s]) and
+  // word, the closer bit of slot s = dist_t(col[s]) < dist_t(from[s]) with
   // dist_t(col[s]) != inf (routing.cpp:16-30 evaluated ahead of time, exact
-  // int64 comparisons); fbw words per row incl. one padding word.
-  const uint2* fbits;
+  // int64 comparisons); fbw words per row incl. one padding word.  No reach
+  // bits: with every edge length > 0 (net.cpp:74-75) a node x != dest with a
+  // finite distance always has a strictly closer out-neighbour (the next node
+  // of a shortest path), and from an infinite-distance node no neighbour is
+  // reachable either, so candidate_neighbors' fallback (routing.cpp:24-29)
+  // never changes the candidate set of a walk.
+  const uint32_t* fbits;
   int64_t fbw;
 };
 

@@ -846,7 +846,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   std::vector<int64_t> off4;
   if (align4) {
     off4.assign(n + 1, 0);
-    for (int32_t u = 0; u < n; ++u) off4[u + 1] = off4[u] + ((g.out_ptr[u + 1] - g.out_ptr[u] + 3) & ~3);
+    // (a row without out-edges still takes 4 padding slots: every row start
+    // is unique, so a head-row descriptor identifies its node)
+    for (int32_t u = 0; u < n; ++u) off4[u + 1] = off4[u] + std::max(4, (g.out_ptr[u + 1] - g.out_ptr[u] + 3) & ~3);
     if (off4[n] >= (int64_t(1) << 29)) throw ValidationError("graph too large for the aligned slot layout");
   }
   const int32_t M = ell ? n * ell : (align4 ? (int32_t)off4[n] : m);
@@ -973,7 +975,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     w.g.nrow = B.upload(nrow);
     const int32_t T = dd->kind == GMACO_DIST_TARGETS ? (int32_t)targets.size() : n;
     const int64_t fbw = (M + 31) / 32 + 1;
-    uint2* fb = B.alloc_direct<uint2>((size_t)T * fbw);  // filled by k_fbits from the device table
+    uint32_t* fb = B.alloc_direct<uint32_t>((size_t)T * fbw);  // filled by k_fbits from the device table
     w.d.fbw = fbw;
     B.flush();  // the kernel reads arena arrays (col, slot_from)
     CK(build_fbits(w, T, fb, h->stream));
@@ -1151,12 +1153,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   }
   p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE") && (ell == 8 || align4);
   if (p.ant_queue) {
-    // slot records {weight (double), head node, head row (first/4) << 5 | degree}
+    // slot records {weight (double), int32 edge cost, head row (first/4) << 5 | degree};
+    // weight and cost are (re)written by sync_rec_weights and stage F+G
     std::vector<int4> rec(M, make_int4(0, 0, -1, 0));
     for (int32_t s = 0; s < M; ++s) {
       if (col[s] < 0) continue;
       const int32_t hd = col[s];
-      rec[s] = make_int4(0, 0, hd, ((row[hd].x >> 2) << 5) | deg[hd]);
+      rec[s] = make_int4(0, 0, 0, (int32_t)((((uint32_t)row[hd].x >> 2) << 5) | (uint32_t)deg[hd]));
     }
     w.rec = B.upload(rec);
     B.flush();  // the kernel below reads arena arrays

@@ -959,10 +959,10 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   int4 tb = make_int4(0, 0, 0, 0);
   long long steps = 0, cands = 0, degs = 0;
   // current ant
-  int32_t vid = 0, ant = 0, dest = 0, first = 0, span = 0, deg = 0, hops = 0;
-  int64_t cost = 0, ec = 0;  // ec: edge cost of the previous hop (load in flight)
+  int32_t vid = 0, ant = 0, dmeta = 0, first = 0, span = 0, deg = 0, hops = 0;
+  int64_t cost = 0;
   bool first_ok = false, active = false;
-  const uint2* fb = nullptr;
+  const uint32_t* fb = nullptr;
   int32_t* tp = nullptr;
   uint4 rnd = make_uint4(0, 0, 0, 0);
   // Grouped form (K divides 32): K consecutive lanes own one vehicle's
@@ -996,17 +996,19 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       vid = v.walkers[a / K];
       ant = (int32_t)(a % K);
       const int32_t x0 = v.walk_start[vid];
-      dest = v.dest[vid];
+      const int32_t dest = v.dest[vid];
       const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
       fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
       const int2 r0 = __ldg(w.g.row + x0);
       first = r0.x;
       span = r0.y;
       deg = __ldg(w.g.deg + x0);
+      // the destination's row descriptor: rows have unique starts, so a hop
+      // reaches dest iff the picked record's descriptor equals it
+      dmeta = (int32_t)(((uint32_t)__ldg(&w.g.row[dest].x) >> 2) << 5) | __ldg(w.g.deg + dest);
       tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
       hops = 0;
       cost = 0;
-      ec = 0;
       first_ok = false;
       active = true;
     }
@@ -1017,12 +1019,12 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       fin = true;
     } else {
       // ---- the hop's single round trip ----
-      uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
+      uint32_t lo = 0, hi = 0;
       if (fb) {
         lo = __ldg(fb + (first >> 5));
         if ((first & 31) + span > 32) hi = __ldg(fb + (first >> 5) + 1);  // row crosses a word
       }
-      int4 rc[W8];  // slot records: weight, head node, head row (span is a multiple of 4)
+      int4 rc[W8];  // slot records: weight, int32 edge cost, head row (span is a multiple of 4)
 #pragma unroll
       for (int i = 0; i < W8; i += 2) {
         if (i < span)
@@ -1033,12 +1035,9 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       double wv[W8];
 #pragma unroll
       for (int i = 0; i < W8; ++i) wv[i] = __hiloint2double(rc[i].y, rc[i].x);
-      cost += ec;  // previous hop's edge cost (its load overlapped this trip)
-      const uint32_t msk = (1u << span) - 1u;
-      const uint32_t closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
-      const uint32_t reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
+      // closer bits only (see DevDist::fbits)
+      const uint32_t cand = __funnelshift_r(lo, hi, first & 31) & ((1u << span) - 1u);
       degs += deg;
-      const uint32_t cand = closer ? closer : reach;
       if (!cand) {
         cost = kInf;
         fin = true;
@@ -1099,37 +1098,39 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
             }
           }
         }
-        int32_t x = -1, meta = 0;
+        int32_t ec = 0, meta = 0;
         if (pick < W8) {
 #pragma unroll
           for (int i = 0; i < W8; ++i)
             if (i == pick) {
-              x = rc[i].z;
+              ec = rc[i].z;
               meta = rc[i].w;
             }
         } else {
           const int4 r = __ldg(R + first + pick);
-          x = r.z;
+          ec = r.z;
           meta = r.w;
         }
         const int32_t sl = first + pick;
-        ec = w.ecost[sl];  // consumed next hop
-        // tour: 4 hops per 16-B store when the scratch stride allows
+        // int32 edge cost from the record; -1 marks a cost >= 2^31 (exact
+        // value in the int64 table, rare)
+        cost += ec >= 0 ? (int64_t)ec : w.ecost[sl];
+        // tour: 4 hops per 16-B streaming store (evict-first: the tours are
+        // read once, by the epilogue) when the scratch stride allows
         tb.x = (hops & 3) == 0 ? sl : tb.x;
         tb.y = (hops & 3) == 1 ? sl : tb.y;
         tb.z = (hops & 3) == 2 ? sl : tb.z;
         tb.w = (hops & 3) == 3 ? sl : tb.w;
         if (!vec_tour)
-          tp[hops] = sl;
+          __stcs(tp + hops, sl);
         else if ((hops & 3) == 3)
-          *reinterpret_cast<int4*>(tp + hops - 3) = tb;
-        first = (meta >> 5) << 2;
+          __stcs(reinterpret_cast<int4*>(tp + hops - 3), tb);
+        fin = meta == dmeta || (hop_limit != 0 && hops + 1 >= hop_limit);
+        first = (int32_t)(((uint32_t)meta >> 5) << 2);
         deg = meta & 31;
         span = ell ? ell : (deg + 3) & ~3;
         ++hops;
         ++steps;
-        fin = x == dest || (hop_limit != 0 && hops >= hop_limit);
-        if (fin) cost += ec;
       }
     }
     if (fin) {
@@ -1289,7 +1290,7 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
     int32_t* tp = kScratch ? v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap : nullptr;
     int64_t cost = 0;
     int32_t x = start;
-    const uint2* __restrict__ fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
+    const uint32_t* __restrict__ fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
     const int2 r0 = __ldg(w.g.row + start);
     int32_t first = r0.x, span = r0.y, deg = __ldg(w.g.deg + start);
     uint4 rnd = make_uint4(0, 0, 0, 0);
@@ -1299,18 +1300,15 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
         break;
       }
       // round trip 1: the row's filter bits and weights (independent loads)
-      uint32_t closer = 0, reach = 0;
+      uint32_t cand = 0;  // closer bits only (see DevDist::fbits)
       if (fb) {
-        const uint2 lo = __ldg(fb + (first >> 5)), hi = __ldg(fb + (first >> 5) + 1);
-        const uint32_t msk = (1u << span) - 1u;
-        closer = __funnelshift_r(lo.x, hi.x, first & 31) & msk;
-        reach = __funnelshift_r(lo.y, hi.y, first & 31) & msk;
+        const uint32_t lo = __ldg(fb + (first >> 5)), hi = __ldg(fb + (first >> 5) + 1);
+        cand = __funnelshift_r(lo, hi, first & 31) & ((1u << span) - 1u);
       }
       double wv[MAXD];
 #pragma unroll
       for (int i = 0; i < MAXD; ++i) wv[i] = i < span ? w.weight[first + i] : 0.0;
       degs += deg;
-      const uint32_t cand = closer ? closer : reach;
       if (!cand) {
         cost = kInf;
         break;
@@ -2079,7 +2077,10 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
       cost = cost + cost * (int64_t)load;
     }
     w.weight[s] = wt;
-    if (w.rec) *reinterpret_cast<double*>(w.rec + s) = wt;
+    if (w.rec) {  // slot record {weight, int32 cost (-1: >= 2^31, see ecost)}
+      *reinterpret_cast<double*>(w.rec + s) = wt;
+      w.rec[s].z = cost <= INT32_MAX ? (int32_t)cost : -1;
+    }
     w.ecost[s] = cost;
     if (w.ecost32) w.ecost32[s] = (int32_t)cost;  // bound checked on the host
   }
@@ -2448,7 +2449,11 @@ int coop_tail_blocks(const DevWorld& w, int device) {
 
 __global__ void k_rec_weights(DevWorld w) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < w.g.M) *reinterpret_cast<double*>(w.rec + s) = w.weight[s];
+  if (s < w.g.M) {
+    *reinterpret_cast<double*>(w.rec + s) = w.weight[s];
+    const int64_t c = w.ecost[s];
+    w.rec[s].z = c <= INT32_MAX ? (int32_t)c : -1;
+  }
 }
 
 cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st) {
@@ -2635,28 +2640,26 @@ cudaError_t build_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t wor
 
 // Progress-filter bitmaps from a device distance table (see DevDist::fbits).
 __global__ void k_fbits(const int64_t* D, int32_t n, int32_t T, const int32_t* col, const int32_t* from, int32_t M,
-                        int64_t fbw, uint2* fb) {
+                        int64_t fbw, uint32_t* fb) {
   const size_t total = (size_t)T * fbw;
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     const size_t t = idx / fbw;
     const int64_t wd = (int64_t)(idx - t * fbw);
     const int64_t* Dr = D + t * n;
-    uint2 out = make_uint2(0u, 0u);
+    uint32_t out = 0;
     for (int b = 0; b < 32; ++b) {
       const int64_t s = wd * 32 + b;
       if (s >= M) break;
       const int32_t c = col[s];
       if (c < 0) continue;
       const int64_t dn = Dr[c];
-      if (dn == kInf) continue;
-      out.y |= 1u << b;
-      if (dn < Dr[from[s]]) out.x |= 1u << b;
+      if (dn != kInf && dn < Dr[from[s]]) out |= 1u << b;
     }
     fb[idx] = out;
   }
 }
 
-cudaError_t build_fbits(const DevWorld& w, int32_t T, uint2* fb, cudaStream_t st) {
+cudaError_t build_fbits(const DevWorld& w, int32_t T, uint32_t* fb, cudaStream_t st) {
   const size_t total = (size_t)T * w.d.fbw;
   k_fbits<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(w.d.table, w.g.n, T, w.g.col,
                                                                                       w.g.slot_from, w.g.M, w.d.fbw, fb);

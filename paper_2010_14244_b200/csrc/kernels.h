@@ -48,7 +48,7 @@ cudaError_t sssp_fill_seed(int64_t* D, size_t total, const int32_t* dests, int32
                            cudaStream_t st);
 cudaError_t sssp_run_coop(const SsspArgs& a, uint32_t* const* q, uint32_t* cnt, uint32_t count, int64_t delta,
                           int device, cudaStream_t st);
-cudaError_t build_fbits(const DevWorld& w, int32_t T, uint2* fb, cudaStream_t st);
+cudaError_t build_fbits(const DevWorld& w, int32_t T, uint32_t* fb, cudaStream_t st);
 cudaError_t build_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t words, uint64_t* out, cudaStream_t st);
 // Batched gather of device arrays into (mapped pinned) host memory.
 struct PackField {
