@@ -171,8 +171,31 @@ struct DevSignals {
   double *head_wait, *rem;
 };
 
+// Per-target candidate rows (ant-queue walker with a bounded destination set,
+// GMACO_DIST_TARGETS).  For target t and node x, x's row holds only the
+// candidate_neighbors of x toward t (routing.cpp:16-30: out-slots whose head is
+// strictly closer, kept in slot = ascending-neighbour order), one 16-B record
+// per candidate {weight f64, int32 edge cost, head row meta}, padded to pairs
+// (one LDG.256 covers a row of <= 2 candidates).  Row meta = off << 8 | c << 4 |
+// deg with off the row's pair offset inside t's table, c the candidate count,
+// deg the out-degree (counters).  Every row, including a candidate-free one,
+// owns at least one pair, so a meta identifies its node.  Records 0-1 are a
+// zero row (meta 0).  Weight and cost halves are refreshed from the shared slot
+// records at the start of each step.
+struct DevTT {
+  int4* rec;             // [nrec] records
+  const int2* sm;        // [nrec] {slot (-1 padding), head row meta}
+  const uint32_t* meta;  // [T * n] row meta of node x in target t's table
+  const int64_t* base;   // [T] first record of target t's table
+  const int64_t* cstart; // [T * (nch + 1)] first record of each kTTChunk-row chunk (+ table end)
+  int64_t nrec;
+  int32_t T, nch;
+};
+constexpr int kTTChunk = 1024;  // rows per refresh chunk
+
 struct DevWorld {
   DevGraph g;
+  DevTT tt;
   DevDist d;
   DevParams p;
   DevVehicles v;

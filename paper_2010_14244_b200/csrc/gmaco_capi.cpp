@@ -738,6 +738,51 @@ int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::v
   return a.D;
 }
 
+// Per-target candidate rows for the ant-queue walker (DevTT, device.cuh).
+// Built on the device from the progress-filter bitmaps: count record pairs
+// per (target, row), scan, then metas and records.  Skipped (bitmap walker
+// kept) when the tables would exceed their memory budget or the meta fields.
+static void build_target_rows(gmaco_engine* h, const std::vector<int32_t>& place, int32_t T) {
+  DevWorld& w = h->w;
+  DevBuffers& B = h->buf;
+  const int64_t n = w.g.n, TN = (int64_t)T * n;
+  if (TN * 16 > (int64_t(8) << 30)) return;  // build temporaries + metas
+  DevBuffers tmp;
+  tmp.stream = h->stream;
+  const int32_t* dplace = tmp.upload(place);
+  int32_t* units = tmp.alloc_direct<int32_t>(TN);
+  int64_t* offs = tmp.alloc_direct<int64_t>(TN + 1);
+  CK(tt_count(w, T, dplace, units, h->stream));
+  CK(tt_scan(units, offs, TN, h->stream));
+  std::vector<int64_t> bnd(T + 1);  // table boundaries in pairs
+  for (int32_t t = 0; t < T; ++t)
+    CK(cudaMemcpyAsync(&bnd[t], offs + (int64_t)t * n, 8, cudaMemcpyDeviceToHost, h->stream));
+  int32_t last = 0;
+  CK(cudaMemcpyAsync(&bnd[T], offs + TN - 1, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(&last, units + TN - 1, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  bnd[T] += last;
+  for (int32_t t = 0; t < T; ++t)
+    if (bnd[t + 1] - bnd[t] >= (int64_t(1) << 24)) return;  // 24-bit row offsets
+  const int64_t nrec = 2 * (bnd[T] + 1);
+  if (nrec >= (int64_t(1) << 31) || nrec * 24 > (int64_t(24) << 30)) return;
+  w.tt.meta = B.alloc_direct<uint32_t>(TN);
+  int64_t* base = B.alloc_direct<int64_t>(T);
+  w.tt.T = T;
+  w.tt.nch = (int32_t)((n + kTTChunk - 1) / kTTChunk);
+  int64_t* cstart = B.alloc_direct<int64_t>((int64_t)T * (w.tt.nch + 1));
+  CK(cudaMemcpyAsync(cstart + (int64_t)T * (w.tt.nch + 1) - 1, &nrec, 8, cudaMemcpyHostToDevice, h->stream));
+  w.tt.rec = B.alloc_direct<int4>(nrec);
+  int2* sm = B.alloc_direct<int2>(nrec);
+  CK(tt_build(w, T, dplace, offs, const_cast<uint32_t*>(w.tt.meta), base, cstart, w.tt.rec, sm, h->stream));
+  w.tt.base = base;
+  w.tt.cstart = cstart;
+  w.tt.sm = sm;
+  w.tt.nrec = nrec;
+  CK(tt_refresh(w, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
 void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distance_desc* dd,
                  const gmaco_sim_config* cfg) {
   PhaseTimer pt0;
@@ -844,11 +889,41 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
                         c.colony.ants <= 256 && maxdeg <= 16;
   const bool align4 = ell == 0 && csr_like;
   std::vector<int64_t> off4;
+  // Row placement order: rows are reached only through row descriptors, so
+  // their order in slot space is free.  Aligned-CSR rows are placed in BFS
+  // order (Cuthill-McKee without the degree sort): a walk's successive rows
+  // and the rows of nearby walks share cache lines and DRAM pages, whatever
+  // the input's node numbering (GMACO_ROW_ORDER=none keeps id order).
+  std::vector<int32_t> place(n);
+  for (int32_t u = 0; u < n; ++u) place[u] = u;
   if (align4) {
-    off4.assign(n + 1, 0);
+    const char* ro = std::getenv("GMACO_ROW_ORDER");
+    if (!(ro && std::string(ro) == "none")) {
+      std::vector<char> seen(n, 0);
+      int32_t qh = 0, qt = 0;
+      for (int32_t r = 0; r < n; ++r) {
+        if (seen[r]) continue;
+        seen[r] = 1;
+        place[qt++] = r;
+        while (qh < qt) {
+          const int32_t u = place[qh++];
+          for (int32_t k = g.out_ptr[u]; k < g.out_ptr[u + 1]; ++k) {
+            const int32_t v = g.to[g.out_edge[k]];
+            if (!seen[v]) { seen[v] = 1; place[qt++] = v; }
+          }
+        }
+      }
+    }
+    off4.assign(n + 1, 0);  // off4[u]: row start of node u
     // (a row without out-edges still takes 4 padding slots: every row start
     // is unique, so a head-row descriptor identifies its node)
-    for (int32_t u = 0; u < n; ++u) off4[u + 1] = off4[u] + std::max(4, (g.out_ptr[u + 1] - g.out_ptr[u] + 3) & ~3);
+    int64_t at = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t u = place[i];
+      off4[u] = at;
+      at += std::max(4, (g.out_ptr[u + 1] - g.out_ptr[u] + 3) & ~3);
+    }
+    off4[n] = at;
     if (off4[n] >= (int64_t(1) << 29)) throw ValidationError("graph too large for the aligned slot layout");
   }
   const int32_t M = ell ? n * ell : (align4 ? (int32_t)off4[n] : m);
@@ -960,7 +1035,14 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   p.replan_all = alg == GMACO_COLONY ? k.replan_all : 0;
   p.need_positions = (alg == GMACO_MACO || alg == GMACO_MACO_P) && !p.siblings_only;
   // debugging / A-B switches (defaults are the production configuration)
-  p.prefetch = std::getenv("GMACO_NO_PREFETCH") ? 0 : 1;
+  // Bulk L2 prefetch of stages C..G's state (prefetch_tail_state) only when
+  // that state fits comfortably in L2: a larger world would evict it again,
+  // and the prefetching CTA would hold the walk kernel's end for milliseconds.
+  {
+    const int64_t Q = (int64_t)S * kPhases;
+    const int64_t tail_bytes = (int64_t)V * 77 + Q * 32 + (int64_t)S * 40 + (int64_t)M * 48;
+    p.prefetch = !std::getenv("GMACO_NO_PREFETCH") && tail_bytes <= (int64_t(48) << 20) ? 1 : 0;
+  }
   p.pdl = std::getenv("GMACO_NO_PDL") ? 0 : 1;
   p.no_smem = std::getenv("GMACO_NO_SMEM") ? 1 : 0;
   p.max_degree = maxdeg;
@@ -1170,6 +1252,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     dv.best_key = B.filled<unsigned long long>(V, ~0ull);
     dv.walkers = B.filled<int32_t>(V, 0);
     dv.ant_hops = B.filled<int32_t>((size_t)V * p.ants, 0);
+    if (dd->kind == GMACO_DIST_TARGETS && maxdeg <= 15 && !std::getenv("GMACO_NO_TT"))
+      build_target_rows(h, place, (int32_t)targets.size());
   }
   dv.dec_rec = B.filled<int32_t>(V, -1);
   dv.plan_n = B.filled<int32_t>(V, 0);

@@ -900,6 +900,7 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
     }
     if (w.p.sharded) v.dec_rec[vid] = -1;
     v.walk_start[vid] = start;
+
     if (start >= 0) {
       v.walk_dec[vid] = deciding;
       v.best_key[vid] = ~0ull;
@@ -972,12 +973,14 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   const bool grouped = K <= 32 && (32 % K) == 0;
   const int lane = threadIdx.x & 31;
   const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
-  unsigned live = 0xffffffffu;  // warp lanes still in the loop (uniform)
+  bool drained = false;  // this lane's (group's) queue fetch came back empty
   for (;;) {
-    bool fetch = !active;
+    // full-warp votes: drained lanes stay in the loop (idle) until the whole
+    // warp is drained, so no vote needs a partial mask
+    bool fetch = !active && !drained;
     if (grouped) {
-      const unsigned idle = __ballot_sync(live, !active);
-      fetch = (idle & gmask) == gmask;
+      const unsigned idle = __ballot_sync(0xffffffffu, !active);
+      fetch = !drained && (idle & gmask) == gmask;
     }
     unsigned long long a = 0;
     if (fetch) {
@@ -990,9 +993,9 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       }
     }
     const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
-    if (grouped) live &= ~__ballot_sync(live, out);
-    if (out) break;
-    if (fetch) {
+    drained |= out;
+    if (__all_sync(0xffffffffu, drained)) break;
+    if (fetch && !out) {
       vid = v.walkers[a / K];
       ant = (int32_t)(a % K);
       const int32_t x0 = v.walk_start[vid];
@@ -1156,6 +1159,192 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ant-queue walker over per-target candidate rows (DevTT): the same queue,
+// grouped fetch and argmin as k_colony_q, but a hop loads only its
+// candidates' records (one LDG.256 for <= 2 candidates, no filter word) and
+// the roulette runs over c <= 4 registers.  Tours hold record indices
+// (k_colony_epi maps the winner's to slots).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  const DevVehicles& v = w.v;
+  const int K = w.p.ants;
+  const int64_t step = w.ctl->step;
+  const unsigned long long total = w.ctl->q_walkers * (unsigned long long)K;
+  const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit, n = w.g.n;
+  const bool vec_tour = (w.p.plan_cap & 3) == 0;
+  long long steps = 0, cands = 0, degs = 0;
+  int32_t vid = 0, ant = 0, dmeta = 0, meta = 0, hops = 0, tbase = 0;
+  int64_t cost = 0;
+  bool first_ok = false, active = false;
+  const int4* tt = w.tt.rec;
+  int32_t* tp = nullptr;
+  int4 tb = make_int4(0, 0, 0, 0);
+  uint4 rnd = make_uint4(0, 0, 0, 0);
+  const bool grouped = K <= 32 && (32 % K) == 0;
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
+  bool drained = false;
+  for (;;) {
+    // full-warp votes (drained lanes idle in the loop until the warp drains)
+    bool fetch = !active && !drained;
+    if (grouped) {
+      const unsigned idle = __ballot_sync(0xffffffffu, !active);
+      fetch = !drained && (idle & gmask) == gmask;
+    }
+    unsigned long long a = 0;
+    if (fetch) {
+      if (grouped) {  // the whole group is fetching: one atomic for K ants
+        unsigned long long b = 0;
+        if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
+        a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
+      } else {
+        a = atomicAdd(&w.ctl->q_next, 1ull);
+      }
+    }
+    const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
+    drained |= out;
+    if (__all_sync(0xffffffffu, drained)) break;
+    if (fetch && !out) {
+      vid = v.walkers[a / K];
+      ant = (int32_t)(a % K);
+      const int32_t x0 = v.walk_start[vid];
+      const int32_t dest = v.dest[vid];
+      const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+      if (tslot < 0) {  // no table: the zero row (no candidate) fails the ant at once
+        tbase = 0;
+        meta = 0;
+        dmeta = -1;
+      } else {
+        tbase = (int32_t)__ldg(w.tt.base + tslot);
+        const uint32_t* mt = w.tt.meta + (size_t)tslot * n;
+        meta = (int32_t)__ldg(mt + x0);
+        dmeta = (int32_t)__ldg(mt + dest);  // metas identify rows: a hop reaches dest iff it picks dest's
+      }
+      tt = w.tt.rec + tbase;
+      tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+      hops = 0;
+      cost = 0;
+      first_ok = false;
+      active = true;
+    }
+    if (!active) continue;  // idle lane waiting for its group (grouped form)
+    bool fin = false;
+    if (hops >= max_hops) {
+      cost = kInf;
+      fin = true;
+    } else {
+      // ---- the hop's single round trip: the candidates' records ----
+      const uint32_t off2 = ((uint32_t)meta >> 8) << 1;
+      const int c = (meta >> 4) & 15;
+      const int4* rp = tt + off2;
+      int4 rc[4];
+      ld256(rp, rc[0], rc[1]);
+      if (c > 2)
+        ld256(rp + 2, rc[2], rc[3]);
+      else
+        rc[2] = rc[3] = make_int4(0, 0, 0, 0);
+      degs += meta & 15;
+      if (c == 0) {
+        cost = kInf;
+        fin = true;
+      } else {
+        if (hops == 0) first_ok = true;
+        cands += c;
+        double u;
+        if (w.p.rng == 1) {
+          u = to_unit(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                           (uint64_t)step | ((uint64_t)(uint32_t)hops << 40)));
+        } else {
+          if ((hops & 1) == 0)
+            rnd = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)hops >> 1),
+                             w.p.rk);
+          u = to_unit(philox_half(rnd, hops));
+        }
+        // sequential left-to-right roulette (routing.cpp:100-113) over the c
+        // candidates; the kept prefixes are the cumulative pass's values
+        double total_w = 0.0, pre[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < c) total_w = __dadd_rn(total_w, __hiloint2double(rc[i].y, rc[i].x));
+          pre[i] = total_w;
+        }
+        for (int i = 4; i < c; ++i) total_w = __dadd_rn(total_w, rec_weight(rp + i));  // rare wide rows
+        int pick = c - 1;
+        if (total_w <= 0.0 || !isfinite(total_w)) {
+          pick = min((int)__dmul_rn(u, (double)c), c - 1);
+        } else {
+          const double point = __dmul_rn(u, total_w);
+          uint32_t hit = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) hit |= (i < c && point < pre[i] ? 1u : 0u) << i;
+          if (hit) {
+            pick = __ffs(hit) - 1;
+          } else {
+            double cum = pre[3];
+            for (int i = 4; i < c; ++i) {
+              cum = __dadd_rn(cum, rec_weight(rp + i));
+              if (point < cum) {
+                pick = i;
+                break;
+              }
+            }
+          }
+        }
+        int32_t ec = 0, nm = 0;
+        if (pick < 4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i == pick) {
+              ec = rc[i].z;
+              nm = rc[i].w;
+            }
+        } else {
+          const int4 r = __ldg(rp + pick);
+          ec = r.z;
+          nm = r.w;
+        }
+        const int32_t ri = tbase + (int32_t)off2 + pick;  // record index (k_colony_epi maps it to the slot)
+        // int32 edge cost; -1 marks a cost >= 2^31 (exact value in the int64 table, rare)
+        cost += ec >= 0 ? (int64_t)ec : w.ecost[w.tt.sm[ri].x];
+        // tour: 4 hops per 16-B streaming store (evict-first: read once, by the epilogue)
+        tb.x = (hops & 3) == 0 ? ri : tb.x;
+        tb.y = (hops & 3) == 1 ? ri : tb.y;
+        tb.z = (hops & 3) == 2 ? ri : tb.z;
+        tb.w = (hops & 3) == 3 ? ri : tb.w;
+        if (!vec_tour)
+          __stcs(tp + hops, ri);
+        else if ((hops & 3) == 3)
+          __stcs(reinterpret_cast<int4*>(tp + hops - 3), tb);
+        fin = nm == dmeta || (hop_limit != 0 && hops + 1 >= hop_limit);
+        meta = nm;
+        ++hops;
+        ++steps;
+      }
+    }
+    if (fin) {
+      if (vec_tour)  // flush the partial 4-hop tour buffer
+        for (int j = hops & ~3; j < hops; ++j) tp[j] = (j & 3) == 0 ? tb.x : (j & 3) == 1 ? tb.y : tb.z;
+      const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
+      v.ant_hops[(size_t)vid * K + ant] = first_ok ? hops : -1;
+      atomicMin(&v.best_key[vid], (cc << 10) | (uint64_t)ant);
+      active = false;
+    }
+  }
+  __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) {
+    steps += __shfl_xor_sync(0xffffffffu, steps, o);
+    cands += __shfl_xor_sync(0xffffffffu, cands, o);
+    degs += __shfl_xor_sync(0xffffffffu, degs, o);
+  }
+  if (lane == 0) {
+    if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
+    if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
+    if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
@@ -1190,7 +1379,11 @@ __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
         }
       }
     } else {
-      const int32_t* tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+      int32_t* tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+      if (w.tt.rec) {  // per-target walker: the tour holds record indices -> slots
+        for (int i = lane; i < hops; i += 32) tour[i] = w.tt.sm[tour[i]].x;
+        __syncwarp();
+      }
       const bool done = hops > 0 && w.g.col[tour[hops - 1]] == v.dest[vid];
       if (done && w.p.deposit == 1) {  // finish_colony's deposit, strided over the warp
         long long len = 0;
@@ -2666,10 +2859,135 @@ cudaError_t build_fbits(const DevWorld& w, int32_t T, uint32_t* fb, cudaStream_t
   return cudaGetLastError();
 }
 
+// ---- per-target candidate rows (DevTT) ------------------------------------
+// (t, p) pairs run t-major over the row placement order `place`, so a
+// target's table inherits the shared rows' locality.
+
+// closer bits of node x's row toward table row t (DevDist::fbits)
+__device__ __forceinline__ uint32_t row_closer_bits(const DevWorld& w, int64_t t, int32_t x) {
+  const int2 r = w.g.row[x];
+  const uint32_t* fb = w.d.fbits + (size_t)t * w.d.fbw;
+  const uint32_t lo = fb[r.x >> 5], hi = fb[(r.x >> 5) + 1];
+  return __funnelshift_r(lo, hi, r.x & 31) & (r.y >= 32 ? 0xffffffffu : ((1u << r.y) - 1u));
+}
+
+__global__ void k_tt_count(DevWorld w, int32_t T, const int32_t* place, int32_t* units) {
+  const int64_t n = w.g.n, total = (int64_t)T * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / n;
+    const int c = __popc(row_closer_bits(w, t, place[i - t * n]));
+    units[i] = max(1, (c + 1) >> 1);  // record pairs; a candidate-free row still owns one
+  }
+}
+
+// offs: exclusive sums of units (t-major, +1 leading zero pair); meta[t*n + x]
+__global__ void k_tt_meta(DevWorld w, int32_t T, const int32_t* place, const int64_t* offs, uint32_t* meta,
+                          int64_t* base, int64_t* cstart, int32_t nch) {
+  const int64_t n = w.g.n, total = (int64_t)T * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / n, p = i - t * n;
+    const int32_t x = place[p];
+    const int c = __popc(row_closer_bits(w, t, x));
+    const int64_t off = offs[i] - offs[t * n];
+    meta[t * n + x] = ((uint32_t)off << 8) | ((uint32_t)c << 4) | (uint32_t)w.g.deg[x];
+    const int64_t r = 2 * (offs[i] + 1);  // pair 0 is the zero row
+    if (p == 0) {
+      base[t] = r;
+      if (t > 0) cstart[(t - 1) * (nch + 1) + nch] = r;  // end of the previous table
+    }
+    if (p % kTTChunk == 0) cstart[t * (nch + 1) + p / kTTChunk] = r;
+  }
+}
+
+__global__ void k_tt_fill(DevWorld w, int32_t T, const int32_t* place, const int64_t* offs, const uint32_t* meta,
+                          int4* rec, int2* sm) {
+  const int64_t n = w.g.n, total = (int64_t)T * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / n;
+    const int32_t x = place[i - t * n];
+    uint32_t bits = row_closer_bits(w, t, x);
+    const int c = __popc(bits);
+    const int first = w.g.row[x].x;
+    const int64_t r0 = 2 * (offs[i] + 1);
+    const int pad = 2 * max(1, (c + 1) >> 1);
+    for (int j = 0; j < pad; ++j) {
+      int32_t s = -1, m = 0;
+      if (bits) {  // candidates in slot (= ascending neighbour) order
+        s = first + __ffs(bits) - 1;
+        bits &= bits - 1;
+        m = (int32_t)meta[t * n + w.g.col[s]];
+      }
+      rec[r0 + j] = make_int4(0, 0, 0, m);
+      sm[r0 + j] = make_int2(s, m);
+    }
+  }
+}
+
+// Block b refreshes chunk b / T of table b % T: the T tables' records of one
+// row chunk are rewritten by consecutive blocks, so the shared slot records
+// they gather are read from DRAM once and hit L2 for the other tables.
+__global__ void __launch_bounds__(256) k_tt_refresh(DevWorld w) {
+  const int32_t T = w.tt.T, nch = w.tt.nch;
+  const int32_t t = blockIdx.x % T, ch = blockIdx.x / T;
+  const int64_t* cs = w.tt.cstart + (int64_t)t * (nch + 1);
+  const int64_t lo = cs[ch], hi = cs[ch + 1];
+  constexpr int U = 4;  // records in flight per thread
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)U * blockDim.x) {
+    int2 q[U];
+    int4 r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = i0 + (int64_t)k * blockDim.x;
+      q[k] = i < hi ? w.tt.sm[i] : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (q[k].x >= 0) r[k] = w.rec[q[k].x];  // the shared slot record {weight, int32 cost, -}
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (q[k].x >= 0) w.tt.rec[i0 + (int64_t)k * blockDim.x] = make_int4(r[k].x, r[k].y, r[k].z, q[k].y);
+  }
+}
+
+cudaError_t tt_count(const DevWorld& w, int32_t T, const int32_t* place, int32_t* units, cudaStream_t st) {
+  k_tt_count<<<148 * 32, 256, 0, st>>>(w, T, place, units);
+  return cudaGetLastError();
+}
+
+cudaError_t tt_scan(const int32_t* units, int64_t* offs, int64_t count, cudaStream_t st) {
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, units, offs, count, st);
+  if (e != cudaSuccess) return e;
+  void* tmp = nullptr;
+  if ((e = cudaMallocAsync(&tmp, std::max<size_t>(bytes, 1), st)) != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(tmp, bytes, units, offs, count, st);
+  cudaFreeAsync(tmp, st);
+  return e;
+}
+
+cudaError_t tt_build(const DevWorld& w, int32_t T, const int32_t* place, const int64_t* offs, uint32_t* meta,
+                     int64_t* base, int64_t* cstart, int4* rec, int2* sm, cudaStream_t st) {
+  k_tt_meta<<<148 * 32, 256, 0, st>>>(w, T, place, offs, meta, base, cstart, w.tt.nch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the zero row (records 0-1)
+  if ((e = cudaMemsetAsync(rec, 0, 2 * sizeof(int4), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sm, 0xff, 2 * sizeof(int2), st)) != cudaSuccess) return e;
+  k_tt_fill<<<148 * 32, 256, 0, st>>>(w, T, place, offs, meta, rec, sm);
+  return cudaGetLastError();
+}
+
+cudaError_t tt_refresh(const DevWorld& w, cudaStream_t st) {
+  if (!w.tt.rec) return cudaSuccess;
+  k_tt_refresh<<<w.tt.T * w.tt.nch, 256, 0, st>>>(w);
+  return cudaGetLastError();
+}
+
 int queue_blocks(const DevWorld& w, int device) {
   if (!w.p.ant_queue) return 0;
   int per_sm = 0, sms = 0;
-  const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q, 128, 0);
+  const cudaError_t oe = w.tt.rec ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_qt, 128, 0)
+                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_colony_q, 128, 0);
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   return per_sm * sms;  // persistent: one full wave
@@ -2717,8 +3035,14 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
     else
       k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
   } else if (w.p.ant_queue) {
-    k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
-    k_colony_q<<<r.queue_blocks, 128, 0, st>>>(w);
+    if (w.tt.rec) {
+      k_tt_refresh<<<w.tt.T * w.tt.nch, 256, 0, st>>>(w);  // this step's weights / costs
+      k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
+      k_colony_qt<<<r.queue_blocks, 128, 0, st>>>(w);
+    } else {
+      k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
+      k_colony_q<<<r.queue_blocks, 128, 0, st>>>(w);
+    }
     k_colony_epi<<<blocks_for(VS, 8) + 1, 256, 0, st>>>(w);  // +1: prefetch CTA
   } else if (w.p.csr_walker) {
     const int vpb = 256 / w.p.ants;
@@ -2805,6 +3129,7 @@ tail:
 int kernels_per_step(const DevWorld& w, const StepResources& r) {
   int k = 1;                 // stage-B walk / decide
   if (w.p.ant_queue) k += 2; // k_colony_pro + k_colony_epi around k_colony_q
+  if (w.tt.rec) k += 1;      // k_tt_refresh
   if (w.p.sharded && !(w.p.algorithm == 4 && r.coop_blocks > 0 && !w.p.need_positions))
     k += 1;  // k_apply_remote[_move] (folded into the cooperative colony tail otherwise)
   if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
