@@ -185,6 +185,7 @@ struct DevSignals {
 struct DevTT {
   int4* rec;             // [nrec] records
   const int2* sm;        // [nrec] {slot (-1 padding), head row meta}
+  const int2* sl;        // [nrec] {slot, len_mm} for the epilogue (nullptr when a length >= 2^31)
   const uint32_t* meta;  // [T * n] row meta of node x in target t's table
   const int64_t* base;   // [T] first record of target t's table
   const int64_t* cstart; // [T * (nch + 1)] first record of each kTTChunk-row chunk (+ table end)

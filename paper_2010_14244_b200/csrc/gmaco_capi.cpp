@@ -774,7 +774,11 @@ static void build_target_rows(gmaco_engine* h, const std::vector<int32_t>& place
   CK(cudaMemcpyAsync(cstart + (int64_t)T * (w.tt.nch + 1) - 1, &nrec, 8, cudaMemcpyHostToDevice, h->stream));
   w.tt.rec = B.alloc_direct<int4>(nrec);
   int2* sm = B.alloc_direct<int2>(nrec);
-  CK(tt_build(w, T, dplace, offs, const_cast<uint32_t*>(w.tt.meta), base, cstart, w.tt.rec, sm, h->stream));
+  int64_t max_len = 0;
+  for (int64_t L : h->g.len) max_len = std::max(max_len, L);
+  int2* sl = max_len < (int64_t(1) << 31) ? B.alloc_direct<int2>(nrec) : nullptr;
+  CK(tt_build(w, T, dplace, offs, const_cast<uint32_t*>(w.tt.meta), base, cstart, w.tt.rec, sm, sl, h->stream));
+  w.tt.sl = sl;
   w.tt.base = base;
   w.tt.cstart = cstart;
   w.tt.sm = sm;

@@ -1380,14 +1380,24 @@ __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
       }
     } else {
       int32_t* tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
-      if (w.tt.rec) {  // per-target walker: the tour holds record indices -> slots
-        for (int i = lane; i < hops; i += 32) tour[i] = w.tt.sm[tour[i]].x;
+      long long len = 0;
+      if (w.tt.sl) {  // per-target walker: record indices -> {slot, length} (one gather per hop)
+        for (int i = lane; i < hops; i += 32) {
+          const int2 q = w.tt.sl[tour[i]];
+          tour[i] = q.x;
+          len += q.y;
+        }
         __syncwarp();
+      } else {
+        if (w.tt.rec) {  // per-target walker: the tour holds record indices -> slots
+          for (int i = lane; i < hops; i += 32) tour[i] = w.tt.sm[tour[i]].x;
+          __syncwarp();
+        }
+        if (w.p.deposit == 1)
+          for (int i = lane; i < hops; i += 32) len += w.g.len[tour[i]];
       }
       const bool done = hops > 0 && w.g.col[tour[hops - 1]] == v.dest[vid];
       if (done && w.p.deposit == 1) {  // finish_colony's deposit, strided over the warp
-        long long len = 0;
-        for (int i = lane; i < hops; i += 32) len += w.g.len[tour[i]];
         for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
         const double km = __ddiv_rn((double)len, 1e6);
         const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
@@ -2900,7 +2910,7 @@ __global__ void k_tt_meta(DevWorld w, int32_t T, const int32_t* place, const int
 }
 
 __global__ void k_tt_fill(DevWorld w, int32_t T, const int32_t* place, const int64_t* offs, const uint32_t* meta,
-                          int4* rec, int2* sm) {
+                          int4* rec, int2* sm, int2* sl) {
   const int64_t n = w.g.n, total = (int64_t)T * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / n;
@@ -2919,6 +2929,7 @@ __global__ void k_tt_fill(DevWorld w, int32_t T, const int32_t* place, const int
       }
       rec[r0 + j] = make_int4(0, 0, 0, m);
       sm[r0 + j] = make_int2(s, m);
+      if (sl) sl[r0 + j] = make_int2(s, s >= 0 ? (int32_t)w.g.len[s] : 0);
     }
   }
 }
@@ -2926,26 +2937,28 @@ __global__ void k_tt_fill(DevWorld w, int32_t T, const int32_t* place, const int
 // Block b refreshes chunk b / T of table b % T: the T tables' records of one
 // row chunk are rewritten by consecutive blocks, so the shared slot records
 // they gather are read from DRAM once and hit L2 for the other tables.
-__global__ void __launch_bounds__(256) k_tt_refresh(DevWorld w) {
+__global__ void __launch_bounds__(256, 4) k_tt_refresh(DevWorld w) {
   const int32_t T = w.tt.T, nch = w.tt.nch;
   const int32_t t = blockIdx.x % T, ch = blockIdx.x / T;
   const int64_t* cs = w.tt.cstart + (int64_t)t * (nch + 1);
-  const int64_t lo = cs[ch], hi = cs[ch + 1];
-  constexpr int U = 4;  // records in flight per thread
-  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)U * blockDim.x) {
+  const int64_t lo = cs[ch];
+  const int32_t cnt = (int32_t)(cs[ch + 1] - lo);
+  const int2* __restrict__ sm = w.tt.sm + lo;
+  int4* __restrict__ out = w.tt.rec + lo;
+  const int4* __restrict__ R = w.rec;
+  constexpr int U = 8;  // records in flight per thread
+  for (int32_t i0 = threadIdx.x; i0 < cnt; i0 += U * 256) {
     int2 q[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) q[k] = i0 + k * 256 < cnt ? sm[i0 + k * 256] : make_int2(-1, 0);
     int4 r[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = i0 + (int64_t)k * blockDim.x;
-      q[k] = i < hi ? w.tt.sm[i] : make_int2(-1, 0);
-    }
-#pragma unroll
     for (int k = 0; k < U; ++k)
-      if (q[k].x >= 0) r[k] = w.rec[q[k].x];  // the shared slot record {weight, int32 cost, -}
+      if (q[k].x >= 0) r[k] = __ldg(R + q[k].x);  // the shared slot record {weight, int32 cost, -}
 #pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (q[k].x >= 0) w.tt.rec[i0 + (int64_t)k * blockDim.x] = make_int4(r[k].x, r[k].y, r[k].z, q[k].y);
+    for (int k = 0; k < U; ++k)  // padding records too: whole 32-B sectors, no L2 fill reads
+      if (i0 + k * 256 < cnt)
+        out[i0 + k * 256] = q[k].x >= 0 ? make_int4(r[k].x, r[k].y, r[k].z, q[k].y) : make_int4(0, 0, 0, 0);
   }
 }
 
@@ -2966,14 +2979,15 @@ cudaError_t tt_scan(const int32_t* units, int64_t* offs, int64_t count, cudaStre
 }
 
 cudaError_t tt_build(const DevWorld& w, int32_t T, const int32_t* place, const int64_t* offs, uint32_t* meta,
-                     int64_t* base, int64_t* cstart, int4* rec, int2* sm, cudaStream_t st) {
+                     int64_t* base, int64_t* cstart, int4* rec, int2* sm, int2* sl, cudaStream_t st) {
   k_tt_meta<<<148 * 32, 256, 0, st>>>(w, T, place, offs, meta, base, cstart, w.tt.nch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // the zero row (records 0-1)
   if ((e = cudaMemsetAsync(rec, 0, 2 * sizeof(int4), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(sm, 0xff, 2 * sizeof(int2), st)) != cudaSuccess) return e;
-  k_tt_fill<<<148 * 32, 256, 0, st>>>(w, T, place, offs, meta, rec, sm);
+  if (sl && (e = cudaMemsetAsync(sl, 0xff, 2 * sizeof(int2), st)) != cudaSuccess) return e;
+  k_tt_fill<<<148 * 32, 256, 0, st>>>(w, T, place, offs, meta, rec, sm, sl);
   return cudaGetLastError();
 }
 

@@ -53,7 +53,7 @@ cudaError_t build_fbits(const DevWorld& w, int32_t T, uint32_t* fb, cudaStream_t
 cudaError_t tt_count(const DevWorld& w, int32_t T, const int32_t* place, int32_t* units, cudaStream_t st);
 cudaError_t tt_scan(const int32_t* units, int64_t* offs, int64_t count, cudaStream_t st);
 cudaError_t tt_build(const DevWorld& w, int32_t T, const int32_t* place, const int64_t* offs, uint32_t* meta,
-                     int64_t* base, int64_t* cstart, int4* rec, int2* sm, cudaStream_t st);
+                     int64_t* base, int64_t* cstart, int4* rec, int2* sm, int2* sl, cudaStream_t st);
 cudaError_t tt_refresh(const DevWorld& w, cudaStream_t st);
 cudaError_t build_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t words, uint64_t* out, cudaStream_t st);
 // Batched gather of device arrays into (mapped pinned) host memory.
