@@ -191,7 +191,7 @@ def secondary_c4(peak, peak_src, steps=10, warmup=3):
             "vehicle_routes_per_sec": (c1.vehicle_routes - c0.vehicle_routes) / (float(stepms.sum()) / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_colony_q (ant-queue walk; pro/epi kernels inside the timed walk)",
+                         "kernel": "k_colony_qt (ant-queue walk over per-target candidate rows; refresh/pro/epi kernels inside the timed walk)",
                          "algorithmic_bytes_per_launch": alg / steps,
                          "avg_launch_us": walk_s / steps * 1e6}}
 
@@ -462,7 +462,8 @@ def run_ours(args, rank, world, local):
         pass
     lattice = args.config != "c4"
     walk_kernel = ("k_colony_grid (stage-B lattice colony walk)" if lattice else
-                   "k_colony_q (stage-B ant-queue colony walk; pro/epi kernels inside the timed walk)")
+                   "k_colony_qt (stage-B ant-queue colony walk over per-target candidate rows; "
+                   "refresh/pro/epi kernels inside the timed walk)")
     note = ("latency-bound: one colony iteration is a ~15 us dependent walk over L2/SMEM-resident state "
             "(~1 MB), see DESIGN.md §7" if args.config in ("c1", "c2") else
             "throughput-bound gather walk, see DESIGN.md §7")
