@@ -323,6 +323,41 @@ def test_colony_rgg_targets_csr_walker(mode, monkeypatch):
     assert O.results_identical(gpu.run(), cpu.run())
 
 
+@pytest.mark.parametrize("variant", ["bitmap_queue", "odd_ants", "cost_over_int32", "length_over_int32"])
+def test_colony_rgg_targets_walker_variants(variant, monkeypatch):
+    """Paths around the per-target-row walker (k_colony_qt), all bit-exact:
+    bitmap_queue = the shared-row queue walker (GMACO_NO_TT); odd_ants = 12
+    ants (lanes fetch single ants, no 16-lane groups); cost_over_int32 =
+    edge costs len*(1+load) beyond 2^31 (the int32 record cost's -1 escape to
+    the int64 table); length_over_int32 = edge lengths beyond 2^31 mm (no
+    {slot, length} epilogue map)."""
+    net, dist, tgt = _rgg_targets(2500, 10, 19)
+    ants = 16
+    if variant == "bitmap_queue":
+        monkeypatch.setenv("GMACO_NO_TT", "1")
+    elif variant == "odd_ants":
+        ants = 12
+    elif variant == "cost_over_int32":
+        net.edge_length_mm = net.edge_length_mm * 20000  # ~1e9 mm: cost >= 2^31 once load >= 2
+    elif variant == "length_over_int32":
+        net.edge_length_mm = net.edge_length_mm * 60000  # some lengths >= 2^31 mm
+        assert net.edge_length_mm.max() >= 2 ** 31
+    cfg = abi.colony_production(_cfg("colony", 600, 9, max_steps=30), ants=ants)
+    cfg.colony.max_hops = 400
+    gpu = Engine(net, cfg, dist)
+    cpu = O.PortWorld(net, cfg, dist)
+    for k in (1, 2, 6):
+        gpu.step(k)
+        cpu.step(k)
+        _same_snapshot(gpu, cpu, f"rgg {variant}")
+        for vid in range(0, 600, 11):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), vid
+    a, b = gpu.counters(), cpu.counters()
+    for f in ("ant_steps", "vehicle_routes", "decisions", "candidates", "degree_sum"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
 def test_colony_rgg_max_hops_cap():
     """Hop cap shorter than many tours: capped ants fail (cost = inf), and
     vehicles whose every ant failed keep their previous plan state."""
