@@ -17,7 +17,10 @@ constexpr int kMaxDegree = 32;  // out-degree bound of the walk kernels (validat
 constexpr int kTabu = 16;       // colony tabu tenure (progress filter off only)
 constexpr int64_t kInf = INT64_MAX;
 
-enum VState : uint8_t { kPending = 0, kAtNode = 1, kOnEdge = 2, kQueued = 3, kArrived = 4, kRetired = 5 };
+enum VState : uint8_t { kPending = 0, kAtNode = 1, kOnEdge = 2, kQueued = 3, kArrived = 4, kRetired = 5,
+                        // released by this step's E1 while stage B runs (DevParams::e1_in_walk): Queued for
+                        // B, AtNode for everything after it; the tail turns it into kAtNode
+                        kReleased = 6 };
 
 struct DevGraph {
   int32_t n, m;
@@ -93,6 +96,10 @@ struct DevParams {
   int32_t ant_queue;        // csr walker in scratch mode: prologue / ant-queue walk / epilogue kernels
   int32_t pdl;              // cooperative tail launched as a programmatic dependent of the walk
   int32_t record_paths;
+  // lattice colony walks: stages C, D, E1 run in extra CTAs of the walk kernel,
+  // concurrently with B (they read only the previous step's signal state, and
+  // a vehicle E1 releases stays Queued for B: kReleased); the tail does E3, F+G
+  int32_t e1_in_walk;
 };
 
 // Control block.  The read-mostly step state shares one cache line; every
@@ -118,6 +125,7 @@ struct DevCtl {
   alignas(128) int64_t candidates;
   alignas(128) int64_t degree_sum;
   alignas(128) uint32_t blocks_done;
+  alignas(128) int32_t nrel;          // vehicles released by a concurrent E1 this step (DevVehicles::rel)
   alignas(128) unsigned long long q_walkers;  // ant queue: walking vehicles this step
   unsigned long long q_next;                  // ant queue: next (vehicle, ant) item
   alignas(128) int32_t max_occ_acc;  // atomicMax target of stage F+G
@@ -157,6 +165,7 @@ struct DevVehicles {
   int32_t* walkers;
   int32_t* ant_hops;            // [V * ants] hops, -1 when the first hop had no candidate
   int32_t* dec_rec;             // [V_pad] this step's decision per vehicle: slot, -1 none, -2 retired
+  int32_t* rel;                 // [V] vehicles released by a concurrent E1 this step (e1_in_walk)
   int64_t* plan_step;
   uint8_t* plan_done;
 };

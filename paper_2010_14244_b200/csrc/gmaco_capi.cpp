@@ -1287,6 +1287,11 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
   }
   h->res.coop_blocks = coop_tail_blocks(w, h->device);
+  // stages C, D, E1 beside the lattice walk (DevParams::e1_in_walk): needs the
+  // cooperative colony tail, which then runs E3 and the kReleased fix-up
+  p.e1_in_walk = lattice_walker && S > 0 && h->res.coop_blocks > 0 && !p.need_positions &&
+                 !std::getenv("GMACO_NO_E1_WALK");
+  if (p.e1_in_walk) dv.rel = B.alloc<int32_t>(V);
   h->res.queue_blocks = queue_blocks(w, h->device);
   CK(configure_grid_carveout(w));
   if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");
@@ -1540,6 +1545,7 @@ void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
   w.p.shard_lo = lo;
   w.p.shard_hi = hi;
   w.p.sharded = 1;
+  w.p.e1_in_walk = 0;        // the sharded tail runs C, D, E1 after the remote vehicles' bookkeeping
   w.v.walk_order = nullptr;  // a rank walks exactly its own vehicle range
   h->reset_graphs();
 }

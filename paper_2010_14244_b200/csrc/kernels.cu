@@ -28,6 +28,7 @@ namespace gmaco {
 
 namespace cg = cooperative_groups;
 constexpr int kTailCoop = 128;
+constexpr int kSigCtas = 8;  // walk-kernel CTAs running stages C, D, E1 (e1_in_walk)
 
 // ---------------------------------------------------------------------------
 // counter-based RNG (rng.hpp:21-56) and Philox4x32-10
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
     const bool deciding = st == kAtNode;
     if (deciding)
       start = v.at_node[vid];
-    else if (w.p.replan_all && st == kQueued)
+    else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
       start = v.at_node[vid];
     else if (w.p.replan_all && st == kOnEdge)
       start = w.g.col[v.on_edge[vid]];
@@ -681,7 +682,7 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
     const bool deciding = st == kAtNode;
     if (deciding)
       start = v.at_node[vid];
-    else if (w.p.replan_all && st == kQueued)
+    else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
       start = v.at_node[vid];
     else if (w.p.replan_all && st == kOnEdge)
       start = w.g.col[v.on_edge[vid]];
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
     const bool deciding = st == kAtNode;
     if (deciding)
       start = v.at_node[vid];
-    else if (w.p.replan_all && st == kQueued)
+    else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
       start = v.at_node[vid];
     else if (w.p.replan_all && st == kOnEdge)
       start = w.g.col[v.on_edge[vid]];
@@ -1463,7 +1464,7 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
     const bool deciding = st == kAtNode;
     if (deciding)
       start = v.at_node[vid];
-    else if (w.p.replan_all && st == kQueued)
+    else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
       start = v.at_node[vid];
     else if (w.p.replan_all && st == kOnEdge)
       start = w.g.col[v.on_edge[vid]];
@@ -1682,6 +1683,10 @@ enum { kTourReplay = 0, kTourScratch = 1, kTourBits = 2 };
 // multiple of 32), so its per-vehicle barrier is the literal id 1: ptxas then
 // reserves 2 named barriers instead of 16, which would otherwise cap the SM
 // at 4 resident CTAs.
+// C, D, E1 of one signal (defined with the tail stages below)
+template <bool kConcurrent = false>
+__device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s);
+
 template <bool kSmem, int kTour, bool kOneVeh = false>
 __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
@@ -1689,6 +1694,18 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
     return;
+  }
+  if (w.p.e1_in_walk) {  // the last kSigCtas blocks before it: stages C, D, E1, concurrent with B
+    const int sb = (int)blockIdx.x - ((int)gridDim.x - 1 - kSigCtas);
+    if (sb >= 0) {
+      __shared__ long long redq[32];
+      long long qt = 0;
+      for (int32_t s = sb * blockDim.x + threadIdx.x; s < w.p.S; s += kSigCtas * blockDim.x)
+        qt += sig_cde1<true>(w, s);
+      qt = block_sum(qt, redq);
+      if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+      return;
+    }
   }
   if (threadIdx.x == 0) trace_min(w.ctl, 0);
   constexpr int kMaxVpb = 256;
@@ -1747,7 +1764,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     const bool deciding = st == kAtNode;
     if (deciding)
       start = v.at_node[vid];
-    else if (w.p.replan_all && st == kQueued)
+    else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
       start = v.at_node[vid];
     else if (w.p.replan_all && st == kOnEdge)
       start = w.g.col[v.on_edge[vid]];
@@ -2035,6 +2052,7 @@ __device__ int select_phase(const DevParams& p, const int32_t* q, const double* 
 // C, D, E1 for one signal: density sample (returned), green assignment at an
 // epoch (engine.cpp:223-239, assign_green signals.cpp:111-117), FIFO
 // discharge (signals.cpp:119-135, engine.cpp:241-252).
+template <bool kConcurrent>
 __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
   const DevSignals& S = w.s;
   int32_t q[kPhases];
@@ -2075,7 +2093,12 @@ __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
       --len;
       --budget;
       w.v.queued[vid] += step - w.v.joined[vid] + 1;
-      w.v.state[vid] = kAtNode;
+      if (kConcurrent) {  // stage B may be reading this vehicle: Queued until the tail
+        w.v.state[vid] = kReleased;
+        w.v.rel[atomicAdd(&w.ctl->nrel, 1)] = vid;
+      } else {
+        w.v.state[vid] = kAtNode;
+      }
       w.v.at_node[vid] = node;
       w.v.queued_phase[vid] = -1;
     }
@@ -2140,7 +2163,8 @@ __device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long lo
     }
     if (st == kOnEdge) atomicAdd(&w.occ_new[v.on_edge[vid]], 1);
   }
-  active += st == kAtNode || st == kOnEdge || st == kQueued || (st == kPending && v.depart[vid] == step + 1);
+  active += st == kAtNode || st == kOnEdge || st == kQueued || st == kReleased ||
+            (st == kPending && v.depart[vid] == step + 1);
   unfinished += st != kArrived && st != kRetired;
 }
 
@@ -2298,6 +2322,7 @@ __device__ __forceinline__ void finalize_step(const DevWorld& w) {
   c->qsamples += w.p.S;
   c->n_t = c->n_next;
   c->n_next = 0;
+  c->nrel = 0;
   c->dcount = 0;
   const int64_t step = c->step + 1;
   c->step = step;
@@ -2462,11 +2487,19 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     }
     // colony mode: E2 already ran inside the walk kernel, so one pass per
     // signal does C, D, E1 (pops the FIFO head) and E3 (appends this step's
-    // arrivals after it) — the reference order for each queue
+    // arrivals after it) — the reference order for each queue.  With
+    // e1_in_walk, C, D, E1 ran beside the walk: E3 only, and the vehicles E1
+    // released become AtNode
     long long qt = 0;
-    for (int64_t s = gtid; s < p.S; s += gstride) {
-      qt += sig_cde1(w, (int32_t)s);
-      sig_e3(w, (int32_t)s);
+    if (p.e1_in_walk) {
+      for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
+      const int32_t nrel = w.ctl->nrel;
+      for (int64_t i = gtid; i < nrel; i += gstride) w.v.state[w.v.rel[i]] = kAtNode;
+    } else {
+      for (int64_t s = gtid; s < p.S; s += gstride) {
+        qt += sig_cde1(w, (int32_t)s);
+        sig_e3(w, (int32_t)s);
+      }
     }
     qt = block_sum(qt, red);
     if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
@@ -3025,7 +3058,8 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
     // staged tables: pack vehicles into 256-thread CTAs; otherwise one
     // vehicle's colony per CTA when it fills whole warps
     const int threads = smem ? (256 / w.p.ants) * w.p.ants : ((w.p.ants % 32 == 0) ? w.p.ants : 256);
-    const unsigned grid = blocks_for(VS, threads / w.p.ants) + 1;  // +1: prefetch CTA
+    // +1: prefetch CTA; + kSigCtas: stages C, D, E1 beside the walk (e1_in_walk)
+    const unsigned grid = blocks_for(VS, threads / w.p.ants) + 1 + (w.p.e1_in_walk ? kSigCtas : 0);
     const size_t dyn = smem + grid_bits_bytes(w, threads);  // staged tables, then move-bit words
 #define GMACO_GRID(SM, MODE) k_colony_grid<SM, MODE><<<grid, threads, dyn, st>>>(w)
     if (smem) {
