@@ -178,6 +178,10 @@ struct DevSignals {
   // per queue [S*8]
   int32_t *qlen, *qhead, *qtail, *arr_head;
   double *head_wait, *rem;
+  // e1_in_walk: queue lengths after this step's E1 [S*8] and this step's
+  // arrivals per queue [2][S*8] (step-parity double buffer), so stage F+G's
+  // congestion load qlen-after-E3 = qlen_e1 + arrivals needs no E3 result
+  int32_t *qlen_e1, *arr_cnt;
 };
 
 // Per-target candidate rows (ant-queue walker with a bounded destination set,

@@ -1291,7 +1291,11 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // cooperative colony tail, which then runs E3 and the kReleased fix-up
   p.e1_in_walk = lattice_walker && S > 0 && h->res.coop_blocks > 0 && !p.need_positions &&
                  !std::getenv("GMACO_NO_E1_WALK");
-  if (p.e1_in_walk) dv.rel = B.alloc<int32_t>(V);
+  if (p.e1_in_walk) {
+    dv.rel = B.alloc<int32_t>(V);
+    ds.qlen_e1 = B.filled<int32_t>((size_t)S * kPhases, 0);
+    ds.arr_cnt = B.filled<int32_t>((size_t)2 * S * kPhases, 0);
+  }
   h->res.queue_blocks = queue_blocks(w, h->device);
   CK(configure_grid_carveout(w));
   if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");

@@ -2107,6 +2107,15 @@ __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
     S.qlen[k] = len;
   }
   if (len == 0) S.head_wait[k] = 0.0;
+  if (kConcurrent) {  // F+G's queue loads without waiting for E3 (DevSignals::qlen_e1)
+    const int64_t Q = (int64_t)w.p.S * kPhases;
+    int32_t* nxt = S.arr_cnt + ((w.ctl->step + 1) & 1) * Q;  // next step's arrival counters
+#pragma unroll
+    for (int ph = 0; ph < kPhases; ++ph) {
+      S.qlen_e1[s * kPhases + ph] = ph == green ? len : q[ph];
+      nxt[s * kPhases + ph] = 0;
+    }
+  }
   return qt;
 }
 
@@ -2152,6 +2161,7 @@ __device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long lo
           v.joined[vid] = step + 1;
           v.progress[vid] = 0;
           v.arr_next[vid] = atomicExch(&w.s.arr_head[bind], vid);
+          if (w.p.e1_in_walk) atomicAdd(w.s.arr_cnt + (step & 1) * (int64_t)w.p.S * kPhases + bind, 1);
         } else {
           st = kAtNode;
           v.at_node[vid] = reached;
@@ -2299,7 +2309,11 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
     int64_t cost = w.g.len[s];
     if (alg == 4 && p.congestion) {
       const int32_t b = w.g.bind[s];
-      const int32_t load = occ + (b >= 0 ? w.s.qlen[b] : 0);
+      int32_t q = 0;  // the queue's length after E3
+      if (b >= 0)
+        q = w.p.e1_in_walk ? w.s.qlen_e1[b] + w.s.arr_cnt[(w.ctl->step & 1) * (int64_t)w.p.S * kPhases + b]
+                           : w.s.qlen[b];
+      const int32_t load = occ + q;
       wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
       cost = cost + cost * (int64_t)load;
     }
@@ -2492,9 +2506,29 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     // released become AtNode
     long long qt = 0;
     if (p.e1_in_walk) {
+      // E3 || F+G in one pass (F+G's queue loads come from qlen_e1 + the
+      // arrival counters), the kReleased fix-up, and the last block to finish
+      // finalizes the step: no grid-wide barrier at all
       for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
       const int32_t nrel = w.ctl->nrel;
       for (int64_t i = gtid; i < nrel; i += gstride) w.v.state[w.v.rel[i]] = kAtNode;
+      int32_t m = 0;
+      for (int64_t s = gtid; s < w.g.M; s += gstride) m = max(m, slot_fg(w, (int32_t)s));
+      m = block_max(m, smax);
+      __shared__ bool is_last;
+      if (threadIdx.x == 0) {
+        if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
+        trace_max(w.ctl, 6);
+        __threadfence();
+        is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+      }
+      __syncthreads();
+      if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        finalize_step(w);
+        __threadfence();
+      }
+      return;
     } else {
       for (int64_t s = gtid; s < p.S; s += gstride) {
         qt += sig_cde1(w, (int32_t)s);
