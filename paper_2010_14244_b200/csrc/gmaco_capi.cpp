@@ -1258,6 +1258,21 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     dv.ant_hops = B.filled<int32_t>((size_t)V * p.ants, 0);
     if (dd->kind == GMACO_DIST_TARGETS && maxdeg <= 15 && !std::getenv("GMACO_NO_TT"))
       build_target_rows(h, place, (int32_t)targets.size());
+    if (!std::getenv("GMACO_NO_ORDER")) {
+      // Walk order for the queue: destination-major (the vehicles walking at
+      // any moment share a few targets' rows, and their paths converge on
+      // them, so those rows stay in L2), then by the origin's row position.
+      // Results do not depend on the order.
+      std::vector<int32_t> posn(n), ord(V);
+      for (int32_t i = 0; i < n; ++i) posn[place[i]] = i;
+      for (int32_t i = 0; i < V; ++i) ord[i] = i;
+      auto tkey = [&](int32_t x) { return slot_of.empty() ? x : slot_of[x]; };
+      std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+        const int32_t ta = tkey(sp.dest[a]), tb = tkey(sp.dest[b]);
+        return ta != tb ? ta < tb : posn[sp.origin[a]] < posn[sp.origin[b]];
+      });
+      dv.walk_order = B.upload(ord);
+    }
   }
   dv.dec_rec = B.filled<int32_t>(V, -1);
   dv.plan_n = B.filled<int32_t>(V, 0);

@@ -880,10 +880,13 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
   __shared__ long long red5[7][32];
   const DevVehicles& v = w.v;
   const int64_t step = w.ctl->step;
-  const int32_t vid = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  // walk order (destination-major, see gmaco_capi.cpp): the walking list, and
+  // so the queue, visits vehicles bound for one target together
+  const int32_t slot = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t vid = (w.v.walk_order && slot < w.p.shard_hi) ? w.v.walk_order[slot] : slot;
   long long act = 0, unf = 0;
   bool walking = false;
-  if (vid < w.p.shard_hi) {
+  if (slot < w.p.shard_hi) {
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
       st = kAtNode;
