@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
   const unsigned long long total = w.ctl->q_walkers * (unsigned long long)K;
   const int32_t max_hops = w.p.max_hops, hop_limit = w.p.hop_limit, n = w.g.n;
   const bool vec_tour = (w.p.plan_cap & 3) == 0;
-  long long steps = 0, cands = 0, degs = 0;
+  uint32_t steps = 0, cands = 0, degs = 0;  // per-thread (widened at the flush)
   int32_t vid = 0, ant = 0, dmeta = 0, meta = 0, hops = 0, tbase = 0;
   int64_t cost = 0;
   bool first_ok = false, active = false;
@@ -1316,7 +1316,10 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
         }
         const int32_t ri = tbase + (int32_t)off2 + pick;  // record index (k_colony_epi maps it to the slot)
         // int32 edge cost; -1 marks a cost >= 2^31 (exact value in the int64 table, rare)
-        cost += ec >= 0 ? (int64_t)ec : w.ecost[w.tt.sm[ri].x];
+        if (__builtin_expect(ec < 0, 0))
+          cost += w.ecost[w.tt.sm[ri].x];
+        else
+          cost += ec;
         // tour: 4 hops per 16-B streaming store (evict-first: read once, by the epilogue)
         tb.x = (hops & 3) == 0 ? ri : tb.x;
         tb.y = (hops & 3) == 1 ? ri : tb.y;
@@ -1342,12 +1345,14 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
     }
   }
   __syncwarp();
+  unsigned long long ws = steps, wc = cands, wd = degs;
   for (int o = 16; o > 0; o >>= 1) {
-    steps += __shfl_xor_sync(0xffffffffu, steps, o);
-    cands += __shfl_xor_sync(0xffffffffu, cands, o);
-    degs += __shfl_xor_sync(0xffffffffu, degs, o);
+    ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    wc += __shfl_xor_sync(0xffffffffu, wc, o);
+    wd += __shfl_xor_sync(0xffffffffu, wd, o);
   }
   if (lane == 0) {
+    const unsigned long long steps = ws, cands = wc, degs = wd;
     if (steps) atomicAdd((unsigned long long*)&w.ctl->ant_steps, (unsigned long long)steps);
     if (cands) atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)cands);
     if (degs) atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)degs);
