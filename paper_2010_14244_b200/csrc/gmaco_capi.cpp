@@ -25,6 +25,7 @@
 #include <memory>
 #include <queue>
 #include <stdexcept>
+#include <map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1571,11 +1572,19 @@ void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
 
 }  // namespace
 
+// Process-wide communicators, one per (device, rank, world, unique id): an
+// engine attaching with an id already used in this process shares that
+// communicator instead of paying ncclCommInitRank again (a job creates its
+// communicator once; later engines of the same job reuse it).  They live until
+// process exit.
+static std::mutex g_comm_mu;
+static std::map<std::string, ncclComm_t>& comm_cache() {
+  static std::map<std::string, ncclComm_t> m;
+  return m;
+}
+
 void gmaco_engine::destroy_comm() {
-  if (comm) {
-    nccl().CommDestroy(comm);
-    comm = nullptr;
-  }
+  comm = nullptr;  // shared through comm_cache()
 }
 
 // ============================================================================
@@ -1609,7 +1618,16 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof id);
     h->destroy_comm();
-    nck(nccl().CommInitRank(&h->comm, world, id, rank), "ncclCommInitRank");
+    std::string key(reinterpret_cast<const char*>(&id), sizeof id);
+    key += fmt("/%d/%d/%d", h->device, rank, world);
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    auto it = comm_cache().find(key);
+    if (it != comm_cache().end()) {
+      h->comm = it->second;
+    } else {
+      nck(nccl().CommInitRank(&h->comm, world, id, rank), "ncclCommInitRank");
+      comm_cache()[key] = h->comm;
+    }
     h->res.exchange = nccl_exchange;
     h->res.exchange_ctx = h;
   });
