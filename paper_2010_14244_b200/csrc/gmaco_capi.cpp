@@ -1565,7 +1565,6 @@ void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
   w.p.shard_lo = lo;
   w.p.shard_hi = hi;
   w.p.sharded = 1;
-  w.p.e1_in_walk = 0;        // the sharded tail runs C, D, E1 after the remote vehicles' bookkeeping
   w.v.walk_order = nullptr;  // a rank walks exactly its own vehicle range
   h->reset_graphs();
 }
