@@ -2523,11 +2523,18 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       // E3 || F+G in one pass (F+G's queue loads come from qlen_e1 + the
       // arrival counters), the kReleased fix-up, and the last block to finish
       // finalizes the step: no grid-wide barrier at all
-      for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
+      // one index space (slots, then signals) so that no thread chains a
+      // signal's E3 after a slot's F+G when the grid covers both
+      const int64_t M = w.g.M;
+      int32_t m = 0;
+      for (int64_t i = gtid; i < M + p.S; i += gstride) {
+        if (i < M)
+          m = max(m, slot_fg(w, (int32_t)i));
+        else
+          sig_e3(w, (int32_t)(i - M));
+      }
       const int32_t nrel = w.ctl->nrel;
       for (int64_t i = gtid; i < nrel; i += gstride) w.v.state[w.v.rel[i]] = kAtNode;
-      int32_t m = 0;
-      for (int64_t s = gtid; s < w.g.M; s += gstride) m = max(m, slot_fg(w, (int32_t)s));
       m = block_max(m, smax);
       __shared__ bool is_last;
       if (threadIdx.x == 0) {
@@ -2726,7 +2733,8 @@ int coop_tail_blocks(const DevWorld& w, int device) {
                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<false>, kTailCoop, 0);
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M);
+  // (colony worlds: slots and signals share one pass, see k_tail_coop)
+  const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M + (w.p.algorithm == 4 ? w.p.S : 0));
   const int64_t want = (work + kTailCoop - 1) / kTailCoop;
   return (int)std::min<int64_t>(want, (int64_t)per_sm * sms);
 }
