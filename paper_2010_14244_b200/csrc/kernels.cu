@@ -1704,13 +1704,18 @@ template <bool kSmem, int kTour, bool kOneVeh = false>
 __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
   if (skip_step(w.ctl)) return;
-  if (blockIdx.x == gridDim.x - 1) {  // dedicated prefetch block: stages C..G's state into L2
+  // Block layout: [kSigCtas signal CTAs (e1_in_walk)][prefetch CTA][walk CTAs].
+  // The special CTAs come first so the block scheduler dispatches them at
+  // once: placed last, they started only when the final wave of walk CTAs was
+  // dispatched and held the kernel's end ~17 us past the last walk (C3).
+  const int nsig = w.p.e1_in_walk ? kSigCtas : 0;
+  if ((int)blockIdx.x == nsig) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
     return;
   }
-  if (w.p.e1_in_walk) {  // the last kSigCtas blocks before it: stages C, D, E1, concurrent with B
-    const int sb = (int)blockIdx.x - ((int)gridDim.x - 1 - kSigCtas);
-    if (sb >= 0) {
+  if (w.p.e1_in_walk) {  // stages C, D, E1, concurrent with B
+    const int sb = (int)blockIdx.x;
+    if (sb < kSigCtas) {
       __shared__ long long redq[32];
       long long qt = 0;
       for (int32_t s = sb * blockDim.x + threadIdx.x; s < w.p.S; s += kSigCtas * blockDim.x)
@@ -1733,7 +1738,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   const int vpb = blockDim.x / K;
   const int lv = threadIdx.x / K;
   const int ant = threadIdx.x - lv * K;
-  const int32_t slot = w.p.shard_lo + blockIdx.x * vpb + lv;  // walk slot; the vehicle via the balance order
+  const int32_t slot = w.p.shard_lo + ((int)blockIdx.x - nsig - 1) * vpb + lv;  // walk slot; the vehicle via the balance order
   const bool live = lv < vpb && slot < w.p.shard_hi;
   const int32_t vid = (w.v.walk_order && live) ? w.v.walk_order[slot] : slot;
   const int64_t step = w.ctl->step;
