@@ -337,7 +337,11 @@ struct DevBuffers {
       return d;
     }
     T* d = alloc<T>(h.size());
-    if (!h.empty()) CK(cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice));
+    if (!h.empty()) {  // complete before returning: a pageable cudaMemcpy may return with its DMA in
+                       // flight, unordered with later kernels on a non-blocking engine stream
+      CK(cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
     return d;
   }
   template <class T>
@@ -1586,6 +1590,14 @@ void gmaco_engine::destroy_comm() {
   comm = nullptr;  // shared through comm_cache()
 }
 
+// Host -> device copy ordered on the engine stream and complete on return
+// (the source may be a temporary; a plain pageable cudaMemcpy can return with
+// its DMA in flight and is unordered with the non-blocking engine stream).
+static void h2d(gmaco_engine* h, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
 // ============================================================================
 // C ABI
 // ============================================================================
@@ -1685,13 +1697,13 @@ int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64
           if (x >= h->g.m) throw ValidationError("exchange_import: invalid edge id");
           x = h->g.edge_slot[x];
         }
-      CK(cudaMemcpy(w.v.dec_rec, d.data(), d.size() * 4, cudaMemcpyHostToDevice));
+      h2d(h, w.v.dec_rec, d.data(), d.size() * 4);
     }
     if (deposits) {
       std::vector<int64_t> d(h->M, 0);
       for (int32_t s = 0; s < h->M; ++s)
         if (h->slot_edge[s] >= 0) d[s] = deposits[h->slot_edge[s]];
-      CK(cudaMemcpy(w.dep, d.data(), d.size() * 8, cudaMemcpyHostToDevice));
+      h2d(h, w.dep, d.data(), d.size() * 8);
     }
   });
 }
@@ -1774,8 +1786,8 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
       const double tau_d = static_cast<double>(t[s]) / 1e6;
       wt[s] = (h->w.p.alpha == 1.0 ? tau_d : std::pow(tau_d, h->w.p.alpha)) * eta[s];
     }
-    CK(cudaMemcpy(h->w.tau, t.data(), m * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->w.weight, wt.data(), m * 8, cudaMemcpyHostToDevice));
+    h2d(h, h->w.tau, t.data(), m * 8);
+    h2d(h, h->w.weight, wt.data(), m * 8);
     if (h->w.rec) {
       CK(sync_rec_weights(h->w, h->stream));
       CK(cudaStreamSynchronize(h->stream));
@@ -2180,14 +2192,14 @@ int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12) {
       CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
       t.trace_on = 1;
       for (int k = 0; k < 12; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
-      CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
+      h2d(h, h->ctl, &t, sizeof t);
       run_steps(h, 1);
     }
     DevCtl t;
     CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
     for (int k = 0; k < 12; ++k) out12[k] = t.trace[k];
     t.trace_on = 0;
-    CK(cudaMemcpy(h->ctl, &t, sizeof t, cudaMemcpyHostToDevice));
+    h2d(h, h->ctl, &t, sizeof t);
   });
 }
 
