@@ -210,7 +210,10 @@ int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist,
 
 /* Multi-GPU: shard the fleet across `world` ranks (partition_entities,
  * parallel.cpp:8-21) and exchange the per-step vectors over NCCL.  `nccl_id`
- * is the 128-byte ncclUniqueId of rank 0.  Call before the first step. */
+ * is the 128-byte ncclUniqueId of rank 0.  Call before the first step.
+ * Engines of one process attaching with the same (device, rank, world, id)
+ * share one communicator: the first attach creates it (ncclCommInitRank),
+ * later ones reuse it; communicators live until process exit. */
 int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id);
 int gmaco_nccl_unique_id(void* out128);
 
