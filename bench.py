@@ -429,8 +429,7 @@ def run_ours(args, rank, world, local):
         e.step(args.warmup)
         t2 = time.perf_counter()
         for k in range(args.steps):
-            e.step(1, count=False)
-            e.vehicles_enqueue(views[k & 1], k & 1)
+            e.step_snapshot(views[k & 1], k & 1)  # one step + its state snapshot: one graph launch
             if k:
                 e.vehicles_wait((k - 1) & 1, views[(k - 1) & 1])
         e.vehicles_wait((args.steps - 1) & 1, views[(args.steps - 1) & 1])
@@ -507,7 +506,7 @@ def run_ours(args, rank, world, local):
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h,
                 "includes": "gmaco_create from host arrays (H2D), warmup+timed steps, per-step D2H of "
-                            "vehicle states (double-buffered: gmaco_vehicles_enqueue/_wait), gmaco_collect"
+                            "vehicle states (double-buffered: gmaco_step_snapshot/gmaco_vehicles_wait), gmaco_collect"
                             + ("; the job's NCCL communicator already exists (created once per job by its first "
                                "engine, outside this timing)" if job_uid else ""),
                 "phases": e2e_phases},

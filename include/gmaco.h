@@ -260,6 +260,11 @@ int gmaco_get_signals(gmaco_engine* h, const gmaco_signal_view* view, int64_t qu
  * copies it into `view` (same field set).  A caller reads every step's result
  * while the next step already runs (gmaco_step with executed == NULL). */
 int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot);
+
+/* gmaco_step(h, 1, NULL) followed by gmaco_vehicles_enqueue(h, fields, slot),
+ * enqueued as ONE graph launch (the step and the snapshot gather captured
+ * together per slot); read the snapshot with gmaco_vehicles_wait. */
+int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot);
 int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view* view);
 int gmaco_signal_count(gmaco_engine* h, int32_t* out);
 int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out);

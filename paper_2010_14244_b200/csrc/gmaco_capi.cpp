@@ -457,6 +457,8 @@ struct gmaco_engine {
     void* buf = nullptr;
     size_t bytes = 0;
     cudaEvent_t done = nullptr;
+    cudaGraphExec_t snap_graph = nullptr;  // gmaco_step_snapshot: one step + this slot's gather
+    PackDesc snap_pd;
     std::vector<std::pair<size_t, size_t>> fields;  // (staging offset, bytes) per requested field, view order
     size_t oe_off = 0;
     bool on_edge = false, armed = false;
@@ -505,6 +507,7 @@ struct gmaco_engine {
     for (auto& s : rslot) {
       PinnedPool::give(s.buf);
       if (s.done) cudaEventDestroy(s.done);
+      if (s.snap_graph) cudaGraphExecDestroy(s.snap_graph);
     }
     buf.release();  // stream-ordered frees need the stream alive
     if (stream) cudaStreamDestroy(stream);
@@ -512,7 +515,8 @@ struct gmaco_engine {
   }
   void destroy_comm();
   void reset_graphs() {
-    for (auto* ge : {&graph_big, &graph_one, &tgraph_big, &tgraph_one, &graph_walk, &graph_tail})
+    for (auto* ge : {&graph_big, &graph_one, &tgraph_big, &tgraph_one, &graph_walk, &graph_tail, &rslot[0].snap_graph,
+                     &rslot[1].snap_graph})
       if (*ge) {
         cudaGraphExecDestroy(*ge);
         *ge = nullptr;
@@ -1900,6 +1904,76 @@ static std::vector<std::tuple<void*, const void*, size_t>> vehicle_fields(const 
   add(v->deviations, d.deviations, 4);
   add(v->path_length_mm, d.path_len_mm, 8);
   return f;
+}
+
+}  // extern "C"
+
+namespace gmaco {
+namespace {
+// Arms readback slot `slot` for `fields` (layout, pinned buffer, done event)
+// and returns the gather descriptor of the snapshot.
+PackDesc arm_slot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
+  auto& rs = h->rslot[slot];
+  const size_t V = h->w.p.V;
+  const auto f = vehicle_fields(h, fields);
+  size_t total = 0;
+  rs.fields.clear();
+  for (const auto& t : f) {
+    rs.fields.emplace_back(total, V * std::get<2>(t));
+    total += (V * std::get<2>(t) + 15) & ~size_t(15);
+  }
+  rs.on_edge = fields->on_edge != nullptr;
+  rs.oe_off = total;
+  if (rs.on_edge) total += V * 4;
+  total = std::max<size_t>(total, 16);
+  if (rs.bytes < total) {
+    PinnedPool::give(rs.buf);
+    rs.buf = PinnedPool::take(total);
+    rs.bytes = total;
+  }
+  if (!rs.done) CK(cudaEventCreateWithFlags(&rs.done, cudaEventDisableTiming));
+  char* dev = nullptr;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), rs.buf, 0));
+  PackDesc pd{};
+  for (size_t i = 0; i < f.size(); ++i) pd.f[pd.n++] = PackField{std::get<1>(f[i]), dev + rs.fields[i].first,
+                                                                 rs.fields[i].second};
+  if (rs.on_edge) pd.f[pd.n++] = PackField{h->w.v.on_edge, dev + rs.oe_off, V * 4};
+  return pd;
+}
+}  // namespace
+}  // namespace gmaco
+
+extern "C" {
+
+int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
+  if (h) h->ctl_valid = false;
+  if (!h || !fields || slot < 0 || slot > 1) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const PackDesc pd = arm_slot(h, fields, slot);
+    auto& rs = h->rslot[slot];
+    // one graph per slot: a step then the snapshot gather, re-captured when the
+    // gather descriptor (field set, buffer) changes
+    if (!rs.snap_graph || std::memcmp(&rs.snap_pd, &pd, sizeof pd) != 0) {
+      if (rs.snap_graph) CK(cudaGraphExecDestroy(rs.snap_graph));
+      StepResources r = h->res;
+      r.capturing = true;
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      cudaError_t err = launch_step(h->w, r, h->stream, nullptr, nullptr);
+      if (err == cudaSuccess) err = launch_pack(pd, h->stream);
+      const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+      CK(err);
+      CK(e2);
+      CK(cudaGraphInstantiate(&rs.snap_graph, graph, 0));
+      cudaGraphDestroy(graph);
+      rs.snap_pd = pd;
+    }
+    unbound_stop(h);
+    CK(cudaGraphLaunch(rs.snap_graph, h->stream));
+    CK(cudaEventRecord(rs.done, h->stream));
+    rs.armed = true;
+    h->pending = true;
+  }, /*stream_ordered=*/true);
 }
 
 int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {

@@ -60,6 +60,7 @@ SIGNATURES = {
     "gmaco_network_write_file": (C.c_int, P(abi.GraphDesc), P(f64), P(f64), P(u8), C.c_char_p),
     "gmaco_network_last_error": (C.c_char_p,),
     "gmaco_vehicles_enqueue": (C.c_int, C.c_void_p, P(abi.VehicleView), i32),
+    "gmaco_step_snapshot": (C.c_int, C.c_void_p, P(abi.VehicleView), i32),
     "gmaco_vehicles_wait": (C.c_int, C.c_void_p, i32, P(abi.VehicleView)),
     "gmaco_last_error": (C.c_char_p, C.c_void_p),
     "gmaco_destroy": (None, C.c_void_p),
@@ -158,6 +159,10 @@ class Engine:
     def vehicles_enqueue(self, view, slot: int) -> None:
         """Snapshot the view's fields after all enqueued steps into slot 0/1 (no wait)."""
         self._check(self.L.gmaco_vehicles_enqueue(self.h, C.byref(view), slot))
+
+    def step_snapshot(self, view, slot: int) -> None:
+        """One step, then the view's fields snapshotted into slot 0/1: one graph launch, no wait."""
+        self._check(self.L.gmaco_step_snapshot(self.h, C.byref(view), slot))
 
     def vehicles_wait(self, slot: int, view) -> None:
         """Wait for slot's snapshot and copy it into view."""

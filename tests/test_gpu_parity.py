@@ -470,9 +470,11 @@ def test_colony_wide_rows(hub_degree, mode, monkeypatch):
     assert O.results_identical(gpu.run(), cpu.run())
 
 
-def test_double_buffered_readback_every_step():
-    """gmaco_vehicles_enqueue / _wait: each step's snapshot (taken while the
-    next step is already enqueued) equals the oracle's state at that step."""
+@pytest.mark.parametrize("fused", [False, True])
+def test_double_buffered_readback_every_step(fused):
+    """gmaco_vehicles_enqueue / _wait (or gmaco_step_snapshot / _wait): each
+    step's snapshot (taken while the next step is already enqueued) equals the
+    oracle's state at that step."""
     import ctypes as C
     net = networks.grid(10, 10, signals="all")
     cfg = abi.colony_production(_cfg("colony", 150, 4, max_steps=30), ants=32)
@@ -485,8 +487,11 @@ def test_double_buffered_readback_every_step():
                              progress_mm=abi.ptr(b["progress_mm"], C.c_int64),
                              decisions=abi.ptr(b["decisions"], C.c_int32)) for b in bufs]
     for k in range(14):
-        gpu.step(1, count=False)
-        gpu.vehicles_enqueue(views[k % 2], k % 2)
+        if fused:  # gmaco_step_snapshot: step + gather in one graph launch
+            gpu.step_snapshot(views[k % 2], k % 2)
+        else:
+            gpu.step(1, count=False)
+            gpu.vehicles_enqueue(views[k % 2], k % 2)
         if k:
             gpu.vehicles_wait((k - 1) % 2, views[(k - 1) % 2])
             cpu.step(1)
