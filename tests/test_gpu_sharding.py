@@ -140,3 +140,26 @@ def test_host_mediated_shards_every_walker(kind, monkeypatch):
             assert same(e, single) is None, (kind, k, same(e, single))
     assert sum(e.counters().ant_steps for e in shards) == single.counters().ant_steps
     del keep
+
+
+def test_nccl_communicator_shared_by_engines_of_a_job():
+    """Engines attaching with the same (rank, world, id) share one
+    communicator (the first attach creates it; a unique id is single-use for
+    ncclCommInitRank), and each still equals the unsharded engine — also after
+    the first engine is closed."""
+    from paper_2010_14244_b200 import engine
+    import ctypes as C
+    net, cfg = world(V=300, ants=32, rows=16)
+    uid = C.create_string_buffer(128)
+    assert engine.load().gmaco_nccl_unique_id(uid) == 0
+    single = Engine(net, cfg, net.grid_distance())
+    single.step(5)
+    first = Engine(net, cfg, net.grid_distance())
+    first.attach_comm(0, 1, uid.raw)
+    first.step(5)
+    assert same(first, single) is None
+    first.close()
+    second = Engine(net, cfg, net.grid_distance())
+    second.attach_comm(0, 1, uid.raw)  # reuses the job's communicator
+    second.step(5)
+    assert same(second, single) is None
