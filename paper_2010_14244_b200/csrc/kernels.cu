@@ -1195,9 +1195,13 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
   const int lane = threadIdx.x & 31;
   const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
   bool drained = false;
+  bool any_idle = true;  // warp-uniform: some lane finished its ant (a group may refetch)
   for (;;) {
-    // full-warp votes (drained lanes idle in the loop until the warp drains)
-    bool fetch = !active && !drained;
+    // full-warp votes (drained lanes idle in the loop until the warp drains);
+    // the fetch votes run only after a lane of the warp went idle
+    bool fetch = false;
+    if (any_idle) {
+    fetch = !active && !drained;
     if (grouped) {
       const unsigned idle = __ballot_sync(0xffffffffu, !active);
       fetch = !drained && (idle & gmask) == gmask;
@@ -1238,6 +1242,8 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
       first_ok = false;
       active = true;
     }
+    }
+    any_idle = __any_sync(0xffffffffu, !active);
     if (!active) continue;  // idle lane waiting for its group (grouped form)
     bool fin = false;
     if (hops >= max_hops) {
