@@ -1186,7 +1186,7 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
   uint32_t steps = 0, cands = 0, degs = 0;  // per-thread (widened at the flush)
   int32_t vid = 0, ant = 0, dmeta = 0, meta = 0, hops = 0, tbase = 0;
   int64_t cost = 0;
-  bool first_ok = false, active = false;
+  bool active = false;
   const int4* tt = w.tt.rec;
   int32_t* tp = nullptr;
   int4 tb = make_int4(0, 0, 0, 0);
@@ -1239,7 +1239,6 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
       tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
       hops = 0;
       cost = 0;
-      first_ok = false;
       active = true;
     }
     }
@@ -1265,7 +1264,6 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
         cost = kInf;
         fin = true;
       } else {
-        if (hops == 0) first_ok = true;
         cands += c;
         double u;
         if (w.p.rng == 1) {
@@ -1345,7 +1343,8 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
       if (vec_tour)  // flush the partial 4-hop tour buffer
         for (int j = hops & ~3; j < hops; ++j) tp[j] = (j & 3) == 0 ? tb.x : (j & 3) == 1 ? tb.y : tb.z;
       const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
-      v.ant_hops[(size_t)vid * K + ant] = first_ok ? hops : -1;
+      // (the first hop had candidates iff any hop was made: max_hops >= 1)
+      v.ant_hops[(size_t)vid * K + ant] = hops > 0 ? hops : -1;
       atomicMin(&v.best_key[vid], (cc << 10) | (uint64_t)ant);
       active = false;
     }
