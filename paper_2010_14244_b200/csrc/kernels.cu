@@ -983,10 +983,14 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   const int lane = threadIdx.x & 31;
   const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
   bool drained = false;  // this lane's (group's) queue fetch came back empty
+  bool any_idle = true;  // warp-uniform: some lane finished its ant (a group may refetch)
   for (;;) {
     // full-warp votes: drained lanes stay in the loop (idle) until the whole
-    // warp is drained, so no vote needs a partial mask
-    bool fetch = !active && !drained;
+    // warp is drained, so no vote needs a partial mask; the fetch votes run
+    // only after a lane of the warp went idle
+    bool fetch = false;
+    if (any_idle) {
+    fetch = !active && !drained;
     if (grouped) {
       const unsigned idle = __ballot_sync(0xffffffffu, !active);
       fetch = !drained && (idle & gmask) == gmask;
@@ -1024,6 +1028,8 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
       first_ok = false;
       active = true;
     }
+    }
+    any_idle = __any_sync(0xffffffffu, !active);
     if (!active) continue;  // idle lane waiting for its group (grouped form)
     bool fin = false;
     if (hops >= max_hops) {
