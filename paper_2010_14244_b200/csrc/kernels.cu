@@ -1407,7 +1407,17 @@ __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
       int32_t* tour = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
       long long len = 0;
       if (w.tt.sl) {  // per-target walker: record indices -> {slot, length} (one gather per hop)
-        for (int i = lane; i < hops; i += 32) {
+        int i = lane;
+        for (; i + 96 < hops; i += 128) {  // four gathers in flight per lane
+          const int32_t r0 = tour[i], r1 = tour[i + 32], r2 = tour[i + 64], r3 = tour[i + 96];
+          const int2 q0 = w.tt.sl[r0], q1 = w.tt.sl[r1], q2 = w.tt.sl[r2], q3 = w.tt.sl[r3];
+          tour[i] = q0.x;
+          tour[i + 32] = q1.x;
+          tour[i + 64] = q2.x;
+          tour[i + 96] = q3.x;
+          len += (long long)q0.y + q1.y + q2.y + q3.y;
+        }
+        for (; i < hops; i += 32) {
           const int2 q = w.tt.sl[tour[i]];
           tour[i] = q.x;
           len += q.y;
