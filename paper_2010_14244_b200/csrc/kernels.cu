@@ -1436,8 +1436,15 @@ __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
         for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
         const double km = __ddiv_rn((double)len, 1e6);
         const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
-        for (int i = lane; i < hops; i += 32)
-          atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
+        int i = lane;
+        for (; i + 96 < hops; i += 128) {  // four slot loads in flight before the fire-and-forget adds
+          const int32_t s0 = tour[i], s1 = tour[i + 32], s2 = tour[i + 64], s3 = tour[i + 96];
+          atomicAdd((unsigned long long*)&w.dep[s0], (unsigned long long)amount);
+          atomicAdd((unsigned long long*)&w.dep[s1], (unsigned long long)amount);
+          atomicAdd((unsigned long long*)&w.dep[s2], (unsigned long long)amount);
+          atomicAdd((unsigned long long*)&w.dep[s3], (unsigned long long)amount);
+        }
+        for (; i < hops; i += 32) atomicAdd((unsigned long long*)&w.dep[tour[i]], (unsigned long long)amount);
       }
       if (lane == 0) {
         v.plan_ant[vid] = ant;
