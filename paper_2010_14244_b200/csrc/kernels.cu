@@ -1202,11 +1202,16 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
   const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
   bool drained = false;
   bool any_idle = true;  // warp-uniform: some lane finished its ant (a group may refetch)
+  uint32_t trip = 0;     // warp-uniform loop trip count
   for (;;) {
     // full-warp votes (drained lanes idle in the loop until the warp drains);
-    // the fetch votes run only after a lane of the warp went idle
+    // the fetch votes run only after a lane of the warp went idle, and only on
+    // even trips: every ant then takes hop h on a trip of h's parity, so the
+    // Philox block (one per hop pair) is computed by the whole warp together,
+    // every other trip, instead of whenever either of its groups needs one
     bool fetch = false;
-    if (any_idle) {
+    const bool even_trip = (trip++ & 1u) == 0;
+    if (any_idle && even_trip) {
     fetch = !active && !drained;
     if (grouped) {
       const unsigned idle = __ballot_sync(0xffffffffu, !active);
