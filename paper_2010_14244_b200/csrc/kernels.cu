@@ -984,12 +984,15 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
   const unsigned gmask = grouped ? (K == 32 ? 0xffffffffu : ((1u << K) - 1u) << (lane / K * K)) : (1u << lane);
   bool drained = false;  // this lane's (group's) queue fetch came back empty
   bool any_idle = true;  // warp-uniform: some lane finished its ant (a group may refetch)
+  uint32_t trip = 0;     // warp-uniform loop trip count
   for (;;) {
     // full-warp votes: drained lanes stay in the loop (idle) until the whole
     // warp is drained, so no vote needs a partial mask; the fetch votes run
-    // only after a lane of the warp went idle
+    // only after a lane of the warp went idle, and only on even trips (the
+    // warp's ants share hop parity: one Philox block per pair for all)
     bool fetch = false;
-    if (any_idle) {
+    const bool even_trip = (trip++ & 1u) == 0;
+    if (any_idle && even_trip) {
     fetch = !active && !drained;
     if (grouped) {
       const unsigned idle = __ballot_sync(0xffffffffu, !active);
