@@ -1259,10 +1259,7 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
     any_idle = __any_sync(0xffffffffu, !active);
     if (!active) continue;  // idle lane waiting for its group (grouped form)
     bool fin = false;
-    if (hops >= max_hops) {
-      cost = kInf;
-      fin = true;
-    } else {
+    {  // (max_hops >= 1: an ant is failed on the hop that reaches max_hops, below)
       // ---- the hop's single round trip: the candidates' records ----
       const uint32_t off2 = ((uint32_t)meta >> 8) << 1;
       const int c = (meta >> 4) & 15;
@@ -1348,6 +1345,10 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
         else if ((hops & 3) == 3)
           __stcs(reinterpret_cast<int4*>(tp + hops - 3), tb);
         fin = nm == dmeta || (hop_limit != 0 && hops + 1 >= hop_limit);
+        if (!fin && hops + 1 >= max_hops) {  // tour cap reached short of dest: the ant fails
+          cost = kInf;
+          fin = true;
+        }
         meta = nm;
         ++hops;
         ++steps;
