@@ -993,44 +993,44 @@ __global__ void __launch_bounds__(128, 6) k_colony_q(DevWorld w) {
     bool fetch = false;
     const bool even_trip = (trip++ & 1u) == 0;
     if (any_idle && even_trip) {
-    fetch = !active && !drained;
-    if (grouped) {
-      const unsigned idle = __ballot_sync(0xffffffffu, !active);
-      fetch = !drained && (idle & gmask) == gmask;
-    }
-    unsigned long long a = 0;
-    if (fetch) {
-      if (grouped) {  // the whole group is fetching: one atomic for K ants
-        unsigned long long b = 0;
-        if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
-        a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
-      } else {
-        a = atomicAdd(&w.ctl->q_next, 1ull);
+      fetch = !active && !drained;
+      if (grouped) {
+        const unsigned idle = __ballot_sync(0xffffffffu, !active);
+        fetch = !drained && (idle & gmask) == gmask;
       }
-    }
-    const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
-    drained |= out;
-    if (__all_sync(0xffffffffu, drained)) break;
-    if (fetch && !out) {
-      vid = v.walkers[a / K];
-      ant = (int32_t)(a % K);
-      const int32_t x0 = v.walk_start[vid];
-      const int32_t dest = v.dest[vid];
-      const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
-      fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
-      const int2 r0 = __ldg(w.g.row + x0);
-      first = r0.x;
-      span = r0.y;
-      deg = __ldg(w.g.deg + x0);
-      // the destination's row descriptor: rows have unique starts, so a hop
-      // reaches dest iff the picked record's descriptor equals it
-      dmeta = (int32_t)(((uint32_t)__ldg(&w.g.row[dest].x) >> 2) << 5) | __ldg(w.g.deg + dest);
-      tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
-      hops = 0;
-      cost = 0;
-      first_ok = false;
-      active = true;
-    }
+      unsigned long long a = 0;
+      if (fetch) {
+        if (grouped) {  // the whole group is fetching: one atomic for K ants
+          unsigned long long b = 0;
+          if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
+          a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
+        } else {
+          a = atomicAdd(&w.ctl->q_next, 1ull);
+        }
+      }
+      const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
+      drained |= out;
+      if (__all_sync(0xffffffffu, drained)) break;
+      if (fetch && !out) {
+        vid = v.walkers[a / K];
+        ant = (int32_t)(a % K);
+        const int32_t x0 = v.walk_start[vid];
+        const int32_t dest = v.dest[vid];
+        const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+        fb = tslot < 0 ? nullptr : w.d.fbits + (size_t)tslot * w.d.fbw;
+        const int2 r0 = __ldg(w.g.row + x0);
+        first = r0.x;
+        span = r0.y;
+        deg = __ldg(w.g.deg + x0);
+        // the destination's row descriptor: rows have unique starts, so a hop
+        // reaches dest iff the picked record's descriptor equals it
+        dmeta = (int32_t)(((uint32_t)__ldg(&w.g.row[dest].x) >> 2) << 5) | __ldg(w.g.deg + dest);
+        tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+        hops = 0;
+        cost = 0;
+        first_ok = false;
+        active = true;
+      }
     }
     any_idle = __any_sync(0xffffffffu, !active);
     if (!active) continue;  // idle lane waiting for its group (grouped form)
@@ -1215,46 +1215,46 @@ __global__ void __launch_bounds__(128, 8) k_colony_qt(DevWorld w) {
     bool fetch = false;
     const bool even_trip = (trip++ & 1u) == 0;
     if (any_idle && even_trip) {
-    fetch = !active && !drained;
-    if (grouped) {
-      const unsigned idle = __ballot_sync(0xffffffffu, !active);
-      fetch = !drained && (idle & gmask) == gmask;
-    }
-    unsigned long long a = 0;
-    if (fetch) {
-      if (grouped) {  // the whole group is fetching: one atomic for K ants
-        unsigned long long b = 0;
-        if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
-        a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
-      } else {
-        a = atomicAdd(&w.ctl->q_next, 1ull);
+      fetch = !active && !drained;
+      if (grouped) {
+        const unsigned idle = __ballot_sync(0xffffffffu, !active);
+        fetch = !drained && (idle & gmask) == gmask;
       }
-    }
-    const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
-    drained |= out;
-    if (__all_sync(0xffffffffu, drained)) break;
-    if (fetch && !out) {
-      vid = v.walkers[a / K];
-      ant = (int32_t)(a % K);
-      const int32_t x0 = v.walk_start[vid];
-      const int32_t dest = v.dest[vid];
-      const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
-      if (tslot < 0) {  // no table: the zero row (no candidate) fails the ant at once
-        tbase = 0;
-        meta = 0;
-        dmeta = -1;
-      } else {
-        tbase = (int32_t)__ldg(w.tt.base + tslot);
-        const uint32_t* mt = w.tt.meta + (size_t)tslot * n;
-        meta = (int32_t)__ldg(mt + x0);
-        dmeta = (int32_t)__ldg(mt + dest);  // metas identify rows: a hop reaches dest iff it picks dest's
+      unsigned long long a = 0;
+      if (fetch) {
+        if (grouped) {  // the whole group is fetching: one atomic for K ants
+          unsigned long long b = 0;
+          if (lane == __ffs(gmask) - 1) b = atomicAdd(&w.ctl->q_next, (unsigned long long)K);
+          a = __shfl_sync(gmask, b, __ffs(gmask) - 1) + (unsigned long long)(lane - (__ffs(gmask) - 1));
+        } else {
+          a = atomicAdd(&w.ctl->q_next, 1ull);
+        }
       }
-      tt = w.tt.rec + tbase;
-      tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
-      hops = 0;
-      cost = 0;
-      active = true;
-    }
+      const bool out = fetch && a >= total;  // group-uniform (total is a multiple of K)
+      drained |= out;
+      if (__all_sync(0xffffffffu, drained)) break;
+      if (fetch && !out) {
+        vid = v.walkers[a / K];
+        ant = (int32_t)(a % K);
+        const int32_t x0 = v.walk_start[vid];
+        const int32_t dest = v.dest[vid];
+        const int32_t tslot = w.d.slot_of ? w.d.slot_of[dest] : dest;
+        if (tslot < 0) {  // no table: the zero row (no candidate) fails the ant at once
+          tbase = 0;
+          meta = 0;
+          dmeta = -1;
+        } else {
+          tbase = (int32_t)__ldg(w.tt.base + tslot);
+          const uint32_t* mt = w.tt.meta + (size_t)tslot * n;
+          meta = (int32_t)__ldg(mt + x0);
+          dmeta = (int32_t)__ldg(mt + dest);  // metas identify rows: a hop reaches dest iff it picks dest's
+        }
+        tt = w.tt.rec + tbase;
+        tp = v.scratch + ((size_t)vid * K + ant) * (size_t)w.p.plan_cap;
+        hops = 0;
+        cost = 0;
+        active = true;
+      }
     }
     any_idle = __any_sync(0xffffffffu, !active);
     if (!active) continue;  // idle lane waiting for its group (grouped form)
