@@ -2244,6 +2244,7 @@ __device__ __forceinline__ void sig_e3(const DevWorld& w, int32_t s) {
   // one round of independent loads for all 8 queues, then the (rare)
   // arrival chains, then one round of head lookups for head_wait
   int32_t chain[kPhases], len[kPhases], head[kPhases];
+  const int64_t e = S.el_steps[s] + 1;  // loaded with the queue words, ahead of the stores
 #pragma unroll
   for (int ph = 0; ph < kPhases; ++ph) {
     chain[ph] = S.arr_head[k0 + ph];
@@ -2284,7 +2285,6 @@ __device__ __forceinline__ void sig_e3(const DevWorld& w, int32_t s) {
 #pragma unroll
   for (int ph = 0; ph < kPhases; ++ph)
     S.head_wait[k0 + ph] = len[ph] == 0 ? 0.0 : __dmul_rn((double)(now - joined[ph]), w.p.dt_s);
-  const int64_t e = S.el_steps[s] + 1;
   S.el_steps[s] = e;
   S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
 }
@@ -2319,8 +2319,21 @@ __device__ __forceinline__ void node_scoped(const DevWorld& w, int32_t u) {
 // (routing.cpp:90-94).  Returns the slot's occupancy (for the running max).
 __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
   const DevParams& p = w.p;
-  int64_t t = w.tau[s];
   const int alg = p.algorithm;
+  const bool aco = alg == 1 || alg == 4;
+  // every load that does not depend on another is issued here, ahead of the
+  // stores below (the compiler may not move a load past a possibly aliasing
+  // store): the slot's chain is two memory round trips instead of four
+  int64_t t = w.tau[s];
+  const int32_t occ = w.occ_new[s];
+  const int64_t d = aco ? w.dep[s] : 0;
+  const double eta = aco ? w.g.eta_beta[s] : 0.0;
+  const int64_t len = aco ? w.g.len[s] : 0;
+  const int32_t b = (alg == 4 && p.congestion) ? w.g.bind[s] : -1;
+  const int64_t par = (b >= 0 && p.e1_in_walk) ? (w.ctl->step & 1) : 0;
+  int32_t q = 0;  // the queue's length after E3
+  if (b >= 0)
+    q = p.e1_in_walk ? w.s.qlen_e1[b] + w.s.arr_cnt[par * (int64_t)p.S * kPhases + b] : w.s.qlen[b];
   if ((alg == 2 || alg == 3) && !p.siblings_only) {
     const int64_t D = w.ctl->dcount;
     const int32_t chain = w.dec_head[s];
@@ -2343,8 +2356,7 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
     }
     const int64_t gap = D - done;
     if (gap > 0) t = max(p.tau_lo, t - gap * p.dec);
-  } else if (alg == 1 || alg == 4) {
-    const int64_t d = w.dep[s];
+  } else if (aco) {
     if (d) {
       t = min(p.tau_hi, t + d);
       w.dep[s] = 0;
@@ -2352,22 +2364,16 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
   }
   const int64_t scaled = (int64_t)floor(__dmul_rn(p.one_minus_rho, (double)t));
   t = max(p.tau_lo, scaled);
-  const int32_t occ = w.occ_new[s];
   if (alg == 4 && p.cong_evap && occ > 0) t = max(p.tau_lo, t - p.dec * (int64_t)occ);
   w.tau[s] = t;
   w.occ_cur[s] = occ;
   w.occ_new[s] = 0;
-  if (alg == 1 || alg == 4) {
+  if (aco) {
     const double tau_d = __ddiv_rn((double)t, 1e6);
     const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : pow(tau_d, p.alpha));
-    double wt = __dmul_rn(ta, w.g.eta_beta[s]);
-    int64_t cost = w.g.len[s];
+    double wt = __dmul_rn(ta, eta);
+    int64_t cost = len;
     if (alg == 4 && p.congestion) {
-      const int32_t b = w.g.bind[s];
-      int32_t q = 0;  // the queue's length after E3
-      if (b >= 0)
-        q = w.p.e1_in_walk ? w.s.qlen_e1[b] + w.s.arr_cnt[(w.ctl->step & 1) * (int64_t)w.p.S * kPhases + b]
-                           : w.s.qlen[b];
       const int32_t load = occ + q;
       wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
       cost = cost + cost * (int64_t)load;
