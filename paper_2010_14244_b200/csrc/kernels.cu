@@ -570,21 +570,29 @@ __global__ void __launch_bounds__(1024) k_colony(DevWorld w) {
 
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
+    // the vehicle's words in one round of loads, ahead of any store (the
+    // prologue runs beside the table staging and must not outlast it)
     uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    const int64_t depart = v.depart[vid];
+    int32_t at = v.at_node[vid];
+    const int32_t origin = v.origin[vid];
+    const int32_t on_edge = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
+      at = origin;
       v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
+      v.at_node[vid] = origin;
     }
     int32_t start = -1;
     const bool deciding = st == kAtNode;
     if (deciding)
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && st == kOnEdge)
-      start = w.g.col[v.on_edge[vid]];
-    if (start >= 0 && start == v.dest[vid]) {
+      start = w.g.col[on_edge];
+    if (start >= 0 && start == dest) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
@@ -677,21 +685,29 @@ __global__ void __launch_bounds__(256) k_colony_ell4(DevWorld w) {
 
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
+    // the vehicle's words in one round of loads, ahead of any store (the
+    // prologue runs beside the table staging and must not outlast it)
     uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    const int64_t depart = v.depart[vid];
+    int32_t at = v.at_node[vid];
+    const int32_t origin = v.origin[vid];
+    const int32_t on_edge = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
+      at = origin;
       v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
+      v.at_node[vid] = origin;
     }
     int32_t start = -1;
     const bool deciding = st == kAtNode;
     if (deciding)
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && st == kOnEdge)
-      start = w.g.col[v.on_edge[vid]];
-    if (start >= 0 && start == v.dest[vid]) {
+      start = w.g.col[on_edge];
+    if (start >= 0 && start == dest) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
@@ -887,21 +903,29 @@ __global__ void __launch_bounds__(256) k_colony_pro(DevWorld w) {
   long long act = 0, unf = 0;
   bool walking = false;
   if (slot < w.p.shard_hi) {
+    // the vehicle's words in one round of loads, ahead of any store (the
+    // prologue runs beside the table staging and must not outlast it)
     uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    const int64_t depart = v.depart[vid];
+    int32_t at = v.at_node[vid];
+    const int32_t origin = v.origin[vid];
+    const int32_t on_edge = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
+      at = origin;
       v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
+      v.at_node[vid] = origin;
     }
     int32_t start = -1;
     const bool deciding = st == kAtNode;
     if (deciding)
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && st == kOnEdge)
-      start = w.g.col[v.on_edge[vid]];
-    if (start >= 0 && start == v.dest[vid]) {
+      start = w.g.col[on_edge];
+    if (start >= 0 && start == dest) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
@@ -1504,21 +1528,29 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
   const DevVehicles& v = w.v;
   long long act = 0, unf = 0;
   if (live && ant == 0) {
+    // the vehicle's words in one round of loads, ahead of any store (the
+    // prologue runs beside the table staging and must not outlast it)
     uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    const int64_t depart = v.depart[vid];
+    int32_t at = v.at_node[vid];
+    const int32_t origin = v.origin[vid];
+    const int32_t on_edge = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
+      at = origin;
       v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
+      v.at_node[vid] = origin;
     }
     int32_t start = -1;
     const bool deciding = st == kAtNode;
     if (deciding)
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && st == kOnEdge)
-      start = w.g.col[v.on_edge[vid]];
-    if (start >= 0 && start == v.dest[vid]) {
+      start = w.g.col[on_edge];
+    if (start >= 0 && start == dest) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
@@ -1809,21 +1841,29 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       reinterpret_cast<unsigned long long*>(dyn_smem + (kSmem ? grid_staged_bytes_dev(w) : 0));
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
   if (live && ant == 0) {
+    // the vehicle's words in one round of loads, ahead of any store (the
+    // prologue runs beside the table staging and must not outlast it)
     uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    const int64_t depart = v.depart[vid];
+    int32_t at = v.at_node[vid];
+    const int32_t origin = v.origin[vid];
+    const int32_t on_edge = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
+      at = origin;
       v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
+      v.at_node[vid] = origin;
     }
     int32_t start = -1;
     const bool deciding = st == kAtNode;
     if (deciding)
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && (st == kQueued || st == kReleased))  // kReleased: queued at stage B
-      start = v.at_node[vid];
+      start = at;
     else if (w.p.replan_all && st == kOnEdge)
-      start = w.g.col[v.on_edge[vid]];
-    if (start >= 0 && start == v.dest[vid]) {
+      start = w.g.col[on_edge];
+    if (start >= 0 && start == dest) {
       v.plan_n[vid] = 0;
       v.plan_step[vid] = step;
       v.plan_done[vid] = 0;
@@ -2181,22 +2221,27 @@ __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
 __device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished) {
   const DevVehicles& v = w.v;
   const int64_t step = w.ctl->step;
+  // the vehicle's words, then its edge's, each in one round of loads ahead
+  // of any store (the compiler may not move a load past an aliasing store)
   uint8_t st = v.state[vid];
+  const int64_t depart = v.depart[vid];
   if (st == kOnEdge) {
-    if (v.latency_debt[vid] >= w.p.dt_us) {
-      v.latency_debt[vid] -= w.p.dt_us;
+    const int64_t debt = v.latency_debt[vid];
+    const int64_t prog = v.progress[vid] + v.advance[vid];
+    const int32_t slot = v.on_edge[vid];
+    const int32_t dest = v.dest[vid];
+    const int64_t L = w.g.len[slot];
+    const int32_t reached = w.g.col[slot];
+    const int32_t bind = w.g.bind[slot];
+    if (debt >= w.p.dt_us) {
+      v.latency_debt[vid] = debt - w.p.dt_us;
       v.lat_steps[vid] += 1;
     } else {
-      const int64_t prog = v.progress[vid] + v.advance[vid];
       v.driving[vid] += 1;
-      const int32_t slot = v.on_edge[vid];
-      const int64_t L = w.g.len[slot];
       if (prog < L) {
         v.progress[vid] = prog;
       } else {
-        const int32_t reached = w.g.col[slot];
-        const int32_t bind = w.g.bind[slot];
-        if (reached == v.dest[vid]) {
+        if (reached == dest) {
           st = kArrived;
           v.progress[vid] = prog;
           v.arrive[vid] = step + 1;
@@ -2226,10 +2271,10 @@ __device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long lo
         v.state[vid] = st;
       }
     }
-    if (st == kOnEdge) atomicAdd(&w.occ_new[v.on_edge[vid]], 1);
+    if (st == kOnEdge) atomicAdd(&w.occ_new[slot], 1);
   }
   active += st == kAtNode || st == kOnEdge || st == kQueued || st == kReleased ||
-            (st == kPending && v.depart[vid] == step + 1);
+            (st == kPending && depart == step + 1);
   unfinished += st != kArrived && st != kRetired;
 }
 
