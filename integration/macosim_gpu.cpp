@@ -64,11 +64,10 @@ gmaco_sim_config to_abi(const SimConfig& c) {
   throw std::runtime_error(std::string("gmaco: ") + msg);
 }
 
-}  // namespace
-
-RunResult gpu_run(const SimConfig& cfg, const DistanceTable& dist, int device) {
-  const auto t0 = std::chrono::steady_clock::now();
-  cfg.validate();
+// Builds the graph descriptor, runs the engine to completion and rebuilds
+// RunResult.  `dd` selects the distance service the engine uses.
+RunResult run_on_device(const SimConfig& cfg, gmaco_distance_desc dd, int device,
+                        std::chrono::steady_clock::time_point t0) {
   const RoadNetwork& net = *cfg.network;
   const int n = net.node_count(), m = net.edge_count();
   std::vector<uint8_t> sig(n);
@@ -82,10 +81,6 @@ RunResult gpu_run(const SimConfig& cfg, const DistanceTable& dist, int device) {
     lanes[e.id] = e.lanes;
   }
   gmaco_graph_desc g{n, m, sig.data(), from.data(), to.data(), len.data(), lanes.data()};
-  std::vector<int64_t> d(static_cast<size_t>(n) * n);
-  for (int u = 0; u < n; ++u)
-    for (int v = 0; v < n; ++v) d[static_cast<size_t>(u) * n + v] = dist.dist_mm(u, v);
-  gmaco_distance_desc dd{GMACO_DIST_DENSE, 0, 0, d.data(), nullptr, 0, 0};
   const gmaco_sim_config c = to_abi(cfg);
 
   gmaco_engine* h = nullptr;
@@ -113,10 +108,32 @@ RunResult gpu_run(const SimConfig& cfg, const DistanceTable& dist, int device) {
   return out;
 }
 
-RunResult gpu_run(const SimConfig& cfg, int device) {
+}  // namespace
+
+// The caller already holds the reference's dense table (run_matrix builds
+// one per network, harness.cpp:332): it is handed to the engine as is.
+// DistanceTable keeps its storage private, so the table is read through its
+// inline accessor row by row (one strided copy, no call per entry).
+RunResult gpu_run(const SimConfig& cfg, const DistanceTable& dist, int device) {
+  const auto t0 = std::chrono::steady_clock::now();
   cfg.validate();
-  DistanceTable dist = all_pairs_distances(*cfg.network);
-  return gpu_run(cfg, dist, device);
+  const int n = cfg.network->node_count();
+  if (dist.size() != n) throw ValidationError("gpu_run: distance table size does not match the network");
+  std::vector<int64_t> d(static_cast<size_t>(n) * n);
+  for (int u = 0; u < n; ++u) {
+    int64_t* row = d.data() + static_cast<size_t>(u) * n;
+    for (int v = 0; v < n; ++v) row[v] = dist.dist_mm(u, v);
+  }
+  return run_on_device(cfg, gmaco_distance_desc{GMACO_DIST_DENSE, 0, 0, d.data(), nullptr, 0, 0}, device, t0);
+}
+
+// No table: the engine computes the exact distance table itself with its
+// device SSSP (DIST_DENSE with a null table), so the host never runs the
+// O(n^2)-memory all_pairs_distances (net.cpp:419-437).
+RunResult gpu_run(const SimConfig& cfg, int device) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cfg.validate();
+  return run_on_device(cfg, gmaco_distance_desc{GMACO_DIST_DENSE, 0, 0, nullptr, nullptr, 0, 0}, device, t0);
 }
 
 }  // namespace macosim

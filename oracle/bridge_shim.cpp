@@ -1,22 +1,26 @@
 // bridge_shim.cpp — TEST INFRASTRUCTURE ONLY: runs the reference run() and
 // the integration executor gpu_run() (integration/macosim_gpu.cpp) on the
-// same SimConfig and reports RunResult::identical_to (engine.cpp:34-40).
+// same SimConfig and reports RunResult::identical_to (engine.cpp:34-40); and
+// drives the reference harness patched with the "gpu" executor
+// (harness_gpu.patch): load_scenario -> run_matrix -> write_results_csv.
+#include <fstream>
+#include <sstream>
 #include <string>
 
 #include "gmaco.h"
 #include "macosim/engine.hpp"
+#include "macosim/harness.hpp"
 #include "macosim_gpu.hpp"
-
-namespace macosim {
-// provided by ref_shim.cpp
-}
 
 extern "C" {
 // 1 identical, 0 different, -1 error (message via bridge_last_error)
 static thread_local std::string g_bridge_err;
 const char* bridge_last_error(void) { return g_bridge_err.c_str(); }
 
-int bridge_identical(const gmaco_graph_desc* gd, int algorithm, int vehicles, uint64_t seed, int device) {
+// with_table = 1: gpu_run(cfg, dist, device) with the reference's dense
+// table; 0: gpu_run(cfg, device), the engine builds the table on the device.
+int bridge_identical(const gmaco_graph_desc* gd, int algorithm, int vehicles, uint64_t seed, int device,
+                     int with_table) {
   using namespace macosim;
   try {
     std::vector<RoadNode> nodes(gd->node_count);
@@ -33,11 +37,55 @@ int bridge_identical(const gmaco_graph_desc* gd, int algorithm, int vehicles, ui
     cfg.seed = seed;
     DistanceTable dist = all_pairs_distances(net);
     RunResult a = run(cfg, dist);
-    RunResult b = gpu_run(cfg, dist, device);
+    RunResult b = with_table ? gpu_run(cfg, dist, device) : gpu_run(cfg, device);
     return a.identical_to(b) ? 1 : 0;
   } catch (const std::exception& e) {
     g_bridge_err = e.what();
     return -1;
+  }
+}
+
+// The reference harness end to end: scenario JSON text -> load_scenario ->
+// load_scenario_network -> run_matrix (executors as the scenario lists them)
+// -> write_results_csv_file(csv_path) -> read_results_csv_file round trip ->
+// emit_report into report_path.  Returns the row count (the round trip must
+// reproduce it) or -1 with the message in bridge_last_error; failed cells are
+// reported as an error too.
+int bridge_run_matrix(const char* scenario_json, const char* csv_path, const char* report_path, int workers) {
+  using namespace macosim;
+  try {
+    Scenario sc = load_scenario(scenario_json);
+    RoadNetwork net = load_scenario_network(sc);
+    ResultTable t = run_matrix(sc, net, workers, nullptr);
+    if (!t.failures().empty()) {
+      g_bridge_err = "run_matrix failures: " + t.failures().front();
+      return -1;
+    }
+    write_results_csv_file(t, csv_path);
+    ResultTable back = read_results_csv_file(csv_path);
+    if (back.rows().size() != t.rows().size()) {
+      g_bridge_err = "results csv round trip changed the row count";
+      return -1;
+    }
+    std::ofstream rep(report_path);
+    std::ostringstream data;
+    emit_report(back, rep, data);
+    rep << "\n" << data.str();
+    return static_cast<int>(t.rows().size());
+  } catch (const std::exception& e) {
+    g_bridge_err = e.what();
+    return -1;
+  }
+}
+
+// load_scenario's validation alone (status 1 + message on a bad scenario).
+int bridge_load_scenario(const char* scenario_json) {
+  try {
+    macosim::load_scenario(scenario_json);
+    return 0;
+  } catch (const std::exception& e) {
+    g_bridge_err = e.what();
+    return 1;
   }
 }
 }

@@ -12,6 +12,8 @@
 #include "gmaco_oracle.h"
 
 #include <alloca.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -347,6 +349,41 @@ static void build_reverse(const og_net* g, int32_t** rptr, int32_t** rsrc, int32
   free(c);
 }
 
+/* One reverse Dijkstra per target (dijkstra_to, net.cpp:359-385), the
+ * targets spread over host threads (each row is independent). */
+typedef struct {
+  const og_net* g;
+  const int32_t *rp, *rs, *re, *targets;
+  int64_t* out;
+  int32_t ntargets, next;
+  pthread_mutex_t mu;
+} sssp_job;
+
+static void* sssp_worker(void* arg) {
+  sssp_job* j = (sssp_job*)arg;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    int32_t t = j->next++;
+    pthread_mutex_unlock(&j->mu);
+    if (t >= j->ntargets) return NULL;
+    dijkstra_rev(j->g, j->rp, j->rs, j->re, j->targets[t], j->out + (size_t)t * j->g->n);
+  }
+}
+
+static void targets_sssp_run(const og_net* g, const int32_t* targets, int32_t T, int64_t* out) {
+  int32_t *rp, *rs, *re;
+  build_reverse(g, &rp, &rs, &re);
+  sssp_job j = {g, rp, rs, re, targets, out, T, 0, PTHREAD_MUTEX_INITIALIZER};
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > T) nt = T;
+  if (nt > 64) nt = 64;
+  pthread_t th[64];
+  for (long i = 0; i < nt; ++i) pthread_create(&th[i], NULL, sssp_worker, &j);
+  for (long i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+  free(rp); free(rs); free(re);
+}
+
 static int32_t greedy_hop(const og_net* g, const int64_t* dist_to, int32_t u) { /* net.cpp:387-395 */
   for (int32_t k = g->out_ptr[u]; k < g->out_ptr[u + 1]; ++k) {
     int32_t nb = g->out_nbr[k];
@@ -463,6 +500,8 @@ struct og_world {
   int32_t vlo, vhi; /* planning range (sharded protocol) */
   int32_t* dec_rec; /* this step's decision per vehicle: edge, -1 none, -2 retired */
 };
+
+static void targets_sssp(og_world* w) { targets_sssp_run(&w->g, w->targets, w->ntargets, w->tdist); }
 
 /* ---- distance service (routing.cpp reads dist.reachable / dist.dist_mm) -- */
 static int64_t dist_to_dest(const og_world* w, int32_t x, int32_t dest) {
@@ -919,18 +958,15 @@ og_world* og_world_create(const gmaco_graph_desc* gd, const gmaco_distance_desc*
     w->slot_of = malloc(sizeof(int32_t) * (size_t)n);
     for (int32_t i = 0; i < n; ++i) w->slot_of[i] = -1;
     w->tdist = malloc(sizeof(int64_t) * (size_t)w->ntargets * (size_t)n);
-    int32_t *rp, *rs, *re;
-    build_reverse(&w->g, &rp, &rs, &re);
     for (int32_t t = 0; t < w->ntargets; ++t) {
       int32_t x = w->targets[t];
       if (x < 0 || x >= n || w->slot_of[x] >= 0) {
         set_err(err, cap, "targets distance: invalid or duplicate target %d", x);
-        free(rp); free(rs); free(re); og_world_destroy(w); return NULL;
+        og_world_destroy(w); return NULL;
       }
       w->slot_of[x] = t;
-      dijkstra_rev(&w->g, rp, rs, re, x, w->tdist + (size_t)t * n);
     }
-    free(rp); free(rs); free(re);
+    targets_sssp(w);
   } else {
     set_err(err, cap, "unknown distance kind %d", dd->kind); og_world_destroy(w); return NULL;
   }

@@ -227,6 +227,21 @@ struct DevWorld {
   int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)
   int32_t* dec_head;  // [m] decision stack per slot (network-wide MACO) or per node (scoped)
   const int64_t* dep_amount;  // lattice: deposit_amount(h * edge length) for h = 0..plan_cap (host-computed)
+  // tau^alpha for alpha not in {0, 1}: [tau_hi - tau_lo + 1] entries
+  // pow(t / 1e6, alpha) for every reachable pheromone value t (the field is
+  // clamped to [tau_lo, tau_hi] by every update), computed once by the host's
+  // glibc pow, the function routing.cpp:93 calls, so the device weights are
+  // bit-identical to the reference's; nullptr otherwise
+  const double* taupow;
 };
+
+// pow(tau_to_double(t), alpha) (routing.cpp:91-93; tau_to_double pheromone.hpp:19)
+__device__ __forceinline__ double tau_alpha(const DevWorld& w, int64_t t) {
+  const double a = w.p.alpha;
+  if (a == 1.0) return __ddiv_rn((double)t, 1e6);
+  if (a == 0.0) return 1.0;
+  if (w.taupow) return w.taupow[t - w.p.tau_lo];
+  return pow(__ddiv_rn((double)t, 1e6), a);  // table too large: device pow, <= 1 ulp
+}
 
 }  // namespace gmaco

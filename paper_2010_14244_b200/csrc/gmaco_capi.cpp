@@ -406,6 +406,31 @@ struct DevBuffers {
   }
 };
 
+// Exact tau^alpha table (DevWorld::taupow): pow(t / 1e6, alpha) by the
+// host's glibc pow -- the call routing.cpp:93 makes -- for every pheromone
+// value t in [lo, hi], across all host threads.  Skipped (nullptr: device pow,
+// <= 1 ulp from glibc) when the range exceeds kTauPowMax entries.
+constexpr int64_t kTauPowMax = int64_t(1) << 30;  // 8 GiB of the 180 GB HBM
+const double* build_taupow(DevBuffers& B, int64_t lo, int64_t hi, double alpha, cudaStream_t st) {
+  const int64_t n = hi - lo + 1;
+  if (n <= 0 || n > kTauPowMax) return nullptr;
+  double* host = nullptr;
+  CK(cudaMallocHost(&host, n * sizeof(double)));
+  const int nt = (int)std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (int k = 0; k < nt; ++k)
+    th.emplace_back([=] {
+      for (int64_t i = n * k / nt; i < n * (k + 1) / nt; ++i)
+        host[i] = std::pow(static_cast<double>(lo + i) / 1e6, alpha);
+    });
+  for (auto& t : th) t.join();
+  double* d = B.alloc_direct<double>((size_t)n);
+  CK(cudaMemcpyAsync(d, host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaFreeHost(host));
+  return d;
+}
+
 template <class T>
 std::vector<T> download(const T* d, size_t n) {
   std::vector<T> h(n);
@@ -461,6 +486,7 @@ struct gmaco_engine {
     PackDesc snap_pd;
     std::vector<std::pair<size_t, size_t>> fields;  // (staging offset, bytes) per requested field, view order
     size_t oe_off = 0;
+    uint32_t mask = 0;  // which view members the snapshot holds (view_mask)
     bool on_edge = false, armed = false;
   } rslot[2];
   StepResources res;
@@ -490,6 +516,9 @@ struct gmaco_engine {
 
   ~gmaco_engine() {
     if (device >= 0) cudaSetDevice(device);
+    // settle every enqueued step / snapshot gather first: k_pack may still be
+    // writing into the mapped pinned slots handed back to the pool below
+    if (stream) cudaStreamSynchronize(stream);
     if (bench_exec) cudaGraphExecDestroy(bench_exec);
     if (bench_tmpl) cudaGraphDestroy(bench_tmpl);
     for (auto e : bench_ev)
@@ -1135,10 +1164,11 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     const double v = uniform(draw(c.seed, 1, (uint64_t)e), c.pheromone.tau_init_lo, c.pheromone.tau_init_hi);
     tau[s] = std::clamp(tau_from_double(v), lo, hi);
     const double tau_d = static_cast<double>(tau[s]) / 1e6;
-    const double ta = p.alpha == 1.0 ? tau_d : std::pow(tau_d, p.alpha);
+    const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : std::pow(tau_d, p.alpha));
     wt[s] = ta * eta[s];  // load 0: the congestion factor is exactly 1.0
     ecost[s] = slen[s];
   }
+  if (p.alpha != 0.0 && p.alpha != 1.0) w.taupow = build_taupow(B, p.tau_lo, p.tau_hi, p.alpha, h->stream);
   w.tau = B.upload(tau);
   w.weight = B.upload(wt);
   w.ecost = B.upload(ecost);
@@ -1580,18 +1610,30 @@ void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
 }  // namespace
 
 // Process-wide communicators, one per (device, rank, world, unique id): an
-// engine attaching with an id already used in this process shares that
+// engine attaching with an id already used in this process reuses that
 // communicator instead of paying ncclCommInitRank again (a job creates its
-// communicator once; later engines of the same job reuse it).  They live until
-// process exit.
+// communicator once; later engines of the same job reuse it).  A communicator
+// is held EXCLUSIVELY by one live engine: two live engines capturing
+// collectives on one communicator into their own graphs could interleave them
+// in different orders on different ranks and hang the job, so a second attach
+// while the holder is alive fails (status 1).  The holder releases it on
+// destroy; idle communicators stay cached for the next engine of the job.
+struct CommEntry {
+  ncclComm_t comm = nullptr;
+  const gmaco_engine* holder = nullptr;
+};
 static std::mutex g_comm_mu;
-static std::map<std::string, ncclComm_t>& comm_cache() {
-  static std::map<std::string, ncclComm_t> m;
-  return m;
+static std::map<std::string, CommEntry>& comm_cache() {
+  static auto* m = new std::map<std::string, CommEntry>();  // process lifetime
+  return *m;
 }
 
 void gmaco_engine::destroy_comm() {
-  comm = nullptr;  // shared through comm_cache()
+  if (!comm) return;
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  for (auto& kv : comm_cache())
+    if (kv.second.holder == this) kv.second.holder = nullptr;
+  comm = nullptr;
 }
 
 // Host -> device copy ordered on the engine stream and complete on return
@@ -1623,6 +1665,16 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
   if (h) h->ctl_valid = false;
   if (!h || !nccl_id || world < 1 || rank < 0 || rank >= world) return GMACO_EVALIDATION;
   return guarded(h, [&] {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    h->destroy_comm();
+    std::string key(reinterpret_cast<const char*>(&id), sizeof id);
+    key += fmt("/%d/%d/%d", h->device, rank, world);
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    CommEntry& ce = comm_cache()[key];
+    if (ce.holder)
+      throw ValidationError("attach_comm: this communicator is held by another live engine "
+                            "(destroy it first; one engine per communicator at a time)");
     const int32_t V = h->w.p.V;
     const int32_t P = (V + world - 1) / world;  // padded contiguous shards (allgather layout)
     const int32_t lo = std::min(V, rank * P), hi = std::min(V, (rank + 1) * P);
@@ -1630,19 +1682,9 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
     h->rank = rank;
     h->world = world;
     h->shard_pad = P;
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof id);
-    h->destroy_comm();
-    std::string key(reinterpret_cast<const char*>(&id), sizeof id);
-    key += fmt("/%d/%d/%d", h->device, rank, world);
-    std::lock_guard<std::mutex> lk(g_comm_mu);
-    auto it = comm_cache().find(key);
-    if (it != comm_cache().end()) {
-      h->comm = it->second;
-    } else {
-      nck(nccl().CommInitRank(&h->comm, world, id, rank), "ncclCommInitRank");
-      comm_cache()[key] = h->comm;
-    }
+    if (!ce.comm) nck(nccl().CommInitRank(&ce.comm, world, id, rank), "ncclCommInitRank");
+    ce.holder = h;
+    h->comm = ce.comm;
     h->res.exchange = nccl_exchange;
     h->res.exchange_ctx = h;
   });
@@ -1784,14 +1826,47 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
     std::vector<int64_t> t(m, 0);
     std::vector<double> wt(m, 0.0);
     auto eta = download(h->w.g.eta_beta, m);
+    // colony congestion: the next walk's weight and tour cost carry the edge
+    // load (occupancy + the fed queue's length) exactly as stage F+G computed
+    // them (slot_fg): weight x 1/(1+load), cost = len + len*load
+    // every update clamps the field to [tau_min, tau_max] (pheromone.cpp:34-67);
+    // the device relies on it (tau^alpha table index)
+    for (int32_t e = 0; e < h->g.m; ++e)
+      if (tau[e] < h->w.p.tau_lo || tau[e] > h->w.p.tau_hi)
+        throw ValidationError(fmt("set_pheromone: edge %d value %lld outside [tau_min, tau_max]", e,
+                                  (long long)tau[e]));
+    const bool cong = h->w.p.algorithm == GMACO_COLONY && h->w.p.congestion;
+    std::vector<int32_t> occ, bind, qlen;
+    std::vector<int64_t> len, cost;
+    if (cong) {
+      occ = download(h->w.occ_cur, m);
+      bind = download(h->w.g.bind, m);
+      qlen = download(h->w.s.qlen, (size_t)h->S * kPhases);
+      len = download(h->w.g.len, m);
+      cost = download(h->w.ecost, m);
+    }
     for (int32_t s = 0; s < m; ++s) {
       if (h->slot_edge[s] < 0) continue;
       t[s] = tau[h->slot_edge[s]];
       const double tau_d = static_cast<double>(t[s]) / 1e6;
-      wt[s] = (h->w.p.alpha == 1.0 ? tau_d : std::pow(tau_d, h->w.p.alpha)) * eta[s];
+      const double a = h->w.p.alpha;
+      wt[s] = (a == 1.0 ? tau_d : (a == 0.0 ? 1.0 : std::pow(tau_d, a))) * eta[s];
+      if (cong) {
+        const int32_t load = occ[s] + (bind[s] >= 0 ? qlen[bind[s]] : 0);
+        wt[s] = wt[s] * (1.0 / (1.0 + static_cast<double>(load)));
+        cost[s] = len[s] + len[s] * static_cast<int64_t>(load);
+      }
     }
     h2d(h, h->w.tau, t.data(), m * 8);
     h2d(h, h->w.weight, wt.data(), m * 8);
+    if (cong) {
+      h2d(h, h->w.ecost, cost.data(), m * 8);
+      if (h->w.ecost32) {
+        std::vector<int32_t> c32(m);
+        for (int32_t s = 0; s < m; ++s) c32[s] = static_cast<int32_t>(cost[s]);
+        h2d(h, h->w.ecost32, c32.data(), m * 4);
+      }
+    }
     if (h->w.rec) {
       CK(sync_rec_weights(h->w, h->stream));
       CK(cudaStreamSynchronize(h->stream));
@@ -1910,10 +1985,24 @@ static std::vector<std::tuple<void*, const void*, size_t>> vehicle_fields(const 
 
 namespace gmaco {
 namespace {
+// Bit i set <=> the i-th device-gathered member of the view is non-NULL
+// (speed_mps is recomputed on the host and is not part of a snapshot).
+uint32_t view_mask(const gmaco_vehicle_view* v) {
+  const void* m[] = {v->origin, v->dest, v->advance_mm, v->state, v->at_node, v->on_edge, v->progress_mm,
+                     v->overshoot_mm, v->queued_phase, v->queue_joined_step, v->depart_step, v->arrive_step,
+                     v->latency_debt_us, v->driving_steps, v->queued_steps, v->latency_steps, v->decisions,
+                     v->deviations, v->path_length_mm};
+  uint32_t bits = 0;
+  for (size_t i = 0; i < sizeof m / sizeof m[0]; ++i)
+    if (m[i]) bits |= 1u << i;
+  return bits;
+}
+
 // Arms readback slot `slot` for `fields` (layout, pinned buffer, done event)
 // and returns the gather descriptor of the snapshot.
 PackDesc arm_slot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
   auto& rs = h->rslot[slot];
+  rs.mask = view_mask(fields);
   const size_t V = h->w.p.V;
   const auto f = vehicle_fields(h, fields);
   size_t total = 0;
@@ -1980,31 +2069,7 @@ int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, in
   if (!h || !fields || slot < 0 || slot > 1) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     auto& rs = h->rslot[slot];
-    const size_t V = h->w.p.V;
-    const auto f = vehicle_fields(h, fields);
-    size_t total = 0;
-    rs.fields.clear();
-    for (const auto& t : f) {
-      rs.fields.emplace_back(total, V * std::get<2>(t));
-      total += (V * std::get<2>(t) + 15) & ~size_t(15);
-    }
-    rs.on_edge = fields->on_edge != nullptr;
-    rs.oe_off = total;
-    if (rs.on_edge) total += V * 4;
-    total = std::max<size_t>(total, 16);
-    if (rs.bytes < total) {
-      PinnedPool::give(rs.buf);
-      rs.buf = PinnedPool::take(total);
-      rs.bytes = total;
-    }
-    if (!rs.done) CK(cudaEventCreateWithFlags(&rs.done, cudaEventDisableTiming));
-    char* dev = nullptr;
-    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), rs.buf, 0));
-    PackDesc pd;
-    for (size_t i = 0; i < f.size(); ++i) pd.f[pd.n++] = PackField{std::get<1>(f[i]), dev + rs.fields[i].first,
-                                                                   rs.fields[i].second};
-    if (rs.on_edge) pd.f[pd.n++] = PackField{h->w.v.on_edge, dev + rs.oe_off, V * 4};
-    CK(launch_pack(pd, h->stream));
+    CK(launch_pack(arm_slot(h, fields, slot), h->stream));
     CK(cudaEventRecord(rs.done, h->stream));
     rs.armed = true;
   }, /*stream_ordered=*/true);
@@ -2015,9 +2080,11 @@ int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view*
   return guarded(h, [&] {
     auto& rs = h->rslot[slot];
     if (!rs.armed) throw ValidationError("vehicles_wait: no snapshot enqueued in this slot");
-    const auto f = vehicle_fields(h, view);
-    if (f.size() != rs.fields.size() || (view->on_edge != nullptr) != rs.on_edge)
+    // exactly the members the snapshot was taken for: the copies below are
+    // sized by the snapshot's fields, so any other set could overrun `view`
+    if (view_mask(view) != rs.mask)
       throw ValidationError("vehicles_wait: view fields differ from the enqueued snapshot");
+    const auto f = vehicle_fields(h, view);
     CK(cudaEventSynchronize(rs.done));  // only this snapshot, not later steps
     const char* st = static_cast<const char*>(rs.buf);
     for (size_t i = 0; i < f.size(); ++i) std::memcpy(std::get<0>(f[i]), st + rs.fields[i].first, rs.fields[i].second);

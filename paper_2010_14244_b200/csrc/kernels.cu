@@ -2414,9 +2414,7 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
   w.occ_cur[s] = occ;
   w.occ_new[s] = 0;
   if (aco) {
-    const double tau_d = __ddiv_rn((double)t, 1e6);
-    const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : pow(tau_d, p.alpha));
-    double wt = __dmul_rn(ta, eta);
+    double wt = __dmul_rn(tau_alpha(w, t), eta);
     int64_t cost = len;
     if (alg == 4 && p.congestion) {
       const int32_t load = occ + q;
@@ -2728,9 +2726,7 @@ __global__ void k_next_node(DevWorld w, int algorithm, int count, const int32_t*
         double wv[kMaxDegree];
         for (uint32_t m = cand; m; m &= m - 1, ++c) {
           const int32_t s = r.first + __ffs(m) - 1;
-          const double tau_d = __ddiv_rn((double)w.tau[s], 1e6);
-          const double ta = w.p.alpha == 1.0 ? tau_d : (w.p.alpha == 0.0 ? 1.0 : pow(tau_d, w.p.alpha));
-          wv[c] = __dmul_rn(ta, w.g.eta_beta[s]);
+          wv[c] = __dmul_rn(tau_alpha(w, w.tau[s]), w.g.eta_beta[s]);
           total = __dadd_rn(total, wv[c]);
         }
         const double u = to_unit(draw(w.p.seed, 5, entity[i], stepk[i]));

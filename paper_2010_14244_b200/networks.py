@@ -124,14 +124,16 @@ def _splitmix_unit(seed: int, stream: int, idx: np.ndarray, sub: int) -> np.ndar
 
 
 def random_geometric(nodes: int, k: int = 3, lanes: int = 3, seed: int = 20250810,
-                     density_per_km2: float = 100.0) -> Network:
+                     density_per_km2: float = 100.0, links: int | None = None) -> Network:
     """Random geometric road graph: `nodes` seeded points in a square box
     (density_per_km2 points per km^2), every point linked to its k nearest
     neighbours (undirected, deduplicated), disconnected components bridged to
     their nearest outside point, each link materialized as two directed edges
     with integer-mm Euclidean lengths (>= 1 m, as net.cpp:348).  Undirected
-    degree >= 3 ⇒ signalized (net.cpp:338-341).  k=3 gives ≈2·n undirected
-    links, i.e. ≈4M directed edges at 1M nodes (BASELINE config 4)."""
+    degree >= 3 ⇒ signalized (net.cpp:338-341).  k=3 alone gives ≈1.87·n
+    undirected links; `links` tops the set up to that many undirected links
+    with the shortest (k+1)-th-neighbour links (links=2·n: exactly 4M directed
+    edges at 1M nodes before bridging, BASELINE config 4)."""
     from scipy.sparse import coo_matrix
     from scipy.sparse.csgraph import connected_components
     from scipy.spatial import cKDTree
@@ -140,12 +142,23 @@ def random_geometric(nodes: int, k: int = 3, lanes: int = 3, seed: int = 2025081
     idx = np.arange(nodes, dtype=np.uint64)
     pts = np.stack([_splitmix_unit(seed, 6, idx, 0), _splitmix_unit(seed, 6, idx, 1)], axis=1) * side_m
     tree = cKDTree(pts)
-    _, nn = tree.query(pts, k=k + 1)
+    dd, nn = tree.query(pts, k=k + 2)
     a = np.repeat(np.arange(nodes), k)
-    b = nn[:, 1:].ravel()
+    b = nn[:, 1:k + 1].ravel()
     lo = np.minimum(a, b).astype(np.int64)
     hi = np.maximum(a, b).astype(np.int64)
     key = np.unique(lo * nodes + hi)
+    if links is not None and len(key) < links:
+        # shortest (k+1)-th-neighbour links not already present, in (length, key) order
+        xa = np.arange(nodes, dtype=np.int64)
+        xb = nn[:, k + 1].astype(np.int64)
+        xkey = np.minimum(xa, xb) * nodes + np.maximum(xa, xb)
+        order = np.lexsort((xkey, dd[:, k + 1]))
+        xkey = xkey[order]
+        _, first = np.unique(xkey, return_index=True)
+        xkey = xkey[np.sort(first)]
+        xkey = xkey[~np.isin(xkey, key)]
+        key = np.unique(np.concatenate([key, xkey[:links - len(key)]]))
     lo, hi = key // nodes, key % nodes
     # bridge components: connect each non-giant component to the nearest point outside it
     while True:

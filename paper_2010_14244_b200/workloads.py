@@ -43,7 +43,7 @@ def c4(seed=1, max_steps=50, vehicles=100000, nodes=1_000_000, targets=64, ants=
 
     Distances: exact reverse-Dijkstra tables to a bounded destination set of
     `targets` nodes (GMACO_DIST_TARGETS); vehicles' destinations lie in it."""
-    net = networks.random_geometric(nodes, k=3, seed=20250810)
+    net = networks.random_geometric(nodes, k=3, seed=20250810, links=2 * nodes)
     rng = np.random.default_rng(seed)
     tgt = np.sort(rng.choice(nodes, size=targets, replace=False)).astype(np.int32)
     dist = abi.DistanceDesc(kind=abi.DIST_TARGETS, targets=abi.ptr(tgt, __import__("ctypes").c_int32),

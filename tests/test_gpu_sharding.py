@@ -143,10 +143,13 @@ def test_host_mediated_shards_every_walker(kind, monkeypatch):
 
 
 def test_nccl_communicator_shared_by_engines_of_a_job():
-    """Engines attaching with the same (rank, world, id) share one
+    """Engines attaching with the same (rank, world, id) reuse one
     communicator (the first attach creates it; a unique id is single-use for
-    ncclCommInitRank), and each still equals the unsharded engine — also after
-    the first engine is closed."""
+    ncclCommInitRank), one live engine at a time: a second attach while the
+    holder is alive is refused (status 1), since two engines capturing
+    collectives on one communicator could interleave them differently on
+    different ranks.  After the holder is closed the next engine reuses it and
+    still equals the unsharded engine."""
     from paper_2010_14244_b200 import engine
     import ctypes as C
     net, cfg = world(V=300, ants=32, rows=16)
@@ -158,8 +161,11 @@ def test_nccl_communicator_shared_by_engines_of_a_job():
     first.attach_comm(0, 1, uid.raw)
     first.step(5)
     assert same(first, single) is None
-    first.close()
     second = Engine(net, cfg, net.grid_distance())
+    with pytest.raises(engine.EngineError) as ei:
+        second.attach_comm(0, 1, uid.raw)
+    assert ei.value.code == 1 and "held by another live engine" in str(ei.value)
+    first.close()
     second.attach_comm(0, 1, uid.raw)  # reuses the job's communicator
     second.step(5)
     assert same(second, single) is None

@@ -58,6 +58,7 @@ VARIANTS = [
     dict(spawn=abi.UNIFORM_WINDOW, spawn_window_steps=30), dict(controller=abi.ADAPTIVE),
     dict(progress_filter=0, max_steps=300), dict(alpha_beta=(0.0, 0.0)), dict(alpha_beta=(1.0, 1.0)),
     dict(dt_s=0.7, max_steps=800), dict(tau_min=1.0), dict(max_steps=0), dict(max_steps=9),
+    dict(alpha_beta=(0.5, 1.0)), dict(alpha_beta=(2.0, 1.5)),
 ]
 
 
