@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--skip-extra", action="store_true", help="skip the chained and e2e legs")
     ap.add_argument("--force-comm", action="store_true",
                     help="attach the NCCL exchange even at one rank (exercises the multi-GPU path)")
+    ap.add_argument("--algorithm", choices=["colony", "maco-p", "maco", "aco", "dijkstra"], default="colony",
+                    help="colony = GMACO-P colonies (the headline); the others run the reference's own "
+                         "algorithms (one decision per vehicle at a node per step) on --config c1|c2|c3")
     return ap.parse_args()
 
 
@@ -94,6 +97,13 @@ def workload_config(seed: int, max_steps: int, vehicles: int = VEHICLES):
 
 def config_block(args, world, vehicles=None):
     from paper_2010_14244_b200 import workloads
+    if args.algorithm != "colony":
+        R, Cc, sig, V = REF_ALG_SHAPES[args.config]
+        return {"workload": f"{args.config.upper()}: {R}x{Cc} grid ({sig} intersections signalized), {V} vehicles, "
+                            f"reference algorithm {args.algorithm} (one routing decision per vehicle at a node "
+                            f"per step; engine step = sequential_step)",
+                "algorithm": args.algorithm, "iterations_timed": args.steps,
+                "l2": "flushed (512 MiB write) between timed steps", "parallelism": "1 GPU"}
     if args.config != "c2":
         return {"workload": f"{args.config.upper()}: {workloads.DESCRIPTIONS[args.config]}",
                 "vehicles_total": vehicles, "iterations_timed": args.steps,
@@ -101,7 +111,9 @@ def config_block(args, world, vehicles=None):
                 "parallelism": f"one world sharded over {world} GPUs" if world > 1 else "1 GPU"}
     return {
         "workload": "C2: 32x32 grid, signals at every intersection, 1000 vehicles per GPU, 64 ants/colony, "
-                    "preemptive signals, congestion-modified pheromone, one colony iteration per step",
+                    "preemptive signals, one colony iteration per step (GPU arm: congestion-modified roulette and "
+                    "best-tour deposit; reference arm: the reference's own next_node_aco tours, which have no "
+                    "congestion term, plus its sequential_step)",
         "network": f"grid {GRID}x{GRID}, 200 m edges, 3 lanes, {GRID * GRID} signals",
         "vehicles_per_gpu": VEHICLES,
         "ants_per_colony": ANTS,
@@ -196,12 +208,144 @@ def secondary_c4(peak, peak_src, steps=10, warmup=3):
                          "avg_launch_us": walk_s / steps * 1e6}}
 
 
+def secondary_c3(steps=10, warmup=3):
+    """C3 (100x100 grid, 10,000 vehicles, 128-ant colonies: the largest
+    lattice config of BASELINE.json that one GPU runs whole) on the same GPU,
+    same rules as the headline.  No HBM-roofline fraction: the lattice walk's
+    state is SMEM/L2-resident, so the byte model does not bound it (its ncu
+    limiter is recorded under profiles/)."""
+    from paper_2010_14244_b200 import workloads
+    from paper_2010_14244_b200.engine import Engine
+    net, cfg, dist, keep = workloads.c3(seed=1, max_steps=warmup + steps + 1)
+    e = Engine(net, cfg, dist)
+    e.step(warmup)
+    c0 = e.counters()
+    walk, stepms = e.bench_steps(steps, L2_FLUSH_BYTES, "both")
+    c1 = e.counters()
+    e.close()
+    tot = float(stepms.sum()) / 1e3
+    return {"workload": "C3: " + workloads.DESCRIPTIONS["c3"], "metric": "ant-steps/sec",
+            "value": (c1.ant_steps - c0.ant_steps) / tot, "unit": "ant-steps/s",
+            "ms_per_step": float(stepms.mean()), "walk_ms_per_step": float(walk.mean()),
+            "iterations_timed": steps,
+            "vehicle_routes_per_sec": (c1.vehicle_routes - c0.vehicle_routes) / tot,
+            "kernel": "k_colony_grid (lattice walker, one-vehicle CTAs, 128 ants)"}
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+REF_ALG_SHAPES = {"c1": (10, 10, "interior", 100), "c2": (32, 32, "all", 1000), "c3": (100, 100, "interior", 10000)}
+
+
+def ref_algorithm_world(alg: str, config: str, seed: int = 1, max_steps: int = 5000):
+    """(net, cfg) of a reference-algorithm run (dijkstra / aco / maco /
+    maco-p; maco-p with preemptive signals, the others fixed, as
+    harness.cpp:63-72) on a BASELINE grid config."""
+    from paper_2010_14244_b200 import abi, networks
+    if config not in REF_ALG_SHAPES:
+        raise SystemExit(f"--algorithm {alg} runs on --config c1, c2 or c3")
+    R, Cc, sig, V = REF_ALG_SHAPES[config]
+    net = networks.grid(R, Cc, signals=sig)
+    cfg = abi.default_config(algorithm=alg, vehicle_count=V, seed=seed, max_steps=max_steps)
+    return net, cfg
+
+
+def reference_algorithms_block(threads: int):
+    """SURVEY 8(d)(i)/(iii) on the GPU box, same process: the paper's own
+    algorithm (MACO-P, preemptive signals) on C2 end to end through the C ABI
+    -- gpu_run's path: gmaco_create with the engine's device SSSP building
+    the exact distance table, gmaco_run, gmaco_collect -- against the
+    reference's run() and parallel_run(nproc) (engine.cpp:435-450,
+    parallel.cpp:276-291) including all_pairs_distances, which they need; and
+    the F+G edge kernel (fold_maco_edge + evaporate_one) in edge-updates/s."""
+    import torch
+    from oracle import oracle as O
+    from paper_2010_14244_b200 import abi
+    from paper_2010_14244_b200.engine import Engine
+    if not O.ref_available():
+        return {"unavailable": "oracle/_ref not built"}
+    net, cfg = ref_algorithm_world("maco-p", "c2")
+    ours, runs, res = [], [], None
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e = Engine(net, cfg, abi.DistanceDesc(kind=abi.DIST_DENSE))  # device SSSP builds the table
+        t1 = time.perf_counter()
+        res = e.run()
+        t2 = time.perf_counter()
+        ctr = e.counters()
+        e.close()
+        ours.append(t2 - t0)
+        runs.append(t2 - t1)
+    ours_s, run_s = float(np.median(ours[1:])), float(np.median(runs[1:]))
+    steps, decisions = int(res[0].steps_executed), int(ctr.decisions)
+    seq, par, seq_run_ms, par_run_ms, ref = [], [], [], [], None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ref = O.ref_run(net, cfg)
+        seq.append(time.perf_counter() - t0)
+        seq_run_ms.append(ref[0].wall_clock_ms)
+        t0 = time.perf_counter()
+        rp = O.ref_run(net, cfg, threads)
+        par.append(time.perf_counter() - t0)
+        par_run_ms.append(rp[0].wall_clock_ms)
+    seq_s, par_s = float(np.median(seq)), float(np.median(par))
+    block = {
+        "workload": "C2 network (32x32, signals at every intersection), 1000 vehicles, algorithm maco-p with "
+                    "preemptive signals (the reference's own path), whole run to completion",
+        "identical_to_reference": O.results_identical(res, ref),
+        "steps": steps, "decisions": decisions,
+        "ours": {"e2e_s": ours_s, "run_s": run_s, "steps_per_sec_e2e": steps / ours_s,
+                 "decisions_per_sec_e2e": decisions / ours_s,
+                 "includes": "gmaco_create from host arrays (device SSSP distance table) + gmaco_run + gmaco_collect"},
+        "reference_run": {"e2e_s": seq_s, "run_ms": float(np.median(seq_run_ms)), "threads": 1,
+                          "includes": "all_pairs_distances + run(cfg, dist)"},
+        "reference_parallel_run": {"e2e_s": par_s, "run_ms": float(np.median(par_run_ms)), "threads": threads,
+                                   "includes": f"all_pairs_distances + parallel_run(cfg, dist, {threads})"},
+        "speedup_e2e_vs_run": seq_s / ours_s, "speedup_e2e_vs_parallel_run": par_s / ours_s,
+        "speedup_run_only_vs_run": float(np.median(seq_run_ms)) / 1e3 / run_s,
+    }
+    # (iii) F+G edge kernel: reference fold + evaporation on all host threads
+    # over the C3 network with a step's worth of decisions, against this
+    # engine's whole stage C..G tail (signals, motion, fold + evaporation) of
+    # a C3 maco step, in edge-updates/s
+    net3, cfg3 = ref_algorithm_world("maco", "c3")
+    rng = np.random.default_rng(1)
+    tau = rng.integers(0, 10 ** 8, net3.edge_count)
+    e3 = Engine(net3, cfg3, net3.grid_distance())
+    e3.step(5)
+    walk, stepms = e3.bench_steps(20, L2_FLUSH_BYTES, "both")
+    dpst = max(1, int(e3.counters().decisions / (25)))
+    e3.close()
+    dec = rng.integers(0, net3.edge_count, dpst)
+    sec, _ = O.ref_fold_bench(tau, dec, 20, threads, cfg3.pheromone)
+    tail_s = float((stepms - walk).mean()) / 1e3
+    block["fold_edge_updates_per_sec"] = {
+        "network": "C3 grid 100x100 (39,600 edges), maco (network-wide fold)",
+        "reference": net3.edge_count * 20 / sec, "reference_threads": threads,
+        "ours_tail": net3.edge_count / tail_s if tail_s > 0 else None,
+        "ours_note": "whole cooperative tail per step (signals + motion + fold + evaporation), L2 flushed",
+        "ours_step_ms": float(stepms.mean()), "ours_decide_ms": float(walk.mean()),
+    }
+    return block
 
 
 # ----------------------------------------------------------------------------
@@ -234,12 +378,55 @@ class RefSampler:
         return s, r, time.perf_counter() - t0
 
 
+class RefStepSampler:
+    """Reference-algorithm steps (sequential_step, engine.cpp:352-400) on the
+    --config world; ant-steps = routing decisions (one next_node_* call
+    each).  A finished world is replaced by a fresh one (next seed)."""
+
+    def __init__(self, alg, config):
+        self.alg, self.config, self.seed, self.w = alg, config, 1, None
+
+    def iteration(self):
+        from oracle import oracle as O
+        if self.w is None or self.w.finished():
+            net, cfg = ref_algorithm_world(self.alg, self.config, self.seed)
+            self.w = O.RefWorld(net, cfg)
+            self.seed += 1
+        d0 = int(self.w.vehicles()["decisions"].sum())
+        t0 = time.perf_counter()
+        self.w.step(1)
+        dt = time.perf_counter() - t0
+        return int(self.w.vehicles()["decisions"].sum()) - d0, 0, dt
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     from oracle import oracle as O
     if not O.ref_available():
         emit({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"})
+        return
+    if args.algorithm != "colony":
+        smp = RefStepSampler(args.algorithm, args.config)
+        for _ in range(args.warmup):
+            smp.iteration()
+        dec = 0
+        dt = 0.0
+        for _ in range(args.steps):
+            d, _, t = smp.iteration()
+            dec += d
+            dt += t
+        value = dec / dt
+        emit({"impl": "reference", "metric": "ant-steps/sec", "value": value, "unit": "ant-steps/s",
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+              "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64",
+              "data": "synthetic", "config": config_block(args, 1),
+              "engine_steps_per_sec": args.steps / dt,
+              "cpu_baseline": {"value": value, "unit": "ant-steps/s", "cores": 1, "kind": "reference",
+                               "cpu_model": cpu_model(),
+                               "sample": f"{args.steps} sequential_step calls of the reference ({args.algorithm}, "
+                                         f"{args.config.upper()}; ant-step = one routing decision)"},
+              "e2e": {"value": value, "unit": "ant-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
         return
     threads = os.cpu_count() or 1
     smp = RefSampler(threads)
@@ -260,6 +447,7 @@ def run_reference(args, rank, world):
         "data": "synthetic", "config": config_block(args, 1),
         "vehicle_routes_per_sec": routes / dt,
         "cpu_baseline": {"value": value, "unit": "ant-steps/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.steps} colony iterations of the C2 workload, reference "
                                    f"next_node_aco tours on {threads} std::threads + sequential_step"},
         "e2e": {"value": value, "unit": "ant-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -282,6 +470,7 @@ def cpu_baseline(seconds):
             dt += t
             its += 1
         return {"value": steps / dt, "unit": "ant-steps/s", "cores": threads, "kind": "reference",
+                "cpu_model": cpu_model(),
                 "sample": f"{its} colony iterations (C2, 64 ants, reference next_node_aco on {threads} "
                           f"threads + sequential_step; finished worlds restarted), {dt:.1f} s"}
     from paper_2010_14244_b200 import networks
@@ -294,6 +483,7 @@ def cpu_baseline(seconds):
         its += 1
     dt = time.perf_counter() - t0
     return {"value": w.counters().ant_steps / dt, "unit": "ant-steps/s", "cores": 1, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{its} colony iterations of the C2 workload on the C oracle, {dt:.1f} s"}
 
 
@@ -317,6 +507,9 @@ def build_workload(args, world):
     shard it (strong scaling), as BASELINE.json states them."""
     from paper_2010_14244_b200 import workloads
     max_steps = args.warmup + args.steps + 1
+    if args.algorithm != "colony":
+        net, cfg = ref_algorithm_world(args.algorithm, args.config, 1, max_steps=100000)
+        return net, cfg, net.grid_distance(), None
     if args.config == "c2":
         return workloads.c2(seed=1, max_steps=max_steps, vehicles=VEHICLES * world)
     return workloads.CONFIGS[args.config](seed=1, max_steps=max_steps)
@@ -462,7 +655,7 @@ def run_ours(args, rank, world, local):
     traffic, traffic_src = None, None
     try:  # DRAM bytes per walk launch from the committed ncu capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as f:
-            rec = json.load(f)[args.config]
+            rec = json.load(f)[args.config if args.algorithm == "colony" else f"{args.algorithm}-{args.config}"]
         traffic, traffic_src = rec["dram_bytes_per_launch"], rec["source"]
     except (OSError, KeyError, ValueError):
         pass
@@ -470,6 +663,8 @@ def run_ours(args, rank, world, local):
     walk_kernel = ("k_colony_grid (stage-B lattice colony walk)" if lattice else
                    "k_colony_qt (stage-B ant-queue colony walk over per-target candidate rows; "
                    "refresh/pro/epi kernels inside the timed walk)")
+    if args.algorithm != "colony":
+        walk_kernel = "k_decide (stage B: one next_node_* decision per vehicle at a node)"
     note = ("latency-bound: one colony iteration is a ~15 us dependent walk over L2/SMEM-resident state "
             "(~1 MB), see DESIGN.md §7" if args.config in ("c1", "c2") else
             "throughput-bound gather walk, see DESIGN.md §7")
@@ -488,6 +683,7 @@ def run_ours(args, rank, world, local):
         "data": "synthetic",
         "config": config_block(args, world, vehicles),
         "vehicle_routes_per_sec": tot_routes / t_dev,
+        "engine_steps_per_sec": args.steps / t_dev,
         "ant_steps_per_iteration": tot_steps / args.steps,
         "walk_kernel_share": (walk_ms / step_ms) if step_ms else None,
         "chained_graph_value": tot_chained / chained_s,
@@ -513,10 +709,24 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
         "completed_vehicles_e2e": completed,
     }
-    if world == 1 and not args.no_secondary and args.config == "c2":
+    headline = args.algorithm == "colony" and args.config == "c2"
+    if world == 1 and not args.no_secondary and headline:
         line["secondary"] = secondary_c4(peak, peak_src)
-    if world == 1 and not args.no_cpu_baseline and args.config == "c2":
+        line["secondary_c3"] = secondary_c3()
+        line["reference_algorithms"] = reference_algorithms_block(os.cpu_count() or 1)
+    if world == 1 and not args.no_cpu_baseline and headline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if world == 1 and not args.no_cpu_baseline and args.algorithm != "colony":
+        smp = RefStepSampler(args.algorithm, args.config)
+        smp.iteration()
+        dec, dt, its = 0, 0.0, 0
+        while dt < args.cpu_seconds and its < 5000:
+            d, _, t = smp.iteration()
+            dec, dt, its = dec + d, dt + t, its + 1
+        line["cpu_baseline"] = {"value": dec / dt, "unit": "ant-steps/s", "cores": 1, "kind": "reference",
+                                "cpu_model": cpu_model(),
+                                "sample": f"{its} reference sequential_step calls ({args.algorithm}, "
+                                          f"{args.config.upper()}), {dt:.1f} s; ant-step = one routing decision"}
     eng.close()
     emit(line)
     if dist:

@@ -127,6 +127,7 @@ def ref_lib():
         _sig(L, "ref_deposit_amount", i64, i64, P(abi.PheromoneParams))
         _sig(L, "ref_fold_maco_edge", i64, i64, P(i32), i32, i64, P(abi.PheromoneParams))
         _sig(L, "ref_apply_maco_update", C.c_int, P(i64), i32, i32, P(abi.PheromoneParams))
+        _sig(L, "ref_fold_bench", f64, P(i64), i32, P(i32), i32, i32, i32, P(abi.PheromoneParams))
         _sig(L, "ref_init_random", C.c_int, P(abi.GraphDesc), P(abi.PheromoneParams), u64, P(i64))
         _sig(L, "ref_select_phase", C.c_int, C.c_int, P(i32), P(f64), C.c_int, P(abi.SignalParams))
         _sig(L, "ref_discharge", C.c_int, i32, P(f64), f64, C.c_int, P(abi.SignalParams))
@@ -361,6 +362,17 @@ class RefWorld(_WorldBase):
         routes = i64()
         steps = self.L.ref_world_colony_iteration(self.h, ants, threads, C.byref(routes))
         return steps, routes.value
+
+
+def ref_fold_bench(tau, dec_edge, iters, threads, params):
+    """Seconds for `iters` passes of the reference's F+G edge kernel
+    (evaporate_one(fold_maco_edge(...)) per edge, parallel.cpp:195-231) over
+    `tau` (updated in place) on `threads` std::threads."""
+    L = ref_lib()
+    t = np.ascontiguousarray(tau, dtype=np.int64)
+    d = np.ascontiguousarray(dec_edge, dtype=np.int32)
+    sec = L.ref_fold_bench(abi.ptr(t, i64), len(t), abi.ptr(d, i32), len(d), iters, threads, C.byref(params))
+    return sec, t
 
 
 def ref_run(net, cfg, workers=0):

@@ -323,6 +323,40 @@ int64_t ref_fold_maco_edge(int64_t tau, const int32_t* positions, int32_t n, int
                            const gmaco_pheromone_params* p) {
   return fold_maco_edge(tau, std::span<const std::int32_t>(positions, n), total, to_pheromone(p));
 }
+// Stage F+G edge kernel of the reference's parallel executor
+// (commit_pheromone, parallel.cpp:195-231): per edge,
+// evaporate_one(fold_maco_edge(tau, positions of its decisions, D)), edges
+// split over `threads` std::threads in contiguous ranges (partition_entities,
+// parallel.cpp:8-21).  dec_edge[D] lists the step's decisions in vid order.
+// Runs `iters` passes over tau (in place) and returns the seconds they took
+// (edge-updates/s = m * iters / seconds).
+double ref_fold_bench(int64_t* tau, int32_t m, const int32_t* dec_edge, int32_t D, int32_t iters,
+                      int32_t threads, const gmaco_pheromone_params* p) {
+  const PheromoneParams pp = to_pheromone(p);
+  std::vector<int32_t> start(m + 1, 0), pos(D);
+  for (int32_t i = 0; i < D; ++i) start[dec_edge[i] + 1]++;
+  for (int32_t e = 0; e < m; ++e) start[e + 1] += start[e];
+  std::vector<int32_t> fill(start.begin(), start.end() - 1);
+  for (int32_t i = 0; i < D; ++i) pos[fill[dec_edge[i]]++] = i;  // ascending position per edge
+  if (threads < 1) threads = 1;
+  auto ranges = partition_entities(m, threads);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int32_t it = 0; it < iters; ++it) {
+    auto work = [&](int t) {
+      for (int32_t e = ranges[t].begin; e < ranges[t].end; ++e)
+        tau[e] = evaporate_one(fold_maco_edge(tau[e], std::span<const std::int32_t>(pos.data() + start[e],
+                                                                                     start[e + 1] - start[e]),
+                                              D, pp),
+                               pp);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 int ref_apply_maco_update(int64_t* tau, int32_t m, int32_t chosen, const gmaco_pheromone_params* p) {
   GUARD({
     std::vector<TauMicros> t(tau, tau + m);

@@ -151,6 +151,7 @@ struct DevVehicles {
   int32_t* dec_next;  // this step's decision stack link (MACO fold)
   int32_t* dflag;     // decided this step (MACO positions)
   int32_t* pos;       // exclusive prefix of dflag = decision position
+  int32_t* bsum;      // [cooperative tail blocks] decisions per tail block's vehicle chunk (pos scan)
   int32_t *path, *path_n;       // realized path (slots), [V * path_cap]
   int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
   int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)

@@ -1341,6 +1341,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     h->res.scan_temp = B.alloc<char>(h->res.scan_temp_bytes);
   }
   h->res.coop_blocks = coop_tail_blocks(w, h->device);
+  if (p.need_positions) dv.bsum = B.alloc<int32_t>(std::max(h->res.coop_blocks, 1));
   // stages C, D, E1 beside the lattice walk (DevParams::e1_in_walk): needs the
   // cooperative colony tail, which then runs E3 and the kReleased fix-up
   p.e1_in_walk = lattice_walker && S > 0 && h->res.coop_blocks > 0 && !p.need_positions &&

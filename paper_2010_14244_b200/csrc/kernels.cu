@@ -2663,6 +2663,21 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     if (gtid == 0) finalize_step(w);
     return;
   }
+  // Network-wide MACO fold (fold_maco_edge, parallel.cpp:77-92): every
+  // decision's position in ascending-vid order is the exclusive prefix of
+  // dflag (set by stage B).  Block b scans the contiguous vehicle chunk
+  // [c0, c1): its count is published before the first grid barrier, its
+  // positions written before the second (F+G reads them after the third) --
+  // no extra barrier and no library scan.
+  const bool pos_scan = p.need_positions;
+  const int64_t chunk = (p.V + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = min((int64_t)p.V, (int64_t)blockIdx.x * chunk), c1 = min((int64_t)p.V, c0 + chunk);
+  if (pos_scan) {
+    long long cnt = 0;
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) cnt += w.v.dflag[i];
+    cnt = block_sum(cnt, red);
+    if (threadIdx.x == 0) w.v.bsum[blockIdx.x] = (int32_t)cnt;
+  }
   // C, D, E1 (signals) || E2 (vehicles)
   long long qt = 0, active = 0, unfinished = 0;
   for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
@@ -2682,6 +2697,33 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   grid.sync();
   // E3
   for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
+  if (pos_scan) {  // positions of this block's chunk (block-uniform loop bounds)
+    long long off = 0;
+    for (int64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += w.v.bsum[b];
+    off = block_sum(off, red);
+    __shared__ long long s_off;
+    __shared__ int32_t wsum[kTailCoop / 32];
+    if (threadIdx.x == 0) s_off = off;
+    __syncthreads();
+    long long base = s_off;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
+      const int64_t i = t0 + threadIdx.x;
+      const int32_t f = i < c1 ? w.v.dflag[i] : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+      if (lane == 0) wsum[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int k = 0; k < kTailCoop / 32; ++k) {
+        before += k < wid ? wsum[k] : 0;
+        total += wsum[k];
+      }
+      if (i < c1) w.v.pos[i] = (int32_t)(base + before + __popc(bal & ((1u << lane) - 1u)));
+      base += total;
+      __syncthreads();
+    }
+  }
   if (p.siblings_only && (p.algorithm == 2 || p.algorithm == 3)) {
     grid.sync();
     for (int64_t u = gtid; u < w.g.n; u += gstride) node_scoped(w, (int32_t)u);
@@ -3280,13 +3322,13 @@ tail:
       cudaError_t e = r.exchange(r.exchange_ctx, st);
       if (e != cudaSuccess) return e;
     }
-    const bool coop_tail = r.coop_blocks > 0 && !w.p.need_positions;
+    const bool coop_tail = r.coop_blocks > 0;
     if (fused && !coop_tail)  // (the cooperative tail applies remote vehicles itself)
       k_apply_remote_move<<<blocks_for(V, 256), 256, 0, st>>>(w);
     else if (!fused)
       k_apply_remote<<<blocks_for(V, 256), 256, 0, st>>>(w);
   }
-  if (r.coop_blocks > 0 && !w.p.need_positions) {
+  if (r.coop_blocks > 0) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(r.coop_blocks);
     lc.blockDim = dim3(kTailCoop);
@@ -3325,9 +3367,9 @@ int kernels_per_step(const DevWorld& w, const StepResources& r) {
   int k = 1;                 // stage-B walk / decide
   if (w.p.ant_queue) k += 2; // k_colony_pro + k_colony_epi around k_colony_q
   if (w.tt.rec) k += 1;      // k_tt_refresh
-  if (w.p.sharded && !(w.p.algorithm == 4 && r.coop_blocks > 0 && !w.p.need_positions))
+  if (w.p.sharded && !(w.p.algorithm == 4 && r.coop_blocks > 0))
     k += 1;  // k_apply_remote[_move] (folded into the cooperative colony tail otherwise)
-  if (r.coop_blocks > 0 && !w.p.need_positions) return k + 1;  // k_tail_coop
+  if (r.coop_blocks > 0) return k + 1;  // k_tail_coop
   if (w.p.S > 0) k += 2;     // k_signals, k_e3
   if (w.p.algorithm != 4) k += 1;  // k_move (colony walks run E2 themselves)
   if ((w.p.algorithm == 2 || w.p.algorithm == 3) && w.p.siblings_only) k += 1;  // k_scoped
