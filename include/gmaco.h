@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GMACO_ABI_VERSION 1
+#define GMACO_ABI_VERSION 2
 
 enum gmaco_status { GMACO_OK = 0, GMACO_EVALIDATION = 1, GMACO_ERUNTIME = 2 };
 
@@ -99,6 +99,29 @@ typedef struct {
   int32_t replan_all;             /* 1: every active vehicle's colony runs every iteration */
 } gmaco_colony_params;
 
+/* Engine implementation switches.  None changes the simulation: every
+ * setting gives bit-identical results (the parity tests pin each path).
+ * Zero-initialised = the production configuration.  They exist for A/B
+ * measurements and for tests that exercise each alternative kernel path. */
+enum gmaco_option_bits {
+  GMACO_OPT_NO_QUEUE = 1u << 0,       /* general graphs: CTA-per-vehicles walker instead of the ant queue */
+  GMACO_OPT_NO_SCRATCH = 1u << 1,     /* replay the winner's tour instead of keeping every ant's tour */
+  GMACO_OPT_NO_TT = 1u << 2,          /* no per-target candidate rows (shared slot records + filter bitmaps) */
+  GMACO_OPT_NO_ORDER = 1u << 3,       /* no walk-length / destination-major walk order */
+  GMACO_OPT_NO_PREFETCH = 1u << 4,    /* no bulk L2 prefetch CTA */
+  GMACO_OPT_NO_PDL = 1u << 5,         /* tail not launched as a programmatic dependent of the walk */
+  GMACO_OPT_NO_SMEM = 1u << 6,        /* lattice walker reads its tables from global memory */
+  GMACO_OPT_NO_BITS = 1u << 7,        /* lattice tours kept as slots instead of per-hop move bits */
+  GMACO_OPT_NO_E1_WALK = 1u << 8,     /* signal stages C, D, E1 in the tail instead of beside the walk */
+  GMACO_OPT_NATURAL_ROWS = 1u << 9,   /* aligned-CSR rows in node order instead of BFS order */
+  GMACO_OPT_PROFILE_CREATE = 1u << 10 /* print gmaco_create phase times to stderr */
+};
+typedef struct {
+  uint32_t flags;    /* gmaco_option_bits */
+  int32_t _pad;
+  double sssp_delta; /* device SSSP near/far step, in mean edge lengths (0 = default 32) */
+} gmaco_engine_options;
+
 /* SimConfig, engine.hpp:29-50 (network / distance passed separately). */
 typedef struct {
   int32_t algorithm;  /* gmaco_algorithm */
@@ -120,6 +143,7 @@ typedef struct {
   gmaco_signal_params signal;
   gmaco_routing_params routing;
   gmaco_colony_params colony;
+  gmaco_engine_options options; /* not in SimConfig: implementation switches, zero = production */
 } gmaco_sim_config;
 
 /* Road network as SoA: RoadNode / RoadEdge (net.hpp:29-43).  Edge i has id i;

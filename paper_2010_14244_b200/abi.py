@@ -63,6 +63,15 @@ class ColonyParams(C.Structure):
     ]
 
 
+# gmaco_option_bits: implementation switches, results bit-identical (gmaco.h)
+(OPT_NO_QUEUE, OPT_NO_SCRATCH, OPT_NO_TT, OPT_NO_ORDER, OPT_NO_PREFETCH, OPT_NO_PDL, OPT_NO_SMEM, OPT_NO_BITS,
+ OPT_NO_E1_WALK, OPT_NATURAL_ROWS, OPT_PROFILE_CREATE) = (1 << i for i in range(11))
+
+
+class EngineOptions(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("_pad", C.c_int32), ("sssp_delta", C.c_double)]
+
+
 class SimConfig(C.Structure):
     _fields_ = [
         ("algorithm", C.c_int32), ("controller", C.c_int32), ("vehicle_count", C.c_int32),
@@ -73,7 +82,7 @@ class SimConfig(C.Structure):
         ("od_block_a_len", C.c_int32), ("od_block_b_len", C.c_int32),
         ("speed_min_mps", C.c_double), ("speed_max_mps", C.c_double),
         ("pheromone", PheromoneParams), ("signal", SignalParams), ("routing", RoutingParams),
-        ("colony", ColonyParams),
+        ("colony", ColonyParams), ("options", EngineOptions),
     ]
 
 

@@ -138,6 +138,8 @@ void build_graph(const gmaco_graph_desc* d, HostGraph& g) {
 void validate_config(const gmaco_sim_config* c) {
   if (!c) throw ValidationError("config is null");
   if (c->vehicle_count < 1) throw ValidationError("config: vehicle_count must be >= 1");
+  if (c->options.flags >> 11) throw ValidationError("options: unknown flag bits");
+  if (!(c->options.sssp_delta >= 0)) throw ValidationError("options: sssp_delta must be >= 0");
   if (!(c->dt_s > 0)) throw ValidationError("config: dt must be positive");
   if (c->max_steps < 0) throw ValidationError("config: max_steps must be >= 0");
   if (c->decision_latency_s < 0) throw ValidationError("config: decision_latency_s must be >= 0");
@@ -203,9 +205,9 @@ void reverse_csr(const HostGraph& g, std::vector<int32_t>& rptr, std::vector<int
   }
 }
 
-// ---- create-phase profiler (GMACO_CREATE_PROFILE=1 prints to stderr) -------
+// ---- create-phase profiler (options.flags & GMACO_OPT_PROFILE_CREATE prints to stderr)
 struct PhaseTimer {
-  bool on = std::getenv("GMACO_CREATE_PROFILE") != nullptr;
+  bool on = false;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   void mark(const char* what) {
     if (!on) return;
@@ -732,6 +734,7 @@ int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::v
   const size_t total = (size_t)T * n;
   if (total >= (size_t(1) << 32)) throw ValidationError("distance table exceeds 2^32 entries");
   PhaseTimer pt;
+  pt.on = (h->cfg.options.flags & GMACO_OPT_PROFILE_CREATE) != 0;
   DevBuffers& B = h->buf;
   std::vector<int32_t> rp, rs, re;
   reverse_csr(g, rp, rs, re);
@@ -758,7 +761,7 @@ int64_t* device_distance_table(gmaco_engine* h, const HostGraph& g, const std::v
   // near/far threshold step: a few mean edge lengths (GMACO_SSSP_DELTA overrides, in edge lengths)
   int64_t lsum = 0;
   for (int32_t e = 0; e < g.m; ++e) lsum += g.len[e];
-  const double mult = std::getenv("GMACO_SSSP_DELTA") ? std::atof(std::getenv("GMACO_SSSP_DELTA")) : 32.0;
+  const double mult = h->cfg.options.sssp_delta > 0 ? h->cfg.options.sssp_delta : 32.0;
   const int64_t delta = std::max<int64_t>(1, (int64_t)(mult * (double)lsum / std::max(1, g.m)));
   CK(cudaMemsetAsync(cnt, 0, 16, h->stream));
   CK(sssp_run_coop(a, q, cnt, (uint32_t)T, delta, h->device, h->stream));
@@ -828,6 +831,7 @@ static void build_target_rows(gmaco_engine* h, const std::vector<int32_t>& place
 void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distance_desc* dd,
                  const gmaco_sim_config* cfg) {
   PhaseTimer pt0;
+  pt0.on = cfg && (cfg->options.flags & GMACO_OPT_PROFILE_CREATE) != 0;
   build_graph(gd, h->g);
   validate_config(cfg);
   pt0.mark("graph + config validation");
@@ -845,6 +849,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   B.arena = true;  // sub-allocate + shadow small arrays; sealed (one copy per chunk) below
   DevWorld& w = h->w;
   PhaseTimer pt;
+  pt.on = pt0.on;
 
   // ---- distance service ---------------------------------------------------
   DistHost dh;
@@ -939,8 +944,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   std::vector<int32_t> place(n);
   for (int32_t u = 0; u < n; ++u) place[u] = u;
   if (align4) {
-    const char* ro = std::getenv("GMACO_ROW_ORDER");
-    if (!(ro && std::string(ro) == "none")) {
+    if (!(c.options.flags & GMACO_OPT_NATURAL_ROWS)) {
       std::vector<char> seen(n, 0);
       int32_t qh = 0, qt = 0;
       for (int32_t r = 0; r < n; ++r) {
@@ -1083,10 +1087,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   {
     const int64_t Q = (int64_t)S * kPhases;
     const int64_t tail_bytes = (int64_t)V * 77 + Q * 32 + (int64_t)S * 40 + (int64_t)M * 48;
-    p.prefetch = !std::getenv("GMACO_NO_PREFETCH") && tail_bytes <= (int64_t(48) << 20) ? 1 : 0;
+    p.prefetch = !(c.options.flags & GMACO_OPT_NO_PREFETCH) && tail_bytes <= (int64_t(48) << 20) ? 1 : 0;
   }
-  p.pdl = std::getenv("GMACO_NO_PDL") ? 0 : 1;
-  p.no_smem = std::getenv("GMACO_NO_SMEM") ? 1 : 0;
+  p.pdl = (c.options.flags & GMACO_OPT_NO_PDL) ? 0 : 1;
+  p.no_smem = (c.options.flags & GMACO_OPT_NO_SMEM) ? 1 : 0;
   p.max_degree = maxdeg;
   // general-graph colony walker: progress-filter bitmaps + next-row
   // descriptors replace the per-hop neighbour distance gathers
@@ -1142,8 +1146,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // move bits: 1 bit per hop in 64-hop SMEM words per ant, when a CTA's
   // words fit 48 KB (lattice CTAs hold <= 256 ants)
   p.bit_words = (p.plan_cap + 63) / 64;
-  p.grid_bits = lattice_walker && (size_t)256 * p.bit_words * 8 <= (size_t(48) << 10) && !std::getenv("GMACO_NO_BITS");
-  p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits && !std::getenv("GMACO_NO_SCRATCH") &&
+  p.grid_bits = lattice_walker && (size_t)256 * p.bit_words * 8 <= (size_t(48) << 10) && !(c.options.flags & GMACO_OPT_NO_BITS);
+  p.scratch_mode = alg == GMACO_COLONY && !p.grid_bits && !(c.options.flags & GMACO_OPT_NO_SCRATCH) &&
                    (size_t)V * p.ants * p.plan_cap * 4 <= (size_t(48) << 30);
   if (alg == GMACO_COLONY) {  // packed (cost, ant) argmin key bound
     int64_t maxlen = 0;
@@ -1244,7 +1248,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   dv.plan = B.alloc<int32_t>(p.scratch_mode ? 1 : (size_t)V * p.plan_cap);
   dv.scratch = B.alloc<int32_t>(p.scratch_mode ? (size_t)V * p.ants * p.plan_cap : 1);
   dv.plan_ant = B.filled<int32_t>(V, 0);
-  if (lattice_walker && !std::getenv("GMACO_NO_ORDER")) {
+  if (lattice_walker && !(c.options.flags & GMACO_OPT_NO_ORDER)) {
     // Walk-length balance: vehicles sorted by origin->destination Manhattan
     // distance, dealt round-robin over the CTAs so every CTA (and SM) holds a
     // mix of long and short colonies; results do not depend on the order.
@@ -1276,7 +1280,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     }
     if (ok) dv.walk_order = B.upload(order);
   }
-  p.ant_queue = p.csr_walker && p.scratch_mode && !std::getenv("GMACO_NO_QUEUE") && (ell == 8 || align4);
+  p.ant_queue = p.csr_walker && p.scratch_mode && !(c.options.flags & GMACO_OPT_NO_QUEUE) && (ell == 8 || align4);
   if (p.ant_queue) {
     // slot records {weight (double), int32 edge cost, head row (first/4) << 5 | degree};
     // weight and cost are (re)written by sync_rec_weights and stage F+G
@@ -1295,9 +1299,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     dv.best_key = B.filled<unsigned long long>(V, ~0ull);
     dv.walkers = B.filled<int32_t>(V, 0);
     dv.ant_hops = B.filled<int32_t>((size_t)V * p.ants, 0);
-    if (dd->kind == GMACO_DIST_TARGETS && maxdeg <= 15 && !std::getenv("GMACO_NO_TT"))
+    if (dd->kind == GMACO_DIST_TARGETS && maxdeg <= 15 && !(c.options.flags & GMACO_OPT_NO_TT))
       build_target_rows(h, place, (int32_t)targets.size());
-    if (!std::getenv("GMACO_NO_ORDER")) {
+    if (!(c.options.flags & GMACO_OPT_NO_ORDER)) {
       // Walk order for the queue: destination-major (the vehicles walking at
       // any moment share a few targets' rows, and their paths converge on
       // them, so those rows stay in L2), then by the origin's row position.
@@ -1345,7 +1349,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // stages C, D, E1 beside the lattice walk (DevParams::e1_in_walk): needs the
   // cooperative colony tail, which then runs E3 and the kReleased fix-up
   p.e1_in_walk = lattice_walker && S > 0 && h->res.coop_blocks > 0 && !p.need_positions &&
-                 !std::getenv("GMACO_NO_E1_WALK");
+                 !(c.options.flags & GMACO_OPT_NO_E1_WALK);
   if (p.e1_in_walk) {
     dv.rel = B.alloc<int32_t>(V);
     ds.qlen_e1 = B.filled<int32_t>((size_t)S * kPhases, 0);

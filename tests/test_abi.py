@@ -3,6 +3,7 @@ loads, exports every declared entry point, rejects invalid input with the
 reference's validation messages (status 1, before any device work) and
 fails loudly (status 2) when no CUDA device exists — there is no CPU path."""
 import ctypes as C
+import os
 import subprocess
 
 import numpy as np
@@ -10,6 +11,8 @@ import pytest
 
 from oracle import oracle as O
 from paper_2010_14244_b200 import abi, engine, networks
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -25,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert engine.load().gmaco_abi_version() == 1
+    assert engine.load().gmaco_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
@@ -34,7 +37,8 @@ def test_struct_layouts_match_header():
     assert C.sizeof(abi.SignalParams) == 64
     assert C.sizeof(abi.RoutingParams) == 32
     assert C.sizeof(abi.ColonyParams) == 32
-    assert C.sizeof(abi.SimConfig) == 304
+    assert C.sizeof(abi.EngineOptions) == 16
+    assert C.sizeof(abi.SimConfig) == 320
     assert C.sizeof(abi.RunResult) == 56
 
 
@@ -128,3 +132,25 @@ def test_null_arguments_are_rejected():
     L = engine.load()
     assert L.gmaco_step(None, 1, None) == abi.EVALIDATION
     assert L.gmaco_create(None, None, None, 0, None) == abi.EVALIDATION
+
+
+def test_struct_layouts_match_the_c_compiler(tmp_path):
+    """ctypes mirrors (abi.py) against the header as gcc lays it out."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    structs = {"gmaco_pheromone_params": abi.PheromoneParams, "gmaco_signal_params": abi.SignalParams,
+               "gmaco_routing_params": abi.RoutingParams, "gmaco_colony_params": abi.ColonyParams,
+               "gmaco_engine_options": abi.EngineOptions, "gmaco_sim_config": abi.SimConfig,
+               "gmaco_graph_desc": abi.GraphDesc, "gmaco_distance_desc": abi.DistanceDesc,
+               "gmaco_run_result": abi.RunResult, "gmaco_vehicle_view": abi.VehicleView,
+               "gmaco_signal_view": abi.SignalView, "gmaco_counters": abi.Counters}
+    src = tmp_path / "sz.c"
+    body = "".join(f'  printf("%zu\\n", sizeof({k}));\n' for k in structs)
+    src.write_text(f'#include <stdio.h>\n#include "gmaco.h"\nint main(void) {{\n{body}  return 0;\n}}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    for (name, st), n in zip(structs.items(), sizes):
+        assert C.sizeof(st) == n, name

@@ -296,18 +296,15 @@ def _rgg_targets(nodes, targets, seed):
 
 
 @pytest.mark.parametrize("mode", ["queue", "block", "replay"])
-def test_colony_rgg_targets_csr_walker(mode, monkeypatch):
+def test_colony_rgg_targets_csr_walker(mode):
     """C4's path at small scale: random-geometric graph (CSR rows, degree up
     to ~9 -> the MAXD=16 general walker), TARGETS distance tables, long
     multi-hop tours.  queue = persistent ant-queue walker (the default in
     scratch mode), block = one-CTA-per-vehicles walker with scratch tours,
     replay = winner replay; all bit-exact."""
-    if mode == "replay":
-        monkeypatch.setenv("GMACO_NO_SCRATCH", "1")
-    if mode == "block":
-        monkeypatch.setenv("GMACO_NO_QUEUE", "1")
     net, dist, tgt = _rgg_targets(3000, 12, 77)
     cfg = abi.colony_production(_cfg("colony", 400, 5, max_steps=40), ants=16)
+    cfg.options.flags = {"queue": 0, "block": abi.OPT_NO_QUEUE, "replay": abi.OPT_NO_SCRATCH}[mode]
     cfg.colony.max_hops = 512
     gpu = Engine(net, cfg, dist)
     cpu = O.PortWorld(net, cfg, dist)
@@ -324,17 +321,18 @@ def test_colony_rgg_targets_csr_walker(mode, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["bitmap_queue", "odd_ants", "cost_over_int32", "length_over_int32"])
-def test_colony_rgg_targets_walker_variants(variant, monkeypatch):
+def test_colony_rgg_targets_walker_variants(variant):
     """Paths around the per-target-row walker (k_colony_qt), all bit-exact:
-    bitmap_queue = the shared-row queue walker (GMACO_NO_TT); odd_ants = 12
+    bitmap_queue = the shared-row queue walker (OPT_NO_TT); odd_ants = 12
     ants (lanes fetch single ants, no 16-lane groups); cost_over_int32 =
     edge costs len*(1+load) beyond 2^31 (the int32 record cost's -1 escape to
     the int64 table); length_over_int32 = edge lengths beyond 2^31 mm (no
     {slot, length} epilogue map)."""
     net, dist, tgt = _rgg_targets(2500, 10, 19)
     ants = 16
+    flags = 0
     if variant == "bitmap_queue":
-        monkeypatch.setenv("GMACO_NO_TT", "1")
+        flags = abi.OPT_NO_TT
     elif variant == "odd_ants":
         ants = 12
     elif variant == "cost_over_int32":
@@ -343,6 +341,7 @@ def test_colony_rgg_targets_walker_variants(variant, monkeypatch):
         net.edge_length_mm = net.edge_length_mm * 60000  # some lengths >= 2^31 mm
         assert net.edge_length_mm.max() >= 2 ** 31
     cfg = abi.colony_production(_cfg("colony", 600, 9, max_steps=30), ants=ants)
+    cfg.options.flags = flags
     cfg.colony.max_hops = 400
     gpu = Engine(net, cfg, dist)
     cpu = O.PortWorld(net, cfg, dist)
@@ -444,18 +443,15 @@ def _hub_graph(hub_degree, seed=5):
 
 
 @pytest.mark.parametrize("hub_degree,mode", [(14, "queue"), (14, "block"), (14, "replay"), (20, "generic")])
-def test_colony_wide_rows(hub_degree, mode, monkeypatch):
+def test_colony_wide_rows(hub_degree, mode):
     """Rows wider than the queue walker's 8-slot register window (span 16 on
     the 4-aligned CSR layout) and, at degree 20, beyond the CSR walkers'
     16-slot bound (generic kernel); dense distance tables."""
-    if mode == "replay":
-        monkeypatch.setenv("GMACO_NO_SCRATCH", "1")
-    if mode == "block":
-        monkeypatch.setenv("GMACO_NO_QUEUE", "1")
     net = _hub_graph(hub_degree)
     maxdeg = np.bincount(net.edge_from).max()
     assert (8 < maxdeg <= 16) if hub_degree <= 16 else maxdeg > 16
     cfg = abi.colony_production(_cfg("colony", 300, 23, max_steps=40), ants=32)
+    cfg.options.flags = {"replay": abi.OPT_NO_SCRATCH, "block": abi.OPT_NO_QUEUE}.get(mode, 0)
     gpu = Engine(net, cfg)
     cpu = O.PortWorld(net, cfg)
     for k in (1, 3, 8):

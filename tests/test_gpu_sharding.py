@@ -97,35 +97,34 @@ def test_nccl_exchange_world1_equals_unsharded():
 
 
 def _walker_world(kind):
-    """(net, cfg, dist factory, env) per stage-B walker kind."""
+    """(net, cfg, dist factory) per stage-B walker kind."""
     from test_gpu_parity import _hub_graph, _rgg_targets
     prod = lambda V, ants, steps: abi.colony_production(abi.default_config(
         algorithm="colony", controller="preemptive", vehicle_count=V, seed=9, max_steps=steps), ants=ants)
     if kind == "lattice-multiword":
         net = networks.grid(40, 40, signals="interior")
-        return net, prod(240, 64, 30), net.grid_distance, {}
+        return net, prod(240, 64, 30), net.grid_distance
     if kind in ("queue", "block"):
         net, _, tgt = _rgg_targets(3000, 12, 77)
         cfg = prod(300, 16, 30)
         cfg.colony.max_hops = 512
+        cfg.options.flags = abi.OPT_NO_QUEUE if kind == "block" else 0
         make = lambda: abi.DistanceDesc(kind=abi.DIST_TARGETS, targets=abi.ptr(tgt, __import__("ctypes").c_int32),
                                         target_count=len(tgt))
-        return net, cfg, make, ({"GMACO_NO_QUEUE": "1"} if kind == "block" else {}), tgt
+        return net, cfg, make, tgt
     if kind == "generic":
         net = _hub_graph(20)
-        return net, prod(200, 32, 30), lambda: abi.DistanceDesc(kind=abi.DIST_DENSE), {}
+        return net, prod(200, 32, 30), lambda: abi.DistanceDesc(kind=abi.DIST_DENSE)
     raise ValueError(kind)
 
 
 @pytest.mark.parametrize("kind", ["lattice-multiword", "queue", "block", "generic"])
-def test_host_mediated_shards_every_walker(kind, monkeypatch):
+def test_host_mediated_shards_every_walker(kind):
     """Sharded stage B on each walker (prologue / queue / epilogue decision
     records included) equals the unsharded engine, step by step."""
     spec = _walker_world(kind)
-    net, cfg, dist, env = spec[:4]
-    keep = spec[4:]  # target arrays referenced by the descriptors
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    net, cfg, dist = spec[:3]
+    keep = spec[3:]  # target arrays referenced by the descriptors
     single = Engine(net, cfg, dist())
     shards = []
     for r in range(3):
