@@ -515,6 +515,41 @@ def build_workload(args, world):
     return workloads.CONFIGS[args.config](seed=1, max_steps=max_steps)
 
 
+def rank_breakdown(me, dist, world, vehicles, net, cfg):
+    """Per-rank timings gathered on rank 0: walk = stage B on the rank's
+    shard; exchange_and_tail = the in-graph NCCL exchange (decision-record
+    allgather + deposit allreduce) plus the replicated tail.
+    exchange_probe_ms times the same two collectives alone through
+    torch.distributed on the same sizes.  Diagnosis only: a failure here is
+    recorded, never raised."""
+    import torch
+    from paper_2010_14244_b200 import abi
+    try:
+        P = -(-vehicles // world)
+        dec = torch.zeros(P, dtype=torch.int32, device="cuda")
+        gat = torch.zeros(P * world, dtype=torch.int32, device="cuda")
+        dep = torch.zeros(net.edge_count, dtype=torch.int64, device="cuda")
+        needs_dep = cfg.algorithm == abi.COLONY and cfg.colony.deposit == abi.DEPOSIT_BEST_TOUR
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        for it in range(13):
+            if it == 3:
+                torch.cuda.synchronize()
+                dist.barrier()
+                ev0.record()
+            dist.all_gather_into_tensor(gat, dec)
+            if needs_dep:
+                dist.all_reduce(dep)
+        ev1.record()
+        torch.cuda.synchronize()
+        me["exchange_probe_ms"] = ev0.elapsed_time(ev1) / 10
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+        return ranks
+    except Exception as exc:  # noqa: BLE001
+        return [dict(me, breakdown_error=repr(exc))]
+
+
 def run_ours(args, rank, world, local):
     import ctypes as C
 
@@ -635,6 +670,11 @@ def run_ours(args, rank, world, local):
         completed = res[0].completed_count
         e.close()
 
+    # ---- per-rank breakdown (diagnosis of a scaling run) -------------------------
+    me = {"rank": rank, "walk_ms": walk_ms / args.steps, "step_ms": step_ms / args.steps,
+          "exchange_and_tail_ms": (step_ms - walk_ms) / args.steps, "ant_steps": ant_steps}
+    ranks = rank_breakdown(me, dist, world, vehicles, net, cfg0) if dist and world > 1 else [me]
+
     # ---- reduce over ranks (time: max; work: sum) ------------------------------
     vals = torch.tensor([step_ms / 1e3, e2e_dt, chained_s, walk_ms], dtype=torch.float64, device="cuda")
     tot = torch.tensor([ant_steps, routes, e2e_steps, chained_steps], dtype=torch.float64, device="cuda")
@@ -707,6 +747,7 @@ def run_ours(args, rank, world, local):
                                "engine, outside this timing)" if job_uid else ""),
                 "phases": e2e_phases},
         "clocks": clk.summary(),
+        "per_rank": ranks,
         "completed_vehicles_e2e": completed,
     }
     headline = args.algorithm == "colony" and args.config == "c2"

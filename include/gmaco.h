@@ -242,13 +242,17 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
 int gmaco_nccl_unique_id(void* out128);
 
 /* Host-mediated sharding (tests, or a caller with its own transport): this
- * engine plans vehicles [lo, hi) only.  Per step: gmaco_step_split(h, 1)
- * (stage B over the shard); gmaco_exchange_export (the shard's decision
- * records [hi-lo] — edge id taken, -1 none, -2 retired — and its best-tour
+ * engine plans vehicles [lo, hi) only (every algorithm: colonies, and the
+ * reference's dijkstra / aco / maco / maco-p, whose MACO fold is replicated
+ * from the exchanged decisions, parallel.cpp:195-258).  Per step:
+ * gmaco_step_split(h, 1) (stage B over the shard); gmaco_exchange_export (the
+ * shard's decision records [hi-lo] — edge id taken, with GMACO_REC_DEVIATED
+ * set for a MACO deviation, -1 none, -2 retired — and its best-tour
  * deposits per edge id [edge_count]); combine across shards (concatenate
  * the records in vehicle order, sum the deposits); gmaco_exchange_import
  * ([vehicle_count] records, [edge_count] deposit sums); then
  * gmaco_step_split(h, 2) (apply the remote decisions, stages C..G). */
+#define GMACO_REC_DEVIATED (1 << 30) /* decision record flag: a MACO deviation (RouteDecision::deviated) */
 int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi);
 int gmaco_step_split(gmaco_engine* h, int32_t part);
 int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits);

@@ -498,7 +498,7 @@ struct og_world {
   ivec dec_vid, dec_edge, completions, enq_vid;
   gmaco_counters ctr;
   int32_t vlo, vhi; /* planning range (sharded protocol) */
-  int32_t* dec_rec; /* this step's decision per vehicle: edge, -1 none, -2 retired */
+  int32_t* dec_rec; /* this step's decision per vehicle: edge (| GMACO_REC_DEVIATED), -1 none, -2 retired */
 };
 
 static void targets_sssp(og_world* w) { targets_sssp_run(&w->g, w->targets, w->ntargets, w->tdist); }
@@ -1068,14 +1068,17 @@ static void activate(og_world* w, int32_t vid) { /* engine.cpp:177-180 */
 
 static void decide(og_world* w, int32_t vid) { /* engine.cpp:175-217 */
   activate(w, vid);
+  if (vid < w->vlo || vid >= w->vhi) return; /* sharded: another shard decides (apply_remote) */
+  w->dec_rec[vid] = -1;
   if (w->state[vid] != GMACO_AT_NODE) return;
   int32_t next = -1;
   int dev = 0;
   int32_t e = route_one(w, w->cfg.algorithm, w->at_node[vid], w->dest[vid], (uint64_t)vid,
                         (uint64_t)w->step, w->active, 0, &next, &dev);
-  if (e < 0) { w->state[vid] = GMACO_RETIRED; return; }
+  if (e < 0) { w->state[vid] = GMACO_RETIRED; w->dec_rec[vid] = -2; return; }
   w->ctr.ant_steps++;
   take_edge(w, vid, e, dev);
+  w->dec_rec[vid] = e | (dev ? GMACO_REC_DEVIATED : 0);
 }
 
 /* Colony stage B (north-star extension): K ants per planning vehicle, best
@@ -1218,10 +1221,25 @@ static void aco_deposit_path(og_world* w, const int32_t* path, int32_t n, int64_
   for (int32_t i = 0; i < n; ++i) w->tau[path[i]] = i64min(w->tau[path[i]] + amount, hi);
 }
 
+/* The step's decisions in ascending vid (commit_pheromone's order,
+ * parallel.cpp:195-231).  A sharded world applied its own shard's decisions
+ * in stage B and the others' in apply_remote, so its lists are re-sorted. */
+static void decisions_in_vid_order(og_world* w) {
+  if (w->vlo == 0 && w->vhi == w->V) return;
+  int32_t* edge_of = malloc(sizeof(int32_t) * (size_t)(w->V ? w->V : 1));
+  for (int32_t v = 0; v < w->V; ++v) edge_of[v] = -1;
+  for (int32_t i = 0; i < w->dec_vid.n; ++i) edge_of[w->dec_vid.a[i]] = w->dec_edge.a[i];
+  int32_t k = 0;
+  for (int32_t v = 0; v < w->V; ++v)
+    if (edge_of[v] >= 0) { w->dec_vid.a[k] = v; w->dec_edge.a[k] = edge_of[v]; k++; }
+  free(edge_of);
+}
+
 static void pheromone_commit(og_world* w) { /* engine.cpp:326-350, parallel.cpp:195-258 */
   const gmaco_pheromone_params* p = &w->cfg.pheromone;
   const int alg = w->cfg.algorithm;
   if (alg == GMACO_MACO || alg == GMACO_MACO_P) {
+    decisions_in_vid_order(w);
     if (p->decrement_siblings_only) { /* apply_maco_update_scoped, pheromone.cpp:48-59 */
       const int64_t lo = min_u(p), hi = max_u(p), inc = inc_u(p), dec = dec_u(p);
       for (int32_t i = 0; i < w->dec_vid.n; ++i) {
@@ -1309,7 +1327,7 @@ static void apply_remote(og_world* w) {
   for (int32_t vid = 0; vid < w->V; ++vid) {
     if (vid >= w->vlo && vid < w->vhi) continue;
     const int32_t rec = w->dec_rec[vid];
-    if (rec >= 0) take_edge(w, vid, rec, 0);
+    if (rec >= 0) take_edge(w, vid, rec & ~GMACO_REC_DEVIATED, (rec & GMACO_REC_DEVIATED) != 0);
     else if (rec == -2) w->state[vid] = GMACO_RETIRED;
   }
 }

@@ -1597,18 +1597,38 @@ cudaError_t nccl_exchange(void* ctx, cudaStream_t st) {
   return (r == ncclSuccess && e == ncclSuccess) ? cudaSuccess : cudaErrorUnknown;
 }
 
+// Vehicle sharding (partition_entities ranges, parallel.cpp:8-21): this
+// engine decides / plans vehicles [lo, hi); every rank replays stages C..G for
+// the whole fleet from the exchanged decision records.  Every algorithm
+// shards: colonies, and the reference's dijkstra / aco / maco / maco-p, whose
+// network-wide MACO fold takes every decision's global position from the
+// records (commit_pheromone, parallel.cpp:195-258).
 void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
   DevWorld& w = h->w;
-  if (w.p.algorithm != GMACO_COLONY) throw ValidationError("sharding: only the colony algorithm shards vehicles");
   if (lo < 0 || hi > w.p.V || lo > hi) throw ValidationError("sharding: invalid vehicle range");
+  if (w.g.M >= GMACO_REC_DEVIATED || h->g.m >= GMACO_REC_DEVIATED)
+    throw ValidationError("sharding: decision records need fewer than 2^30 edges");
   if (pad_total > w.p.V) {  // allgather layout: world * shard_pad records
     int32_t* d = h->buf.filled<int32_t>(pad_total, -1);
     w.v.dec_rec = d;
   }
+  // the walk order (destination-major / walk-length balanced) restricted to
+  // the shard, in the same relative order: slot lo + i holds the shard's i-th
+  // vehicle of the full order, so a rank keeps the order's locality
+  if (w.v.walk_order) {
+    const int32_t V = w.p.V;
+    std::vector<int32_t> full = download(w.v.walk_order, V), mine(V, -1);
+    int32_t k = lo;
+    for (int32_t i = 0; i < V; ++i)
+      if (full[i] >= lo && full[i] < hi) mine[k++] = full[i];
+    int32_t* d = h->buf.alloc_direct<int32_t>(V);
+    CK(cudaMemcpyAsync(d, mine.data(), (size_t)V * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    w.v.walk_order = d;
+  }
   w.p.shard_lo = lo;
   w.p.shard_hi = hi;
   w.p.sharded = 1;
-  w.v.walk_order = nullptr;  // a rank walks exactly its own vehicle range
   h->reset_graphs();
 }
 
@@ -1730,7 +1750,8 @@ int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits
     if (decisions && hi > lo) {  // records at the boundary: edge id, -1 none, -2 retired
       CK(cudaMemcpy(decisions, w.v.dec_rec + lo, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost));
       for (int32_t i = 0; i < hi - lo; ++i)
-        if (decisions[i] >= 0) decisions[i] = h->slot_edge[decisions[i]];
+        if (decisions[i] >= 0)
+          decisions[i] = h->slot_edge[decisions[i] & ~GMACO_REC_DEVIATED] | (decisions[i] & GMACO_REC_DEVIATED);
     }
     if (deposits) scatter_slots(h, download(w.dep, h->M), deposits);
   });
@@ -1745,8 +1766,9 @@ int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64
       std::vector<int32_t> d(decisions, decisions + w.p.V);
       for (auto& x : d)
         if (x >= 0) {
-          if (x >= h->g.m) throw ValidationError("exchange_import: invalid edge id");
-          x = h->g.edge_slot[x];
+          const int32_t e = x & ~GMACO_REC_DEVIATED;
+          if (e >= h->g.m) throw ValidationError("exchange_import: invalid edge id");
+          x = h->g.edge_slot[e] | (x & GMACO_REC_DEVIATED);
         }
       h2d(h, w.v.dec_rec, d.data(), d.size() * 4);
     }

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "gmaco.h"
 #include "kernels.h"
 
 namespace gmaco {
@@ -368,7 +369,7 @@ __device__ __forceinline__ void flush_counters(DevCtl* c, const Sum5& t) {
 __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_t slot, bool deviated,
                                           int32_t from) {
   const DevVehicles& v = w.v;
-  if (w.p.sharded) v.dec_rec[vid] = slot;
+  if (w.p.sharded) v.dec_rec[vid] = slot | (deviated ? GMACO_REC_DEVIATED : 0);
   v.state[vid] = kOnEdge;
   v.on_edge[vid] = slot;
   v.progress[vid] = v.overshoot[vid];
@@ -400,11 +401,14 @@ __global__ void __launch_bounds__(256) k_decide(DevWorld w) {
   if (skip_step(w.ctl)) return;
   if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
   __shared__ long long red[32];
-  const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
+  // sharded: this rank decides vehicles [shard_lo, shard_hi); the others'
+  // records arrive with the exchange (k_apply_remote)
+  const int32_t vid = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t step = w.ctl->step;
   long long decided = 0, cands = 0, degs = 0;
-  if (vid < w.p.V) {
+  if (vid < w.p.shard_hi) {
     const DevVehicles& v = w.v;
+    if (w.p.sharded) v.dec_rec[vid] = -1;
     uint8_t st = v.state[vid];
     if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
       st = kAtNode;
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(256) k_decide(DevWorld w) {
       }
       if (slot < 0) {
         v.state[vid] = kRetired;  // engine.cpp:202-205
+        if (w.p.sharded) v.dec_rec[vid] = -2;
       } else {
         take_edge(w, vid, slot, dev, x);
         if (w.p.need_positions) v.dflag[vid] = 1;
@@ -2525,19 +2530,29 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
   if (skip_step(w.ctl)) return;
+  __shared__ long long red[32];
   const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (vid >= w.p.V || (vid >= w.p.shard_lo && vid < w.p.shard_hi)) return;
-  const DevVehicles& v = w.v;
-  const int64_t step = w.ctl->step;
-  if (v.state[vid] == kPending && v.depart[vid] == step) {
-    v.state[vid] = kAtNode;
-    v.at_node[vid] = v.origin[vid];
+  long long applied = 0;
+  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) {
+    const DevVehicles& v = w.v;
+    const int64_t step = w.ctl->step;
+    if (v.state[vid] == kPending && v.depart[vid] == step) {
+      v.state[vid] = kAtNode;
+      v.at_node[vid] = v.origin[vid];
+    }
+    const int32_t rec = v.dec_rec[vid];
+    if (rec >= 0) {
+      take_edge(w, vid, rec & ~GMACO_REC_DEVIATED, (rec & GMACO_REC_DEVIATED) != 0, v.at_node[vid]);
+      applied = 1;
+    } else if (rec == -2) {
+      v.state[vid] = kRetired;
+    }
+    // network-wide MACO fold: remote decisions take their positions too
+    if (w.p.need_positions) v.dflag[vid] = rec >= 0 ? 1 : 0;
   }
-  const int32_t rec = v.dec_rec[vid];
-  if (rec >= 0)
-    take_edge(w, vid, rec, false, v.at_node[vid]);
-  else if (rec == -2)
-    v.state[vid] = kRetired;
+  // the fold's decision total D (fold_maco_edge's total_decisions) is global
+  applied = block_sum(applied, red);
+  if (threadIdx.x == 0 && applied) atomicAdd((unsigned long long*)&w.ctl->dcount, (unsigned long long)applied);
 }
 
 // colony mode: a remote vehicle's decision, then its motion (E2) and the

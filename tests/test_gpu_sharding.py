@@ -168,3 +168,76 @@ def test_nccl_communicator_shared_by_engines_of_a_job():
     second.attach_comm(0, 1, uid.raw)  # reuses the job's communicator
     second.step(5)
     assert same(second, single) is None
+
+
+def ref_world(alg, V=301):
+    net = networks.grid(12, 12, signals="all")
+    cfg = abi.default_config(algorithm=alg.replace("-scoped", ""), vehicle_count=V, seed=5, max_steps=120)
+    cfg.routing.deviation_threshold = 150  # MACO deviations happen early on
+    cfg.pheromone.decrement_siblings_only = int(alg == "maco-scoped")
+    return net, cfg
+
+
+@pytest.mark.parametrize("alg", ["maco-p", "maco", "maco-scoped", "aco", "dijkstra"])
+def test_reference_algorithms_shard(alg):
+    """The reference's own algorithms sharded over 3 engines (k_decide over
+    the shard, decision records with the deviation flag exchanged,
+    k_apply_remote, replicated cooperative tail with the in-kernel position
+    scan over every rank's decisions) equal the unsharded engine step by
+    step and the unsharded oracle at the end."""
+    net, cfg = ref_world(alg)
+    single = Engine(net, cfg, net.grid_distance())
+    shards = []
+    for r in range(3):
+        e = Engine(net, cfg, net.grid_distance())
+        e.set_shard(*sharding.shard_bounds(cfg.vehicle_count, 3, r))
+        shards.append(e)
+    step = sharding.local_transport(shards)
+    for k in range(25):
+        step()
+        single.step(1)
+        for e in shards:
+            assert same(e, single) is None, (alg, k, same(e, single))
+    while not single.finished():
+        step()
+        single.step(1)
+    for e in shards:
+        assert e.finished() and e.current_step() == single.current_step()
+    assert sum(e.counters().decisions for e in shards) == single.counters().decisions
+    ref = O.PortWorld(net, cfg, net.grid_distance()).run()
+    assert O.results_identical(shards[1].collect(), ref)
+    if alg.startswith("maco"):
+        assert single.vehicles()["deviations"].sum() > 0
+
+
+def test_maco_p_mixed_engine_and_oracle_shards():
+    """Edge-id records (deviation flag included) cross the boundary between
+    a GPU shard and an oracle shard."""
+    net, cfg = ref_world("maco-p", V=200)
+    cpu_single = O.PortWorld(net, cfg, net.grid_distance())
+    g = Engine(net, cfg, net.grid_distance())
+    g.set_shard(*sharding.shard_bounds(200, 2, 0))
+    c = O.PortWorld(net, cfg, net.grid_distance())
+    c.set_shard(*sharding.shard_bounds(200, 2, 1))
+    step = sharding.local_transport([g, c])
+    for _ in range(20):
+        step()
+        cpu_single.step(1)
+    assert same(g, cpu_single) is None
+    assert same(c, cpu_single) is None
+
+
+def test_maco_p_nccl_exchange_world1_equals_unsharded():
+    from paper_2010_14244_b200 import engine
+    import ctypes as C
+    net = networks.grid(32, 32, signals="all")
+    cfg = abi.default_config(algorithm="maco-p", vehicle_count=1000, seed=3, max_steps=200)
+    uid = C.create_string_buffer(128)
+    assert engine.load().gmaco_nccl_unique_id(uid) == 0
+    e = Engine(net, cfg, net.grid_distance())
+    e.attach_comm(0, 1, uid.raw)
+    single = Engine(net, cfg, net.grid_distance())
+    e.step(40)
+    single.step(40)
+    assert same(e, single) is None
+    assert O.results_identical(e.run(), single.run())

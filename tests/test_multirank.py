@@ -1,6 +1,9 @@
-"""Multi-rank protocol on CPU: world_size-2 gloo run of the sharded colony
+"""Multi-rank protocol on CPU: world_size-2 gloo runs of the sharded world
 (oracle shards exchanging decision records and deposits through
-torch.distributed) must equal the unsharded world bit for bit."""
+torch.distributed) must equal the unsharded world bit for bit -- for GMACO-P
+colonies and for the reference's own algorithms, whose network-wide MACO
+fold is replicated on every rank from the exchanged decisions in global vid
+order (commit_pheromone, parallel.cpp:195-258)."""
 import hashlib
 import os
 import socket
@@ -17,10 +20,18 @@ from paper_2010_14244_b200 import abi, networks, sharding
 STEPS = 12
 
 
-def make_world():
+ALGS = ["colony", "maco-p", "maco", "maco-scoped", "aco", "dijkstra"]
+
+
+def make_world(alg="colony"):
     net = networks.grid(12, 12, signals="all")
-    cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive",
-                                                   vehicle_count=301, seed=5, max_steps=80), ants=16)
+    if alg == "colony":
+        cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive",
+                                                       vehicle_count=301, seed=5, max_steps=80), ants=16)
+    else:
+        cfg = abi.default_config(algorithm=alg.replace("-scoped", ""), vehicle_count=301, seed=5, max_steps=80)
+        cfg.routing.deviation_threshold = 150  # MACO deviations happen (n_t > threshold early on)
+        cfg.pheromone.decrement_siblings_only = int(alg == "maco-scoped")
     return net, cfg
 
 
@@ -37,11 +48,11 @@ def digest(w):
     return h.hexdigest()
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, alg):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    net, cfg = make_world()
+    net, cfg = make_world(alg)
     w = O.PortWorld(net, cfg, net.grid_distance())
     w.world_size = world
     w.set_shard(*sharding.shard_bounds(cfg.vehicle_count, world, rank))
@@ -70,14 +81,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_gloo_two_rank_sharded_colony_equals_single_world():
-    net, cfg = make_world()
+@pytest.mark.parametrize("alg", ["colony", "maco-p"])
+def test_gloo_two_rank_sharded_world_equals_single_world(alg):
+    net, cfg = make_world(alg)
     single = O.PortWorld(net, cfg, net.grid_distance())
     single.step(STEPS)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, alg)) for r in range(2)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]
@@ -94,8 +106,9 @@ def test_gloo_two_rank_sharded_colony_equals_single_world():
     assert sum(o[4] for o in out) == c.vehicle_routes
 
 
-def test_in_process_three_shards_equal_single_world():
-    net, cfg = make_world()
+@pytest.mark.parametrize("alg", ALGS)
+def test_in_process_three_shards_equal_single_world(alg):
+    net, cfg = make_world(alg)
     single = O.PortWorld(net, cfg, net.grid_distance())
     shards = []
     for r in range(3):
@@ -109,3 +122,5 @@ def test_in_process_three_shards_equal_single_world():
         ref = digest(single)
         assert all(digest(w) == ref for w in shards)
     assert sum(w.counters().ant_steps for w in shards) == single.counters().ant_steps
+    if alg.startswith("maco"):
+        assert single.vehicles()["deviations"].sum() > 0  # deviated records crossed the exchange

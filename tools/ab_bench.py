@@ -1,0 +1,33 @@
+"""A/B timing of one workload on two builds of the engine library.
+
+  python tools/ab_bench.py LIB CONFIG [steps] [warmup]
+
+Loads LIB (a libgmaco.so build) instead of the in-tree library, then times
+`steps` iterations of paper_2010_14244_b200.workloads.CONFIG with an L2 flush
+before each (gmaco_bench_steps, events around the walk and the step), and
+prints one JSON line: mean / p50 walk and step ms, ant-steps per step."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from paper_2010_14244_b200 import engine, workloads  # noqa: E402
+
+lib, config = sys.argv[1], sys.argv[2]
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+warmup = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+engine.load(lib)
+kw = {}
+if len(sys.argv) > 5:
+    kw["vehicles"] = int(sys.argv[5])
+net, cfg, dist, keep = workloads.CONFIGS[config](seed=1, max_steps=warmup + steps + 1, **kw)
+e = engine.Engine(net, cfg, dist)
+e.step(warmup)
+c0 = e.counters()
+walk, step = e.bench_steps(steps, 512 << 20, "both")
+c1 = e.counters()
+print(json.dumps({"lib": lib, "config": config, "walk_ms_mean": float(walk.mean()), "walk_ms_p50": float(np.median(walk)),
+                  "step_ms_mean": float(step.mean()), "step_ms_p50": float(np.median(step)),
+                  "ant_steps_per_step": (c1.ant_steps - c0.ant_steps) / steps}))
