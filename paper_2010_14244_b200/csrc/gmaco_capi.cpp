@@ -282,8 +282,11 @@ struct DevBuffers {
   static constexpr size_t kChunk = size_t(8) << 20, kArenaMax = size_t(1) << 20, kAlign = 256;
   struct Chunk {
     char* dev = nullptr;
-    std::unique_ptr<char[]> shadow;  // uninitialized: only written ranges are touched / sent
-    size_t used = 0, sent = 0;       // [sent, used) not yet on the device
+    // pinned host shadow from the process-wide pool (reused across engines:
+    // no page faults on first touch, and the flush is a true async DMA);
+    // uninitialized: only written ranges are touched / sent
+    char* shadow = nullptr;
+    size_t used = 0, sent = 0;  // [sent, used) not yet on the device
   };
   std::vector<void*> ptrs;
   std::vector<Chunk> chunks;
@@ -361,7 +364,7 @@ struct DevBuffers {
     bool any = false;
     for (auto& ch : chunks)
       if (ch.used > ch.sent) {
-        CK(cudaMemcpyAsync(ch.dev + ch.sent, ch.shadow.get() + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice,
+        CK(cudaMemcpyAsync(ch.dev + ch.sent, ch.shadow + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice,
                            stream));
         ch.sent = ch.used;
         any = true;
@@ -369,8 +372,11 @@ struct DevBuffers {
     if (any) CK(cudaStreamSynchronize(stream));
   }
   void seal() {
-    flush();
-    for (auto& ch : chunks) ch.shadow.reset();
+    flush();  // (synchronizes: the DMA from the shadows is complete)
+    for (auto& ch : chunks) {
+      PinnedPool::give(ch.shadow);
+      ch.shadow = nullptr;
+    }
     arena = false;
   }
   // Back to the pool, ordered after the owner's work on `stream` (call
@@ -379,6 +385,7 @@ struct DevBuffers {
     for (void* p : ptrs) cudaFreeAsync(p, stream);
     for (auto& ch : chunks) cudaFreeAsync(ch.dev, stream);
     if (!ptrs.empty() || !chunks.empty() || !big.empty()) cudaStreamSynchronize(stream);
+    for (auto& ch : chunks) PinnedPool::give(ch.shadow);  // (a build that failed before seal)
     for (void* p : big) cudaFree(p);
     ptrs.clear();
     chunks.clear();
@@ -393,7 +400,7 @@ struct DevBuffers {
       Chunk ch;
       ch.dev = static_cast<char*>(raw_alloc(kChunk));
       ptrs.pop_back();  // owned by the chunk list
-      ch.shadow.reset(new char[kChunk]);
+      ch.shadow = static_cast<char*>(PinnedPool::take(kChunk));
       chunks.push_back(std::move(ch));
     }
     Chunk& ch = chunks.back();
@@ -403,7 +410,7 @@ struct DevBuffers {
   }
   char* shadow_of(const void* d) {
     for (auto& ch : chunks)
-      if (d >= ch.dev && d < ch.dev + kChunk) return ch.shadow.get() + (static_cast<const char*>(d) - ch.dev);
+      if (d >= ch.dev && d < ch.dev + kChunk) return ch.shadow + (static_cast<const char*>(d) - ch.dev);
     throw std::runtime_error("arena: pointer outside every chunk");
   }
 };
@@ -512,6 +519,7 @@ struct gmaco_engine {
   int64_t last_walk_launches = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   int64_t wall_ms = 0;
+  int64_t direct_steps = 0;  // steps launched without a graph (run_steps, kDirectSteps)
   // multi-GPU
   int32_t rank = 0, world = 1, shard_pad = 0;
   ncclComm_t comm = nullptr;
@@ -1421,10 +1429,24 @@ void unbound_stop(gmaco_engine* h) {
 // need_count = false: the steps stay enqueued (no final host sync); the
 // control-block mirror is refreshed by the next synchronizing call (e.g. the
 // batched gmaco_get_vehicles), so a step/read loop costs one round trip.
+// Short runs launch their first kDirectSteps steps straight onto the stream:
+// capturing and instantiating a step graph costs ~70-150 us of host time,
+// more than a few dozen direct launches (the GPU runs ~25 us steps while the
+// host enqueues the next).  Longer runs then switch to the captured graphs.
+constexpr int64_t kDirectSteps = 48;
+bool launch_direct(gmaco_engine* h) {
+  if (h->direct_steps >= kDirectSteps) return false;
+  ++h->direct_steps;
+  CK(launch_step(h->w, h->res, h->stream, nullptr, nullptr));
+  return true;
+}
+
 int64_t run_steps(gmaco_engine* h, int64_t steps, bool need_count = true) {
   if (!need_count && !h->timing) {  // enqueue only: no mirror needed (steps past finished() are no-ops)
     if (steps <= 0) return -1;
     unbound_stop(h);
+    if (!h->graph_one && !h->graph_big)
+      while (steps > 0 && launch_direct(h)) --steps;
     for (int64_t i = 0; i < steps / kGraphSteps; ++i) {
       if (!h->graph_big) h->graph_big = capture(h, kGraphSteps, false);
       CK(cudaGraphLaunch(h->graph_big, h->stream));
@@ -1459,6 +1481,10 @@ int64_t run_steps(gmaco_engine* h, int64_t steps, bool need_count = true) {
     const int64_t remaining = target - cur;
     const bool big = remaining >= kGraphSteps;
     cudaGraphExec_t& ge = h->timing ? (big ? h->tgraph_big : h->tgraph_one) : (big ? h->graph_big : h->graph_one);
+    if (!ge && !h->timing && !big && launch_direct(h)) {  // (direct: past finished() a step is a no-op)
+      cur += 1;
+      continue;
+    }
     if (!ge) ge = capture(h, big ? kGraphSteps : 1, h->timing);
     CK(cudaGraphLaunch(ge, h->stream));
     if (h->timing) {
@@ -2067,8 +2093,19 @@ int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32
   return guarded(h, [&] {
     const PackDesc pd = arm_slot(h, fields, slot);
     auto& rs = h->rslot[slot];
-    // one graph per slot: a step then the snapshot gather, re-captured when the
-    // gather descriptor (field set, buffer) changes
+    // the first kDirectSteps steps: a direct step launch + the gather kernel
+    // (no capture cost for short runs)
+    if (!rs.snap_graph && h->direct_steps < kDirectSteps) {
+      unbound_stop(h);
+      launch_direct(h);
+      CK(launch_pack(pd, h->stream));
+      CK(cudaEventRecord(rs.done, h->stream));
+      rs.armed = true;
+      h->pending = true;
+      return;
+    }
+    // then one graph per slot: a step then the snapshot gather, re-captured
+    // when the gather descriptor (field set, buffer) changes
     if (!rs.snap_graph || std::memcmp(&rs.snap_pd, &pd, sizeof pd) != 0) {
       if (rs.snap_graph) CK(cudaGraphExecDestroy(rs.snap_graph));
       StepResources r = h->res;

@@ -9,8 +9,11 @@ sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2010_14244_b200 import abi, networks  # noqa: E402
+from paper_2010_14244_b200 import abi, engine, networks  # noqa: E402
 from paper_2010_14244_b200.engine import Engine  # noqa: E402
+
+if os.environ.get("LIB"):  # A/B: another build of the library
+    engine.load(os.environ["LIB"])
 
 net = networks.grid(32, 32, signals="all")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
