@@ -114,7 +114,8 @@ enum gmaco_option_bits {
   GMACO_OPT_NO_BITS = 1u << 7,        /* lattice tours kept as slots instead of per-hop move bits */
   GMACO_OPT_NO_E1_WALK = 1u << 8,     /* signal stages C, D, E1 in the tail instead of beside the walk */
   GMACO_OPT_NATURAL_ROWS = 1u << 9,   /* aligned-CSR rows in node order instead of BFS order */
-  GMACO_OPT_PROFILE_CREATE = 1u << 10 /* print gmaco_create phase times to stderr */
+  GMACO_OPT_PROFILE_CREATE = 1u << 10, /* print gmaco_create phase times to stderr */
+  GMACO_OPT_REDZONES = 1u << 11        /* guard bytes around every device array (gmaco_debug_check_redzones) */
 };
 typedef struct {
   uint32_t flags;    /* gmaco_option_bits */
@@ -321,6 +322,11 @@ int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
  * timestamps (ns, %globaltimer, 12 slots; see DevCtl::trace in
  * paper_2010_14244_b200/csrc/device.cuh). */
 int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
+/* Memory check of a world created with GMACO_OPT_REDZONES: settles the
+ * stream and verifies every guard band around the engine's device arrays.
+ * *corrupted receives the number of overwritten guards (0 = no out-of-bounds
+ * write reached one); gmaco_last_error describes the first. */
+int gmaco_debug_check_redzones(gmaco_engine* h, int64_t* corrupted);
 /* Benchmark entry point: enqueues `steps` engine steps without host
  * synchronization (one CUDA graph per step), with an L2-flushing memset of
  * flush_bytes before each step outside the timed span; returns per-step

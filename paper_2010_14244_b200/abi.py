@@ -65,7 +65,7 @@ class ColonyParams(C.Structure):
 
 # gmaco_option_bits: implementation switches, results bit-identical (gmaco.h)
 (OPT_NO_QUEUE, OPT_NO_SCRATCH, OPT_NO_TT, OPT_NO_ORDER, OPT_NO_PREFETCH, OPT_NO_PDL, OPT_NO_SMEM, OPT_NO_BITS,
- OPT_NO_E1_WALK, OPT_NATURAL_ROWS, OPT_PROFILE_CREATE) = (1 << i for i in range(11))
+ OPT_NO_E1_WALK, OPT_NATURAL_ROWS, OPT_PROFILE_CREATE, OPT_REDZONES) = (1 << i for i in range(12))
 
 
 class EngineOptions(C.Structure):

@@ -138,7 +138,7 @@ void build_graph(const gmaco_graph_desc* d, HostGraph& g) {
 void validate_config(const gmaco_sim_config* c) {
   if (!c) throw ValidationError("config is null");
   if (c->vehicle_count < 1) throw ValidationError("config: vehicle_count must be >= 1");
-  if (c->options.flags >> 11) throw ValidationError("options: unknown flag bits");
+  if (c->options.flags >> 12) throw ValidationError("options: unknown flag bits");
   if (!(c->options.sssp_delta >= 0)) throw ValidationError("options: sssp_delta must be >= 0");
   if (!(c->dt_s > 0)) throw ValidationError("config: dt must be positive");
   if (c->max_steps < 0) throw ValidationError("config: max_steps must be >= 0");
@@ -302,7 +302,28 @@ struct DevBuffers {
   // up to kPoolKeep of freed memory: engines created one after another (the
   // bench legs, the tests) reuse it instead of paying cudaMalloc per array.
   static constexpr uint64_t kPoolKeep = uint64_t(4) << 30;
-  void* raw_alloc(size_t bytes) {
+  // Checked builds of a world (GMACO_OPT_REDZONES): every allocation gets
+  // kRedzone guard bytes of kRedzoneByte before and after it (arena arrays:
+  // after), verified by gmaco_debug_check_redzones -- this engine's own
+  // memcheck for out-of-bounds writes (compute-sanitizer is not available on
+  // the GPU pool).
+  static constexpr size_t kRedzone = 1024;
+  static constexpr unsigned char kRedzoneByte = 0xA5;
+  bool redzones = false;
+  std::vector<std::pair<const char*, size_t>> zones;  // device guard ranges
+  void* raw_alloc(size_t bytes, bool guard = true) {
+    const size_t rz = redzones && guard ? kRedzone : 0;
+    char* base = static_cast<char*>(raw_alloc_base(bytes + 2 * rz));
+    if (rz) {
+      CK(cudaMemsetAsync(base, kRedzoneByte, rz, stream));
+      CK(cudaMemsetAsync(base + rz + bytes, kRedzoneByte, rz, stream));
+      CK(cudaStreamSynchronize(stream));
+      zones.emplace_back(base, rz);
+      zones.emplace_back(base + rz + bytes, rz);
+    }
+    return base + rz;
+  }
+  void* raw_alloc_base(size_t bytes) {
     static thread_local int configured_dev = -1;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -320,6 +341,7 @@ struct DevBuffers {
       big.push_back(p);
       return p;
     }
+    // (the pointer freed later is the base, the one pushed here)
     CK(cudaMallocAsync(&p, bytes, stream));
     CK(cudaStreamSynchronize(stream));  // usable by any stream / host call right away
     ptrs.push_back(p);
@@ -395,16 +417,21 @@ struct DevBuffers {
 
  private:
   void* carve(size_t bytes, const void*) {
-    const size_t need = (bytes + kAlign - 1) & ~(kAlign - 1);
+    const size_t rz = redzones ? kRedzone : 0;
+    const size_t need = (bytes + rz + kAlign - 1) & ~(kAlign - 1);
     if (chunks.empty() || chunks.back().used + need > kChunk) {
       Chunk ch;
-      ch.dev = static_cast<char*>(raw_alloc(kChunk));
+      ch.dev = static_cast<char*>(raw_alloc(kChunk, /*guard=*/false));
       ptrs.pop_back();  // owned by the chunk list
       ch.shadow = static_cast<char*>(PinnedPool::take(kChunk));
       chunks.push_back(std::move(ch));
     }
     Chunk& ch = chunks.back();
     void* p = ch.dev + ch.used;
+    if (rz) {  // trailing guard, sent with the chunk's next flush
+      std::memset(ch.shadow + ch.used + bytes, kRedzoneByte, rz);
+      zones.emplace_back(ch.dev + ch.used + bytes, rz);
+    }
     ch.used += need;
     return p;
   }
@@ -854,6 +881,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       throw ValidationError(fmt("node %d out-degree exceeds the engine bound of %d", u, kMaxDegree));
 
   DevBuffers& B = h->buf;
+  B.redzones = (c.options.flags & GMACO_OPT_REDZONES) != 0;
   B.arena = true;  // sub-allocate + shadow small arrays; sealed (one copy per chunk) below
   DevWorld& w = h->w;
   PhaseTimer pt;
@@ -2161,6 +2189,30 @@ int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view*
         view->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
     rs.armed = false;
   }, /*stream_ordered=*/true);
+}
+
+int gmaco_debug_check_redzones(gmaco_engine* h, int64_t* corrupted) {
+  if (!h || !corrupted) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    CK(cudaStreamSynchronize(h->stream));
+    if (!h->buf.redzones) throw ValidationError("check_redzones: the world was created without GMACO_OPT_REDZONES");
+    int64_t bad = 0;
+    std::string first;
+    std::vector<unsigned char> tmp;
+    for (size_t i = 0; i < h->buf.zones.size(); ++i) {
+      const auto& z = h->buf.zones[i];
+      tmp.resize(z.second);
+      CK(cudaMemcpy(tmp.data(), z.first, z.second, cudaMemcpyDeviceToHost));
+      for (size_t b = 0; b < z.second; ++b)
+        if (tmp[b] != DevBuffers::kRedzoneByte) {
+          if (!bad) first = fmt("guard %zu (%p) byte %zu overwritten", i, (const void*)z.first, b);
+          ++bad;
+          break;
+        }
+    }
+    *corrupted = bad;
+    h->err = bad ? first : fmt("%zu guards intact", h->buf.zones.size());
+  });
 }
 
 int gmaco_signal_count(gmaco_engine* h, int32_t* out) {

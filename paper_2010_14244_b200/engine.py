@@ -46,6 +46,7 @@ SIGNATURES = {
     "gmaco_set_timing": (C.c_int, C.c_void_p, i32),
     "gmaco_bench_steps": (C.c_int, C.c_void_p, i32, i64, P(f64), P(f64)),
     "gmaco_debug_trace": (C.c_int, C.c_void_p, i32, P(u64)),
+    "gmaco_debug_check_redzones": (C.c_int, C.c_void_p, P(i64)),
     "gmaco_set_shard": (C.c_int, C.c_void_p, i32, i32),
     "gmaco_step_split": (C.c_int, C.c_void_p, i32),
     "gmaco_exchange_export": (C.c_int, C.c_void_p, P(i32), P(i64)),
@@ -250,6 +251,13 @@ class Engine:
         return out
 
     # -- sharding (multi-GPU) -----------------------------------------------------
+    def check_redzones(self) -> tuple[int, str]:
+        """(overwritten guard bands, message) of a world created with
+        abi.OPT_REDZONES."""
+        n = i64()
+        self._check(self.L.gmaco_debug_check_redzones(self.h, C.byref(n)))
+        return n.value, self.L.gmaco_last_error(self.h).decode()
+
     def attach_comm(self, rank: int, world: int, nccl_id: bytes):
         buf = C.create_string_buffer(nccl_id, 128)
         self._check(self.L.gmaco_attach_comm(self.h, rank, world, buf))
