@@ -255,6 +255,17 @@ int gmaco_nccl_unique_id(void* out128);
  * gmaco_step_split(h, 2) (apply the remote decisions, stages C..G). */
 #define GMACO_REC_DEVIATED (1 << 30) /* decision record flag: a MACO deviation (RouteDecision::deviated) */
 int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi);
+/* By-target shards (worlds with per-target candidate rows: TARGETS
+ * distances, ant-queue walker): this engine plans the vehicles bound for the
+ * destination targets dealt to `rank` (targets by vehicle count, largest
+ * first, each to the least-loaded rank; identical on every rank), refreshes
+ * only those targets' tables and keeps its walk destination-major.
+ * gmaco_attach_comm picks this form by itself for such worlds.  With it,
+ * gmaco_exchange_export returns the shard's records in the order
+ * gmaco_shard_vehicles lists its vehicles (*n = shard size; vids written
+ * when cap >= *n). */
+int gmaco_shard_by_target(gmaco_engine* h, int32_t rank, int32_t world);
+int gmaco_shard_vehicles(gmaco_engine* h, int32_t* vids, int32_t cap, int32_t* n);
 int gmaco_step_split(gmaco_engine* h, int32_t part);
 int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits);
 int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64_t* deposits);

@@ -88,6 +88,7 @@ struct DevParams {
   // vehicle sharding (multi-GPU): this rank plans vehicles [shard_lo, shard_hi);
   // the others' decisions arrive through the exchange (k_apply_remote)
   int32_t shard_lo, shard_hi, sharded;
+  int32_t rank;          // this rank (by-target sharding: DevVehicles::owner)
   int32_t no_smem;          // A/B switch: read the walk tables from global memory
   int32_t grid_bits;        // lattice walker keeps tours as per-hop move bits (SMEM words)
   int32_t bit_words;        // 64-hop move-bit words per ant (ceil(plan_cap / 64))
@@ -156,7 +157,10 @@ struct DevVehicles {
   int32_t *plan, *plan_n;       // best planned tour (slots), [V * plan_cap] (replay mode)
   int32_t* scratch;             // [V * ants * plan_cap] every ant's tour (scratch mode)
   int32_t* plan_ant;            // winning ant per vehicle (scratch mode)
-  const int32_t* walk_order;    // lattice walker: walk slot -> vehicle (walk-length balanced), or nullptr
+  const int32_t* walk_order;    // walk slot -> vehicle (walk-length balanced / destination-major; a shard's
+                                //     own vehicles at slots [shard_lo, shard_hi)), or nullptr
+  const int16_t* owner;         // by-target sharding: [V] rank planning each vehicle (nullptr: the
+                                //     contiguous range [shard_lo, shard_hi) is this rank's)
   // ant-queue walker (general graphs, scratch mode): per-vehicle walk start
   // (-1 = not walking), deciding flag, packed (cost, ant) argmin key, the
   // walking-vehicle list the queue indexes, and per-ant hop counts
@@ -205,6 +209,8 @@ struct DevTT {
   const int64_t* cstart; // [T * (nch + 1)] first record of each kTTChunk-row chunk (+ table end)
   int64_t nrec;
   int32_t T, nch;
+  const int32_t* own_t;  // by-target sharding: the T_own tables this rank refreshes (nullptr: all T)
+  int32_t T_own;
 };
 constexpr int kTTChunk = 1024;  // rows per refresh chunk
 

@@ -549,6 +549,12 @@ struct gmaco_engine {
   int64_t direct_steps = 0;  // steps launched without a graph (run_steps, kDirectSteps)
   // multi-GPU
   int32_t rank = 0, world = 1, shard_pad = 0;
+  // by-target sharding: node -> target table (TARGETS distances), the
+  // allgather send / receive buffers and the received record -> vehicle map
+  std::vector<int32_t> target_of_node;
+  int32_t* xsend = nullptr;
+  int32_t* xrecv = nullptr;
+  int32_t* xgath = nullptr;
   ncclComm_t comm = nullptr;
 
   ~gmaco_engine() {
@@ -1354,6 +1360,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     }
   }
   dv.dec_rec = B.filled<int32_t>(V, -1);
+  if (w.tt.rec) h->target_of_node = slot_of;  // by-target sharding (shard_by_target)
   dv.plan_n = B.filled<int32_t>(V, 0);
   dv.plan_step = B.filled<int64_t>(V, -1);
   dv.plan_done = B.filled<uint8_t>(V, 0);
@@ -1643,12 +1650,77 @@ cudaError_t nccl_exchange(void* ctx, cudaStream_t st) {
   const size_t P = h->shard_pad;
   // both collectives in one NCCL group: a single fused launch per step
   const NcclApi& N = nccl();
+  if (w.v.owner) {  // by-target shards: this rank's records in its walk order
+    const cudaError_t e = rec_pack(w, h->xsend, (int32_t)P, st);
+    if (e != cudaSuccess) return e;
+  }
   if (N.GroupStart() != ncclSuccess) return cudaErrorUnknown;
-  ncclResult_t r = N.AllGather(w.v.dec_rec + (size_t)h->rank * P, w.v.dec_rec, P, ncclInt32, h->comm, st);
+  ncclResult_t r = w.v.owner ? N.AllGather(h->xsend, h->xrecv, P, ncclInt32, h->comm, st)
+                             : N.AllGather(w.v.dec_rec + (size_t)h->rank * P, w.v.dec_rec, P, ncclInt32, h->comm, st);
   if (r == ncclSuccess && w.p.deposit == GMACO_DEPOSIT_BEST_TOUR)
     r = N.AllReduce(w.dep, w.dep, (size_t)w.g.M, ncclInt64, ncclSum, h->comm, st);
   const ncclResult_t e = N.GroupEnd();
-  return (r == ncclSuccess && e == ncclSuccess) ? cudaSuccess : cudaErrorUnknown;
+  if (r != ncclSuccess || e != ncclSuccess) return cudaErrorUnknown;
+  return w.v.owner ? rec_unpack(w, h->xrecv, h->xgath, (int32_t)(P * h->world), st) : cudaSuccess;
+}
+
+// By-target sharding (worlds with per-target candidate rows): rank r plans
+// the vehicles bound for the targets dealt to it -- largest vehicle count
+// first, each to the least-loaded rank (ties: lowest index), identically on
+// every rank -- so it refreshes and walks only its own targets' tables
+// (k_tt_refresh over T/world tables instead of T) and its walk stays
+// destination-major.  The planning list is the full walk order filtered to
+// the rank's vehicles.  Returns every rank's list (the allgather layout).
+std::vector<std::vector<int32_t>> shard_by_target(gmaco_engine* h, int32_t rank, int32_t world) {
+  DevWorld& w = h->w;
+  if (w.p.sharded) throw ValidationError("sharding: the engine is already sharded");
+  if (!w.tt.rec || h->target_of_node.empty())
+    throw ValidationError("sharding: by-target shards need per-target rows (TARGETS distances, ant-queue walker)");
+  if (rank < 0 || rank >= world || world > 32767) throw ValidationError("sharding: invalid rank / world");
+  const int32_t V = w.p.V, T = w.tt.T;
+  const std::vector<int32_t> dest = download(w.v.dest, V);
+  std::vector<int32_t> order(V);
+  if (w.v.walk_order) order = download(w.v.walk_order, V);
+  else for (int32_t i = 0; i < V; ++i) order[i] = i;
+  std::vector<int64_t> cnt(T, 0);
+  for (int32_t i = 0; i < V; ++i) cnt[h->target_of_node[dest[i]]]++;
+  std::vector<int32_t> ts(T);
+  for (int32_t t = 0; t < T; ++t) ts[t] = t;
+  std::stable_sort(ts.begin(), ts.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+  std::vector<int64_t> load(world, 0);
+  std::vector<int16_t> towner(T, 0);
+  for (int32_t t : ts) {
+    int32_t best = 0;
+    for (int32_t r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    towner[t] = (int16_t)best;
+    load[best] += cnt[t];
+  }
+  std::vector<int16_t> owner(V);
+  std::vector<std::vector<int32_t>> lists(world);
+  for (int32_t i = 0; i < V; ++i) owner[i] = towner[h->target_of_node[dest[i]]];
+  for (int32_t i = 0; i < V; ++i) lists[owner[order[i]]].push_back(order[i]);
+  std::vector<int32_t> own_t;
+  for (int32_t t = 0; t < T; ++t)
+    if (towner[t] == rank) own_t.push_back(t);
+  auto up = [&](const auto& vec) {
+    using E = typename std::decay_t<decltype(vec)>::value_type;
+    E* d = h->buf.alloc_direct<E>(std::max<size_t>(vec.size(), 1));
+    if (!vec.empty()) CK(cudaMemcpyAsync(d, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return d;
+  };
+  const std::vector<int32_t>& mine = lists[rank];
+  w.v.walk_order = up(mine);  // slots [0, n_own): this rank's vehicles
+  w.v.owner = up(owner);
+  w.tt.own_t = up(own_t);
+  w.tt.T_own = (int32_t)own_t.size();
+  w.p.shard_lo = 0;
+  w.p.shard_hi = (int32_t)mine.size();
+  w.p.rank = rank;
+  w.p.sharded = 1;
+  h->reset_graphs();
+  return lists;
 }
 
 // Vehicle sharding (partition_entities ranges, parallel.cpp:8-21): this
@@ -1660,6 +1732,7 @@ cudaError_t nccl_exchange(void* ctx, cudaStream_t st) {
 void set_shard(gmaco_engine* h, int32_t lo, int32_t hi, int32_t pad_total) {
   DevWorld& w = h->w;
   if (lo < 0 || hi > w.p.V || lo > hi) throw ValidationError("sharding: invalid vehicle range");
+  if (w.v.owner) throw ValidationError("sharding: the engine is sharded by target");
   if (w.g.M >= GMACO_REC_DEVIATED || h->g.m >= GMACO_REC_DEVIATED)
     throw ValidationError("sharding: decision records need fewer than 2^30 edges");
   if (pad_total > w.p.V) {  // allgather layout: world * shard_pad records
@@ -1755,12 +1828,27 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
       throw ValidationError("attach_comm: this communicator is held by another live engine "
                             "(destroy it first; one engine per communicator at a time)");
     const int32_t V = h->w.p.V;
-    const int32_t P = (V + world - 1) / world;  // padded contiguous shards (allgather layout)
-    const int32_t lo = std::min(V, rank * P), hi = std::min(V, (rank + 1) * P);
-    set_shard(h, lo, hi, world * P);
+    if (h->w.tt.rec) {  // per-target rows: shard by destination target
+      const auto lists = shard_by_target(h, rank, world);
+      int32_t P = 1;
+      for (const auto& l : lists) P = std::max<int32_t>(P, (int32_t)l.size());
+      std::vector<int32_t> gath((size_t)world * P, -1);
+      for (int32_t r = 0; r < world; ++r)
+        std::copy(lists[r].begin(), lists[r].end(), gath.begin() + (size_t)r * P);
+      h->xsend = h->buf.alloc_direct<int32_t>(P);
+      h->xrecv = h->buf.alloc_direct<int32_t>((size_t)world * P);
+      h->xgath = h->buf.alloc_direct<int32_t>((size_t)world * P);
+      CK(cudaMemcpyAsync(h->xgath, gath.data(), gath.size() * 4, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      h->shard_pad = P;
+    } else {
+      const int32_t P = (V + world - 1) / world;  // padded contiguous shards (allgather layout)
+      const int32_t lo = std::min(V, rank * P), hi = std::min(V, (rank + 1) * P);
+      set_shard(h, lo, hi, world * P);
+      h->shard_pad = P;
+    }
     h->rank = rank;
     h->world = world;
-    h->shard_pad = P;
     if (!ce.comm) nck(nccl().CommInitRank(&ce.comm, world, id, rank), "ncclCommInitRank");
     ce.holder = h;
     h->comm = ce.comm;
@@ -1775,6 +1863,31 @@ int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
   return guarded(h, [&] {
     set_shard(h, lo, hi, 0);
     h->res.exchange = nullptr;
+  });
+}
+
+int gmaco_shard_by_target(gmaco_engine* h, int32_t rank, int32_t world) {
+  if (h) h->ctl_valid = false;
+  if (!h) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    shard_by_target(h, rank, world);
+    h->res.exchange = nullptr;
+  });
+}
+
+int gmaco_shard_vehicles(gmaco_engine* h, int32_t* vids, int32_t cap, int32_t* n) {
+  if (!h || !n) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    const DevWorld& w = h->w;
+    *n = w.p.shard_hi - w.p.shard_lo;
+    if (vids && cap >= *n) {
+      if (w.v.owner) {
+        const auto mine = download(w.v.walk_order, *n);
+        std::copy(mine.begin(), mine.end(), vids);
+      } else {
+        for (int32_t i = 0; i < *n; ++i) vids[i] = w.p.shard_lo + i;
+      }
+    }
   });
 }
 
@@ -1801,8 +1914,14 @@ int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits
   return guarded(h, [&] {
     const DevWorld& w = h->w;
     const int32_t lo = w.p.shard_lo, hi = w.p.shard_hi;
-    if (decisions && hi > lo) {  // records at the boundary: edge id, -1 none, -2 retired
+    if (decisions && hi > lo && w.v.owner) {  // by-target shard: own records in planning order
+      const auto rec = download(w.v.dec_rec, w.p.V);
+      const auto mine = download(w.v.walk_order, hi);
+      for (int32_t i = 0; i < hi; ++i) decisions[i] = rec[mine[i]];
+    } else if (decisions && hi > lo) {  // records at the boundary: edge id, -1 none, -2 retired
       CK(cudaMemcpy(decisions, w.v.dec_rec + lo, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost));
+    }
+    if (decisions && hi > lo) {
       for (int32_t i = 0; i < hi - lo; ++i)
         if (decisions[i] >= 0)
           decisions[i] = h->slot_edge[decisions[i] & ~GMACO_REC_DEVIATED] | (decisions[i] & GMACO_REC_DEVIATED);

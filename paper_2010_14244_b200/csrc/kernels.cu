@@ -1423,9 +1423,11 @@ __global__ void __launch_bounds__(256) k_colony_epi(DevWorld w) {
   const DevVehicles& v = w.v;
   const int64_t step = w.ctl->step;
   const int lane = threadIdx.x & 31;
-  const int32_t vid = w.p.shard_lo + blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  // this rank's vehicles, in walk order when one is set (by-target shards)
+  const int32_t slot = w.p.shard_lo + blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int32_t vid = (w.v.walk_order && slot < w.p.shard_hi) ? w.v.walk_order[slot] : slot;
   long long routes = 0, decided = 0, act = 0, unf = 0;
-  const int32_t start = vid < w.p.shard_hi ? v.walk_start[vid] : -1;
+  const int32_t start = slot < w.p.shard_hi ? v.walk_start[vid] : -1;
   if (start >= 0) {
     const int K = w.p.ants;
     const bool deciding = v.walk_dec[vid];
@@ -2528,12 +2530,17 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
 // replicated vehicle state — activation (engine.cpp:177-180), then the
 // decision's bookkeeping (engine.cpp:202-216) or retirement.
 // ---------------------------------------------------------------------------
+// A vehicle another rank plans (its decision record arrives with the exchange).
+__device__ __forceinline__ bool is_remote(const DevWorld& w, int32_t vid) {
+  return w.v.owner ? w.v.owner[vid] != w.p.rank : !(vid >= w.p.shard_lo && vid < w.p.shard_hi);
+}
+
 __global__ void __launch_bounds__(256) k_apply_remote(DevWorld w) {
   if (skip_step(w.ctl)) return;
   __shared__ long long red[32];
   const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
   long long applied = 0;
-  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) {
+  if (vid < w.p.V && is_remote(w, vid)) {
     const DevVehicles& v = w.v;
     const int64_t step = w.ctl->step;
     if (v.state[vid] == kPending && v.depart[vid] == step) {
@@ -2577,7 +2584,7 @@ __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
   __shared__ long long red[32];
   const int32_t vid = blockIdx.x * blockDim.x + threadIdx.x;
   long long act = 0, unf = 0;
-  if (vid < w.p.V && !(vid >= w.p.shard_lo && vid < w.p.shard_hi)) apply_remote_one(w, vid, act, unf);
+  if (vid < w.p.V && is_remote(w, vid)) apply_remote_one(w, vid, act, unf);
   act = block_sum(act, red);
   unf = block_sum(unf, red);
   if (threadIdx.x == 0) {
@@ -2612,7 +2619,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       // in to save a kernel boundary per step)
       long long act = 0, unf = 0;
       for (int64_t vid = gtid; vid < p.V; vid += gstride)
-        if (!(vid >= p.shard_lo && vid < p.shard_hi)) apply_remote_one(w, (int32_t)vid, act, unf);
+        if (is_remote(w, (int32_t)vid)) apply_remote_one(w, (int32_t)vid, act, unf);
       act = block_sum(act, red);
       if (threadIdx.x == 0 && act) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)act);
       unf = block_sum(unf, red);
@@ -3173,8 +3180,8 @@ __global__ void k_tt_fill(DevWorld w, int32_t T, const int32_t* place, const int
 // row chunk are rewritten by consecutive blocks, so the shared slot records
 // they gather are read from DRAM once and hit L2 for the other tables.
 __global__ void __launch_bounds__(256, 4) k_tt_refresh(DevWorld w) {
-  const int32_t T = w.tt.T, nch = w.tt.nch;
-  const int32_t t = blockIdx.x % T, ch = blockIdx.x / T;
+  const int32_t T = w.tt.own_t ? w.tt.T_own : w.tt.T, nch = w.tt.nch;
+  const int32_t t = w.tt.own_t ? w.tt.own_t[blockIdx.x % T] : (int32_t)(blockIdx.x % T), ch = blockIdx.x / T;
   const int64_t* cs = w.tt.cstart + (int64_t)t * (nch + 1);
   const int64_t lo = cs[ch];
   const int32_t cnt = (int32_t)(cs[ch + 1] - lo);
@@ -3195,6 +3202,25 @@ __global__ void __launch_bounds__(256, 4) k_tt_refresh(DevWorld w) {
       if (i0 + k * 256 < cnt)
         out[i0 + k * 256] = q[k].x >= 0 ? make_int4(r[k].x, r[k].y, r[k].z, q[k].y) : make_int4(0, 0, 0, 0);
   }
+}
+
+// By-target sharding exchange: this rank's records in its walk order into the
+// allgather send buffer, then every rank's records back to their vehicles.
+__global__ void k_rec_pack(DevWorld w, int32_t* send, int32_t pad) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < pad) send[i] = i < w.p.shard_hi ? w.v.dec_rec[w.v.walk_order[i]] : -1;
+}
+__global__ void k_rec_unpack(DevWorld w, const int32_t* recv, const int32_t* gath, int32_t count) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count && gath[i] >= 0) w.v.dec_rec[gath[i]] = recv[i];
+}
+cudaError_t rec_pack(const DevWorld& w, int32_t* send, int32_t pad, cudaStream_t st) {
+  k_rec_pack<<<blocks_for(pad, 256), 256, 0, st>>>(w, send, pad);
+  return cudaGetLastError();
+}
+cudaError_t rec_unpack(const DevWorld& w, const int32_t* recv, const int32_t* gath, int32_t count, cudaStream_t st) {
+  k_rec_unpack<<<blocks_for(count, 256), 256, 0, st>>>(w, recv, gath, count);
+  return cudaGetLastError();
 }
 
 cudaError_t tt_count(const DevWorld& w, int32_t T, const int32_t* place, int32_t* units, cudaStream_t st) {
@@ -3228,7 +3254,7 @@ cudaError_t tt_build(const DevWorld& w, int32_t T, const int32_t* place, const i
 
 cudaError_t tt_refresh(const DevWorld& w, cudaStream_t st) {
   if (!w.tt.rec) return cudaSuccess;
-  k_tt_refresh<<<w.tt.T * w.tt.nch, 256, 0, st>>>(w);
+  k_tt_refresh<<<(w.tt.own_t ? w.tt.T_own : w.tt.T) * w.tt.nch, 256, 0, st>>>(w);
   return cudaGetLastError();
 }
 
@@ -3288,7 +3314,7 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       k_colony_ell4<0><<<blocks_for(VS, vpb), threads, 0, st>>>(w);
   } else if (w.p.ant_queue) {
     if (w.tt.rec) {
-      k_tt_refresh<<<w.tt.T * w.tt.nch, 256, 0, st>>>(w);  // this step's weights / costs
+      k_tt_refresh<<<(w.tt.own_t ? w.tt.T_own : w.tt.T) * w.tt.nch, 256, 0, st>>>(w);  // this step's weights / costs
       k_colony_pro<<<blocks_for(VS, 256), 256, 0, st>>>(w);
       k_colony_qt<<<r.queue_blocks, 128, 0, st>>>(w);
     } else {
@@ -3384,6 +3410,7 @@ int kernels_per_step(const DevWorld& w, const StepResources& r) {
   if (w.tt.rec) k += 1;      // k_tt_refresh
   if (w.p.sharded && !(w.p.algorithm == 4 && r.coop_blocks > 0))
     k += 1;  // k_apply_remote[_move] (folded into the cooperative colony tail otherwise)
+  if (w.v.owner && r.exchange) k += 2;  // by-target shards: k_rec_pack / k_rec_unpack around the allgather
   if (r.coop_blocks > 0) return k + 1;  // k_tail_coop
   if (w.p.S > 0) k += 2;     // k_signals, k_e3
   if (w.p.algorithm != 4) k += 1;  // k_move (colony walks run E2 themselves)

@@ -25,6 +25,9 @@ struct StepResources {
 
 // Enqueues one engine step (stages B..G) on `st`.  Optional events bracket
 // the stage-B walk kernel (recorded as external events while capturing).
+// By-target sharding exchange buffers (gmaco_capi.cpp nccl_exchange).
+cudaError_t rec_pack(const DevWorld& w, int32_t* send, int32_t pad, cudaStream_t st);
+cudaError_t rec_unpack(const DevWorld& w, const int32_t* recv, const int32_t* gath, int32_t count, cudaStream_t st);
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end);
 size_t scan_temp_bytes(int V);

@@ -49,6 +49,8 @@ SIGNATURES = {
     "gmaco_debug_check_redzones": (C.c_int, C.c_void_p, P(i64)),
     "gmaco_set_shard": (C.c_int, C.c_void_p, i32, i32),
     "gmaco_step_split": (C.c_int, C.c_void_p, i32),
+    "gmaco_shard_by_target": (C.c_int, C.c_void_p, i32, i32),
+    "gmaco_shard_vehicles": (C.c_int, C.c_void_p, P(i32), i32, P(i32)),
     "gmaco_exchange_export": (C.c_int, C.c_void_p, P(i32), P(i64)),
     "gmaco_exchange_import": (C.c_int, C.c_void_p, P(i32), P(i64)),
     "gmaco_network_parse": (C.c_int, C.c_char_p, C.c_size_t, P(C.c_void_p)),
@@ -265,6 +267,17 @@ class Engine:
     def set_shard(self, lo: int, hi: int):
         self.shard = (lo, hi)
         self._check(self.L.gmaco_set_shard(self.h, lo, hi))
+
+    def shard_by_target(self, rank: int, world: int):
+        """By-target shard (per-target-row worlds): plans the vehicles bound
+        for the targets dealt to `rank`; self.owned lists them."""
+        self._check(self.L.gmaco_shard_by_target(self.h, rank, world))
+        n = i32()
+        self._check(self.L.gmaco_shard_vehicles(self.h, None, 0, C.byref(n)))
+        vids = np.zeros(max(n.value, 1), dtype=np.int32)
+        self._check(self.L.gmaco_shard_vehicles(self.h, abi.ptr(vids, i32), len(vids), C.byref(n)))
+        self.owned = vids[: n.value].copy()
+        self.shard = (0, n.value)
 
     def step_split(self, part: int):
         self._check(self.L.gmaco_step_split(self.h, part))

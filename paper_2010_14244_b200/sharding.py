@@ -49,3 +49,24 @@ def local_transport(worlds):
             w.exchange_import(dec[: w.V], dep)
             w.step_split(2)
     return run_step
+
+
+def local_transport_owned(worlds):
+    """In-process collectives for shards with explicit vehicle lists
+    (Engine.shard_by_target: `owned` = the shard's vehicles in the order its
+    records are exported).  Records are scattered back to vehicle order --
+    what the engine's own NCCL path does on the device (k_rec_unpack)."""
+    V = worlds[0].V
+
+    def run_step():
+        for w in worlds:
+            w.step_split(1)
+        exported = [w.exchange_export() for w in worlds]
+        dec = np.full(V, -1, dtype=np.int32)
+        for w, (d, _) in zip(worlds, exported):
+            dec[w.owned] = d
+        dep = np.sum([p for _, p in exported], axis=0).astype(np.int64)
+        for w in worlds:
+            w.exchange_import(dec, dep)
+            w.step_split(2)
+    return run_step

@@ -241,3 +241,61 @@ def test_maco_p_nccl_exchange_world1_equals_unsharded():
     single.step(40)
     assert same(e, single) is None
     assert O.results_identical(e.run(), single.run())
+
+
+def _c4_like(V=500, seed=11):
+    from test_gpu_parity import _rgg_targets
+    net, dist, tgt = _rgg_targets(3000, 12, seed)
+    cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive",
+                                                   vehicle_count=V, seed=seed, max_steps=40), ants=16)
+    cfg.colony.max_hops = 512
+    return net, cfg, dist, tgt
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_by_target_shards_equal_unsharded(nshards):
+    """C4's path sharded by destination target (each shard refreshes and
+    walks only its own targets' tables, destination-major order kept):
+    every shard equals the unsharded engine step by step, the shards
+    partition the fleet, and the refreshed tables partition the targets."""
+    net, cfg, dist, tgt = _c4_like()
+    single = Engine(net, cfg, dist)
+    shards = []
+    for r in range(nshards):
+        e = Engine(net, cfg, dist)
+        e.shard_by_target(r, nshards)
+        shards.append(e)
+    owned = np.sort(np.concatenate([e.owned for e in shards]))
+    assert np.array_equal(owned, np.arange(cfg.vehicle_count))
+    dest = single.vehicles()["dest"]
+    tsets = [set(dest[e.owned].tolist()) for e in shards]
+    for a in range(nshards):
+        for b in range(a + 1, nshards):
+            assert not (tsets[a] & tsets[b]), "a target is planned on two shards"
+    step = sharding.local_transport_owned(shards)
+    for k in range(8):
+        step()
+        single.step(1)
+        for e in shards:
+            assert same(e, single) is None, (k, same(e, single))
+    assert sum(e.counters().ant_steps for e in shards) == single.counters().ant_steps
+    for e in shards:  # planned tours live on the vehicle's own shard
+        for vid in e.owned[::5]:
+            assert np.array_equal(e.route(int(vid), True), single.route(int(vid), True))
+
+
+def test_by_target_nccl_world1_equals_unsharded():
+    """The by-target NCCL exchange (records packed in planning order,
+    allgather, unpacked to vehicles) at world size 1."""
+    from paper_2010_14244_b200 import engine
+    import ctypes as C
+    net, cfg, dist, tgt = _c4_like(V=400, seed=3)
+    uid = C.create_string_buffer(128)
+    assert engine.load().gmaco_nccl_unique_id(uid) == 0
+    e = Engine(net, cfg, dist)
+    e.attach_comm(0, 1, uid.raw)
+    single = Engine(net, cfg, dist)
+    e.step(10)
+    single.step(10)
+    assert same(e, single) is None
+    assert O.results_identical(e.run(), single.run())
