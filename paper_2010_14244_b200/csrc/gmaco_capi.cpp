@@ -1352,7 +1352,37 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       for (int32_t i = 0; i < n; ++i) posn[place[i]] = i;
       for (int32_t i = 0; i < V; ++i) ord[i] = i;
       auto tkey = [&](int32_t x) { return slot_of.empty() ? x : slot_of[x]; };
+      // Longest walks first, in kLptBands bands of origin->destination
+      // distance (a walk's hop count follows it): the queue's last ants are
+      // short walks instead of stragglers holding the kernel's end.  Within a
+      // band, destination-major order keeps the rows of a few targets hot.
+      constexpr int kLptBands = 4;
+      std::vector<int32_t> band(V, 0);
+      if (w.d.table) {
+        std::vector<int32_t> rowv(V), orgv(V);
+        for (int32_t i = 0; i < V; ++i) {
+          rowv[i] = tkey(sp.dest[i]);
+          orgv[i] = sp.origin[i];
+        }
+        DevBuffers tmpb;
+        tmpb.stream = h->stream;
+        int32_t* drow = tmpb.upload(rowv);
+        int32_t* dorg = tmpb.upload(orgv);
+        int64_t* dd_ = tmpb.alloc<int64_t>(V);
+        CK(gather_dist(w.d.table, n, drow, dorg, V, dd_, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::vector<int64_t> dv_ = download(dd_, V), sorted_ = dv_;
+        std::sort(sorted_.begin(), sorted_.end());
+        int64_t cut[kLptBands - 1];
+        for (int b = 1; b < kLptBands; ++b) cut[b - 1] = sorted_[(size_t)V * (kLptBands - b) / kLptBands];
+        for (int32_t i = 0; i < V; ++i) {
+          int b = 0;
+          while (b < kLptBands - 1 && dv_[i] < cut[b]) ++b;
+          band[i] = b;  // 0: the longest quarter
+        }
+      }
       std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+        if (band[a] != band[b]) return band[a] < band[b];
         const int32_t ta = tkey(sp.dest[a]), tb = tkey(sp.dest[b]);
         return ta != tb ? ta < tb : posn[sp.origin[a]] < posn[sp.origin[b]];
       });

@@ -3204,6 +3204,19 @@ __global__ void __launch_bounds__(256, 4) k_tt_refresh(DevWorld w) {
   }
 }
 
+// dist(origin_i -> dest_i) of every vehicle from a [row][n] distance table
+// (walk-order keys at create).
+__global__ void k_gather_dist(const int64_t* table, int32_t n, const int32_t* row, const int32_t* x, int32_t count,
+                              int64_t* out) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = row[i] < 0 ? INT64_MAX : table[(size_t)row[i] * n + x[i]];
+}
+cudaError_t gather_dist(const int64_t* table, int32_t n, const int32_t* row, const int32_t* x, int32_t count,
+                        int64_t* out, cudaStream_t st) {
+  k_gather_dist<<<blocks_for(count, 256), 256, 0, st>>>(table, n, row, x, count, out);
+  return cudaGetLastError();
+}
+
 // By-target sharding exchange: this rank's records in its walk order into the
 // allgather send buffer, then every rank's records back to their vehicles.
 __global__ void k_rec_pack(DevWorld w, int32_t* send, int32_t pad) {

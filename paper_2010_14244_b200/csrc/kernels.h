@@ -25,6 +25,8 @@ struct StepResources {
 
 // Enqueues one engine step (stages B..G) on `st`.  Optional events bracket
 // the stage-B walk kernel (recorded as external events while capturing).
+cudaError_t gather_dist(const int64_t* table, int32_t n, const int32_t* row, const int32_t* x, int32_t count,
+                        int64_t* out, cudaStream_t st);
 // By-target sharding exchange buffers (gmaco_capi.cpp nccl_exchange).
 cudaError_t rec_pack(const DevWorld& w, int32_t* send, int32_t pad, cudaStream_t st);
 cudaError_t rec_unpack(const DevWorld& w, const int32_t* recv, const int32_t* gath, int32_t count, cudaStream_t st);
