@@ -34,6 +34,7 @@
 #include "gmaco.h"
 #include "kernels.h"
 #include "nccl.h"
+#include "nvtx3/nvToolsExt.h"
 
 namespace gmaco {
 namespace {
@@ -599,6 +600,13 @@ struct gmaco_engine {
 namespace {
 
 thread_local std::string g_create_err;
+
+// NVTX range per C-ABI entry point (SURVEY §5 tracing): a no-op unless a
+// profiler (nsys / ncu with NVTX filtering) attaches.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 int guarded(gmaco_engine* h, F&& f, bool stream_ordered = false) {
@@ -1844,6 +1852,7 @@ int gmaco_nccl_unique_id(void* out128) {
 }
 
 int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* nccl_id) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h || !nccl_id || world < 1 || rank < 0 || rank >= world) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -1888,6 +1897,7 @@ int gmaco_attach_comm(gmaco_engine* h, int32_t rank, int32_t world, const void* 
 }
 
 int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -1897,6 +1907,7 @@ int gmaco_set_shard(gmaco_engine* h, int32_t lo, int32_t hi) {
 }
 
 int gmaco_shard_by_target(gmaco_engine* h, int32_t rank, int32_t world) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -1922,6 +1933,7 @@ int gmaco_shard_vehicles(gmaco_engine* h, int32_t* vids, int32_t cap, int32_t* n
 }
 
 int gmaco_step_split(gmaco_engine* h, int32_t part) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h || (part != 1 && part != 2)) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -1940,6 +1952,7 @@ int gmaco_step_split(gmaco_engine* h, int32_t part) {
 }
 
 int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits) {
+  NvtxRange nvtx_(__func__);
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const DevWorld& w = h->w;
@@ -1961,6 +1974,7 @@ int gmaco_exchange_export(gmaco_engine* h, int32_t* decisions, int64_t* deposits
 }
 
 int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64_t* deposits) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -1986,6 +2000,7 @@ int gmaco_exchange_import(gmaco_engine* h, const int32_t* decisions, const int64
 
 int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist, const gmaco_sim_config* cfg,
                  int32_t device, gmaco_engine** out) {
+  NvtxRange nvtx_(__func__);
   if (!out) {
     g_create_err = "gmaco_create: out is null";
     return GMACO_EVALIDATION;
@@ -2000,6 +2015,7 @@ int gmaco_create(const gmaco_graph_desc* graph, const gmaco_distance_desc* dist,
 }
 
 int gmaco_step(gmaco_engine* h, int64_t steps, int64_t* executed) {
+  NvtxRange nvtx_(__func__);
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const int64_t k = run_steps(h, steps, executed != nullptr);
@@ -2024,6 +2040,7 @@ int gmaco_current_step(gmaco_engine* h, int64_t* out) {
 }
 
 int gmaco_run(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s) {
+  NvtxRange nvtx_(__func__);
   if (!h || !result) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const auto t0 = std::chrono::steady_clock::now();
@@ -2039,16 +2056,19 @@ int gmaco_run(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s)
 
 int gmaco_collect(gmaco_engine* h, gmaco_run_result* result, double* travel_times_s, int32_t* retired_vid,
                   int32_t* retired_node, int32_t retired_cap) {
+  NvtxRange nvtx_(__func__);
   if (!h || !result) return GMACO_EVALIDATION;
   return guarded(h, [&] { collect(h, result, travel_times_s, retired_vid, retired_node, retired_cap); });
 }
 
 int gmaco_get_pheromone(gmaco_engine* h, int64_t* tau) {
+  NvtxRange nvtx_(__func__);
   if (!h || !tau) return GMACO_EVALIDATION;
   return guarded(h, [&] { scatter_slots(h, download(h->w.tau, h->M), tau); });
 }
 
 int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h || !tau) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -2110,6 +2130,7 @@ int gmaco_get_occupancy(gmaco_engine* h, int32_t* occ) {
 }
 
 int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
+  NvtxRange nvtx_(__func__);
   if (!h || !v) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const DevVehicles& d = h->w.v;
@@ -2265,6 +2286,7 @@ PackDesc arm_slot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slo
 extern "C" {
 
 int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
+  NvtxRange nvtx_(__func__);
   if (h) h->ctl_valid = false;
   if (!h || !fields || slot < 0 || slot > 1) return GMACO_EVALIDATION;
   return guarded(h, [&] {
@@ -2307,6 +2329,7 @@ int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32
 }
 
 int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, int32_t slot) {
+  NvtxRange nvtx_(__func__);
   if (!h || !fields || slot < 0 || slot > 1) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     auto& rs = h->rslot[slot];
@@ -2317,6 +2340,7 @@ int gmaco_vehicles_enqueue(gmaco_engine* h, const gmaco_vehicle_view* fields, in
 }
 
 int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view* view) {
+  NvtxRange nvtx_(__func__);
   if (!h || !view || slot < 0 || slot > 1) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     auto& rs = h->rslot[slot];
@@ -2341,6 +2365,7 @@ int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view*
 }
 
 int gmaco_debug_check_redzones(gmaco_engine* h, int64_t* corrupted) {
+  NvtxRange nvtx_(__func__);
   if (!h || !corrupted) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     CK(cudaStreamSynchronize(h->stream));
@@ -2371,6 +2396,7 @@ int gmaco_signal_count(gmaco_engine* h, int32_t* out) {
 }
 
 int gmaco_get_signals(gmaco_engine* h, const gmaco_signal_view* v, int64_t cap) {
+  NvtxRange nvtx_(__func__);
   if (!h || !v) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const DevSignals& d = h->w.s;
@@ -2433,6 +2459,7 @@ int gmaco_get_counters(gmaco_engine* h, gmaco_counters* out) {
 
 int gmaco_route_query(gmaco_engine* h, int32_t vid, int32_t planned, int32_t* out_edges, int32_t cap,
                       int32_t* out_len) {
+  NvtxRange nvtx_(__func__);
   if (!h || !out_len) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     const DevWorld& w = h->w;
@@ -2470,6 +2497,7 @@ int gmaco_route_query(gmaco_engine* h, int32_t vid, int32_t planned, int32_t* ou
 int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int32_t* current, const int32_t* dest,
                     const uint64_t* rng_entity, const uint64_t* rng_step, int64_t n_t, int32_t* out_next,
                     int32_t* out_via, uint8_t* out_deviated) {
+  NvtxRange nvtx_(__func__);
   if (!h) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     if (count < 0) throw ValidationError("next_node: negative count");
@@ -2545,6 +2573,7 @@ void build_bench_graph(gmaco_engine* h, int64_t flush_bytes, int mode) {
 }
 
 int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, double* walk_ms, double* step_ms) {
+  NvtxRange nvtx_(__func__);
   if (!h || steps < 0) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     refresh_ctl(h);
