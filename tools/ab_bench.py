@@ -22,7 +22,13 @@ engine.load(lib)
 kw = {}
 if len(sys.argv) > 5:
     kw["vehicles"] = int(sys.argv[5])
-net, cfg, dist, keep = workloads.CONFIGS[config](seed=1, max_steps=warmup + steps + 1, **kw)
+if config.startswith("ref:"):  # ref:ALGORITHM:CONFIG -- a reference algorithm on a grid config (bench.py)
+    import bench
+    _, alg, cname = config.split(":")
+    net, cfg = bench.ref_algorithm_world(alg, cname, 1, max_steps=100000)
+    dist, keep = net.grid_distance(), None
+else:
+    net, cfg, dist, keep = workloads.CONFIGS[config](seed=1, max_steps=warmup + steps + 1, **kw)
 e = engine.Engine(net, cfg, dist)
 e.step(warmup)
 c0 = e.counters()

@@ -27,6 +27,10 @@ METRICS = [
     ("smsp__inst_executed.sum", "warp_instructions"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads_per_instr"),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem_throughput_%"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "l1_lsu_wavefronts_%"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "l1_throughput_%"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_throughput_%"),
+    ("sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "fp64_pipe_%"),
 ]
 
 
@@ -57,8 +61,10 @@ def report(path):
     for row in rows[2:]:
         k = {"kernel": row[hdr.index("Kernel Name")]}
         for m, name in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
+            hits = [j for j, x in enumerate(hdr) if x == m] + [j for j, x in enumerate(hdr) if x.endswith("." + m)]
+            hits = [j for j in hits if row[j] not in ("", "no data")]
+            if hits:
+                i = hits[0]
                 k[name] = f"{row[i]} {units[i]}".strip()
         kernels.append(k)
     src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
