@@ -374,6 +374,13 @@ struct DevBuffers {
   }
   template <class T>
   T* filled(size_t n, T value) {
+    const size_t bytes = n * sizeof(T);
+    if (arena && bytes && bytes <= kArenaMax) {  // straight into the shadow (no temporary)
+      T* d = static_cast<T*>(carve(bytes, nullptr));
+      T* sh = reinterpret_cast<T*>(shadow_of(d));
+      std::fill(sh, sh + n, value);
+      return d;
+    }
     std::vector<T> h(n, value);
     return upload(h);
   }
@@ -771,7 +778,14 @@ void ensure_device(gmaco_engine* h) {
   CK(cudaSetDevice(h->device));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->buf.stream = h->stream;
-  CK(configure_kernels());
+  static std::mutex mu;  // kernel attributes are per device and process: set them once
+  static std::vector<char> configured;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)configured.size() <= h->device) configured.resize(h->device + 1, 0);
+  if (!configured[h->device]) {
+    CK(configure_kernels());
+    configured[h->device] = 1;
+  }
 }
 
 // Exact distances dist(x -> dests[t]) for every node x on the device
@@ -1049,6 +1063,8 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   std::vector<int32_t> col(M, -1), slot_from(M, -1), bind(M, -1), key(M, -1);
   std::vector<int64_t> slen(M, 0);
   std::vector<double> eta(M, 0.0);
+  int64_t last_len = -1;  // eta depends on the length only: lattices have one (one pow call)
+  double last_eta = 0.0;
   for (int32_t s = 0; s < M; ++s) {
     const int32_t e = h->slot_edge[s];
     if (e < 0) continue;
@@ -1056,8 +1072,12 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     slot_from[s] = g.from[e];
     slen[s] = g.len[e];
     key[s] = dd->kind == GMACO_DIST_GRID ? ((g.to[e] / dd->grid_cols) << 16) | (g.to[e] % dd->grid_cols) : g.to[e];
-    const double vis = 1.0 / (static_cast<double>(g.len[e]) / 1000.0);  // routing.cpp:92
-    eta[s] = std::pow(vis, c.routing.aco_beta);
+    if (g.len[e] != last_len) {
+      const double vis = 1.0 / (static_cast<double>(g.len[e]) / 1000.0);  // routing.cpp:92
+      last_eta = std::pow(vis, c.routing.aco_beta);
+      last_len = g.len[e];
+    }
+    eta[s] = last_eta;
   }
   // signals (engine.cpp:124-136, make_signal_state signals.cpp:29-46)
   std::vector<int32_t> sig_of_node(n, -1), lanes_s;
@@ -1303,13 +1323,18 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     // distance, dealt round-robin over the CTAs so every CTA (and SM) holds a
     // mix of long and short colonies; results do not depend on the order.
     const int32_t Cc = dd->grid_cols;
-    std::vector<int32_t> ord(V);
-    for (int32_t i = 0; i < V; ++i) ord[i] = i;
-    auto dist = [&](int32_t i) {
+    // stable counting sort by decreasing Manhattan distance (O(V + rows + cols))
+    std::vector<int32_t> dist(V), ord(V);
+    int32_t dmax = 0;
+    for (int32_t i = 0; i < V; ++i) {
       const int32_t o = sp.origin[i], t = sp.dest[i];
-      return std::abs(o / Cc - t / Cc) + std::abs(o % Cc - t % Cc);
-    };
-    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return dist(a) > dist(b); });
+      dist[i] = std::abs(o / Cc - t / Cc) + std::abs(o % Cc - t % Cc);
+      dmax = std::max(dmax, dist[i]);
+    }
+    std::vector<int32_t> at(dmax + 2, 0);
+    for (int32_t i = 0; i < V; ++i) at[dmax - dist[i] + 1]++;
+    for (int32_t k = 0; k <= dmax; ++k) at[k + 1] += at[k];
+    for (int32_t i = 0; i < V; ++i) ord[at[dmax - dist[i]]++] = i;
     // vehicles per CTA of the launch (launch_step): staged tables pack 256/K;
     // otherwise one vehicle per CTA when K fills whole warps (then the order
     // is longest-first: CTAs start in index order, LPT packing of the waves)
@@ -1588,16 +1613,23 @@ int64_t run_steps(gmaco_engine* h, int64_t steps, bool need_count = true) {
   return h->ctl_host->step - start;
 }
 
+void read_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v);
+
 void collect(gmaco_engine* h, gmaco_run_result* r, double* travel, int32_t* rvid, int32_t* rnode, int32_t cap) {
-  refresh_ctl(h);
   const DevWorld& w = h->w;
   const int32_t V = w.p.V;
-  auto state = download(w.v.state, V);
-  auto arrive = download(w.v.arrive, V);
-  auto depart = download(w.v.depart, V);
-  auto queued = download(w.v.queued, V);
-  auto decisions = download(w.v.decisions, V);
-  auto at_node = download(w.v.at_node, V);
+  // one gather + one sync for the six fields and the control block
+  std::vector<uint8_t> state(V);
+  std::vector<int64_t> arrive(V), depart(V), queued(V);
+  std::vector<int32_t> decisions(V), at_node(V);
+  gmaco_vehicle_view view{};
+  view.state = state.data();
+  view.arrive_step = arrive.data();
+  view.depart_step = depart.data();
+  view.queued_steps = queued.data();
+  view.decisions = decisions.data();
+  view.at_node = at_node.data();
+  read_vehicles(h, &view);
   const DevCtl& c = *h->ctl_host;
   gmaco_run_result out{};
   out.steps_executed = c.step;
@@ -1833,6 +1865,80 @@ static void h2d(gmaco_engine* h, void* dst, const void* src, size_t bytes) {
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
 }
+
+namespace {
+// The requested vehicle fields (and the control block) in one gather into
+// pinned staging memory plus one sync (gmaco_get_vehicles, collect).
+void read_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
+    const DevVehicles& d = h->w.v;
+    const size_t V = h->w.p.V;
+    // requested fields: async copies into one pinned staging buffer, one
+    // stream sync, then host copies out (one round trip instead of one per field)
+    std::vector<std::pair<void*, size_t>> outs;  // (user dst, staging offset)
+    std::vector<std::pair<const void*, size_t>> srcs;
+    size_t total = 0;
+    auto plan = [&](void* dst, const void* src, size_t elem) {
+      if (!dst) return;
+      outs.emplace_back(dst, total);
+      srcs.emplace_back(src, V * elem);
+      total += (V * elem + 15) & ~size_t(15);
+    };
+    plan(v->origin, d.origin, 4);
+    plan(v->dest, d.dest, 4);
+    plan(v->advance_mm, d.advance, 8);
+    plan(v->state, d.state, 1);
+    plan(v->at_node, d.at_node, 4);
+    plan(v->progress_mm, d.progress, 8);
+    plan(v->overshoot_mm, d.overshoot, 8);
+    plan(v->queued_phase, d.queued_phase, 4);
+    plan(v->queue_joined_step, d.joined, 8);
+    plan(v->depart_step, d.depart, 8);
+    plan(v->arrive_step, d.arrive, 8);
+    plan(v->latency_debt_us, d.latency_debt, 8);
+    plan(v->driving_steps, d.driving, 8);
+    plan(v->queued_steps, d.queued, 8);
+    plan(v->latency_steps, d.lat_steps, 8);
+    plan(v->decisions, d.decisions, 4);
+    plan(v->deviations, d.deviations, 4);
+    plan(v->path_length_mm, d.path_len_mm, 8);
+    const size_t oe_off = total;
+    if (v->on_edge) total += V * 4;
+    total += 16;  // never empty: the control block copy + sync always run
+    {
+      if (h->stage_bytes < total) {
+        PinnedPool::give(h->stage);
+        h->stage = nullptr;
+        h->stage = PinnedPool::take(total);
+        h->stage_bytes = total;
+      }
+      char* st = static_cast<char*>(h->stage);
+      char* st_dev = nullptr;
+      void* ctl_dev = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), h->stage, 0));
+      CK(cudaHostGetDevicePointer(&ctl_dev, h->ctl_host, 0));
+      // one gather kernel into mapped pinned memory; the control block rides
+      // along, so the host mirror is current after the single sync
+      PackDesc pd;
+      for (size_t i = 0; i < outs.size(); ++i) pd.f[pd.n++] = PackField{srcs[i].first, st_dev + outs[i].second, srcs[i].second};
+      if (v->on_edge) pd.f[pd.n++] = PackField{d.on_edge, st_dev + oe_off, V * 4};
+      pd.f[pd.n++] = PackField{h->ctl, ctl_dev, sizeof(DevCtl)};
+      CK(launch_pack(pd, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      h->pending = false;
+      h->ctl_valid = true;
+      if (h->ctl_host->error) throw std::runtime_error("device path buffer overflow");
+      for (size_t i = 0; i < outs.size(); ++i) std::memcpy(outs[i].first, st + outs[i].second, srcs[i].second);
+      if (v->on_edge) {
+        const int32_t* oe = reinterpret_cast<const int32_t*>(st + oe_off);
+        for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
+      }
+    }
+    if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
+      for (size_t i = 0; i < V; ++i)
+        v->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+    }
+  }
+}  // namespace
 
 // ============================================================================
 // C ABI
@@ -2132,75 +2238,7 @@ int gmaco_get_occupancy(gmaco_engine* h, int32_t* occ) {
 int gmaco_get_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
   NvtxRange nvtx_(__func__);
   if (!h || !v) return GMACO_EVALIDATION;
-  return guarded(h, [&] {
-    const DevVehicles& d = h->w.v;
-    const size_t V = h->w.p.V;
-    // requested fields: async copies into one pinned staging buffer, one
-    // stream sync, then host copies out (one round trip instead of one per field)
-    std::vector<std::pair<void*, size_t>> outs;  // (user dst, staging offset)
-    std::vector<std::pair<const void*, size_t>> srcs;
-    size_t total = 0;
-    auto plan = [&](void* dst, const void* src, size_t elem) {
-      if (!dst) return;
-      outs.emplace_back(dst, total);
-      srcs.emplace_back(src, V * elem);
-      total += (V * elem + 15) & ~size_t(15);
-    };
-    plan(v->origin, d.origin, 4);
-    plan(v->dest, d.dest, 4);
-    plan(v->advance_mm, d.advance, 8);
-    plan(v->state, d.state, 1);
-    plan(v->at_node, d.at_node, 4);
-    plan(v->progress_mm, d.progress, 8);
-    plan(v->overshoot_mm, d.overshoot, 8);
-    plan(v->queued_phase, d.queued_phase, 4);
-    plan(v->queue_joined_step, d.joined, 8);
-    plan(v->depart_step, d.depart, 8);
-    plan(v->arrive_step, d.arrive, 8);
-    plan(v->latency_debt_us, d.latency_debt, 8);
-    plan(v->driving_steps, d.driving, 8);
-    plan(v->queued_steps, d.queued, 8);
-    plan(v->latency_steps, d.lat_steps, 8);
-    plan(v->decisions, d.decisions, 4);
-    plan(v->deviations, d.deviations, 4);
-    plan(v->path_length_mm, d.path_len_mm, 8);
-    const size_t oe_off = total;
-    if (v->on_edge) total += V * 4;
-    total += 16;  // never empty: the control block copy + sync always run
-    {
-      if (h->stage_bytes < total) {
-        PinnedPool::give(h->stage);
-        h->stage = nullptr;
-        h->stage = PinnedPool::take(total);
-        h->stage_bytes = total;
-      }
-      char* st = static_cast<char*>(h->stage);
-      char* st_dev = nullptr;
-      void* ctl_dev = nullptr;
-      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), h->stage, 0));
-      CK(cudaHostGetDevicePointer(&ctl_dev, h->ctl_host, 0));
-      // one gather kernel into mapped pinned memory; the control block rides
-      // along, so the host mirror is current after the single sync
-      PackDesc pd;
-      for (size_t i = 0; i < outs.size(); ++i) pd.f[pd.n++] = PackField{srcs[i].first, st_dev + outs[i].second, srcs[i].second};
-      if (v->on_edge) pd.f[pd.n++] = PackField{d.on_edge, st_dev + oe_off, V * 4};
-      pd.f[pd.n++] = PackField{h->ctl, ctl_dev, sizeof(DevCtl)};
-      CK(launch_pack(pd, h->stream));
-      CK(cudaStreamSynchronize(h->stream));
-      h->pending = false;
-      h->ctl_valid = true;
-      if (h->ctl_host->error) throw std::runtime_error("device path buffer overflow");
-      for (size_t i = 0; i < outs.size(); ++i) std::memcpy(outs[i].first, st + outs[i].second, srcs[i].second);
-      if (v->on_edge) {
-        const int32_t* oe = reinterpret_cast<const int32_t*>(st + oe_off);
-        for (size_t i = 0; i < V; ++i) v->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
-      }
-    }
-    if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
-      for (size_t i = 0; i < V; ++i)
-        v->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
-    }
-  }, /*stream_ordered=*/true);
+  return guarded(h, [&] { read_vehicles(h, v); }, /*stream_ordered=*/true);
 }
 // The requested vehicle fields of a view, in declaration order:
 // (user destination, device source, element bytes).
