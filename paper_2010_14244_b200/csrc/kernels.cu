@@ -396,57 +396,53 @@ __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_
 // ---------------------------------------------------------------------------
 // B: reference decision kernel (dijkstra / aco / maco), one thread per vehicle
 // ---------------------------------------------------------------------------
+// One vehicle's stage B (engine.cpp:175-217): activation, the routing
+// decision, its bookkeeping; adds to the block's counters.
 template <int DK>
-__global__ void __launch_bounds__(256) k_decide(DevWorld w) {
-  if (skip_step(w.ctl)) return;
-  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
-  __shared__ long long red[32];
-  // sharded: this rank decides vehicles [shard_lo, shard_hi); the others'
-  // records arrive with the exchange (k_apply_remote)
-  const int32_t vid = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t step = w.ctl->step;
-  long long decided = 0, cands = 0, degs = 0;
-  if (vid < w.p.shard_hi) {
-    const DevVehicles& v = w.v;
-    if (w.p.sharded) v.dec_rec[vid] = -1;
-    uint8_t st = v.state[vid];
-    if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
-      st = kAtNode;
-      v.state[vid] = kAtNode;
-      v.at_node[vid] = v.origin[vid];
-    }
-    if (w.p.need_positions) v.dflag[vid] = 0;
-    if (st == kAtNode) {
-      const int32_t x = v.at_node[vid];
-      const Target<DK> t(w.d, v.dest[vid]);
-      int32_t slot = -1;
-      bool dev = false;
-      if (w.p.algorithm == 0) {
-        slot = dijkstra_pick<DK>(w.g, t, x);
+__device__ __forceinline__ void decide_vehicle(const DevWorld& w, int32_t vid, int64_t step, long long& decided,
+                                               long long& cands, long long& degs) {
+  const DevVehicles& v = w.v;
+  if (w.p.sharded) v.dec_rec[vid] = -1;
+  uint8_t st = v.state[vid];
+  if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+    st = kAtNode;
+    v.state[vid] = kAtNode;
+    v.at_node[vid] = v.origin[vid];
+  }
+  if (w.p.need_positions) v.dflag[vid] = 0;
+  if (st != kAtNode) return;
+  const int32_t x = v.at_node[vid];
+  const Target<DK> t(w.d, v.dest[vid]);
+  int32_t slot = -1;
+  bool dev = false;
+  if (w.p.algorithm == 0) {
+    slot = dijkstra_pick<DK>(w.g, t, x);
+  } else {
+    const Row r = scan_row<DK>(w.g, t, x);
+    degs += r.deg;
+    const uint32_t cand = (w.p.progress_filter && r.closer) ? r.closer : r.reach;
+    if (cand) {
+      cands += __popc(cand);
+      if (w.p.algorithm == 1) {
+        const double u = to_unit(draw(w.p.seed, 5, (uint64_t)vid, (uint64_t)step));
+        slot = roulette_pick(w.weight, r.first, cand, u);
       } else {
-        const Row r = scan_row<DK>(w.g, t, x);
-        degs += r.deg;
-        const uint32_t cand = (w.p.progress_filter && r.closer) ? r.closer : r.reach;
-        if (cand) {
-          cands += __popc(cand);
-          if (w.p.algorithm == 1) {
-            const double u = to_unit(draw(w.p.seed, 5, (uint64_t)vid, (uint64_t)step));
-            slot = roulette_pick(w.weight, r.first, cand, u);
-          } else {
-            slot = maco_pick(w, r.first, cand, w.ctl->n_t, &dev);
-          }
-        }
-      }
-      if (slot < 0) {
-        v.state[vid] = kRetired;  // engine.cpp:202-205
-        if (w.p.sharded) v.dec_rec[vid] = -2;
-      } else {
-        take_edge(w, vid, slot, dev, x);
-        if (w.p.need_positions) v.dflag[vid] = 1;
-        decided = 1;
+        slot = maco_pick(w, r.first, cand, w.ctl->n_t, &dev);
       }
     }
   }
+  if (slot < 0) {
+    v.state[vid] = kRetired;  // engine.cpp:202-205
+    if (w.p.sharded) v.dec_rec[vid] = -2;
+  } else {
+    take_edge(w, vid, slot, dev, x);
+    if (w.p.need_positions) v.dflag[vid] = 1;
+    decided = 1;
+  }
+}
+
+__device__ __forceinline__ void flush_decide_counters(const DevWorld& w, long long decided, long long cands,
+                                                      long long degs, long long* red) {
   const long long d = block_sum(decided, red);
   const long long c = block_sum(cands, red);
   const long long g = block_sum(degs, red);
@@ -459,6 +455,20 @@ __global__ void __launch_bounds__(256) k_decide(DevWorld w) {
     atomicAdd((unsigned long long*)&w.ctl->candidates, (unsigned long long)c);
     atomicAdd((unsigned long long*)&w.ctl->degree_sum, (unsigned long long)g);
   }
+}
+
+template <int DK>
+__global__ void __launch_bounds__(256) k_decide(DevWorld w) {
+  if (skip_step(w.ctl)) return;
+  if (blockIdx.x == 0 && w.p.prefetch) prefetch_tail_state(w);
+  __shared__ long long red[32];
+  // sharded: this rank decides vehicles [shard_lo, shard_hi); the others'
+  // records arrive with the exchange (k_apply_remote)
+  const int32_t vid = w.p.shard_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t step = w.ctl->step;
+  long long decided = 0, cands = 0, degs = 0;
+  if (vid < w.p.shard_hi) decide_vehicle<DK>(w, vid, step, decided, cands, degs);
+  flush_decide_counters(w, decided, cands, degs, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -2600,7 +2610,7 @@ __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
 // grid.sync() orders E3 after E2 and F+G after E3.  Launched with the
 // cooperative attribute, which guarantees co-residency of the grid.
 // ---------------------------------------------------------------------------
-template <bool kFusedMotion>
+template <bool kFusedMotion, int kDecideDK>
 __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
   if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
@@ -2611,6 +2621,16 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const DevParams& p = w.p;
+  if (kDecideDK >= 0) {
+    // reference algorithms, unsharded: stage B in the same launch (one kernel
+    // per step); decisions never see each other (engine.cpp:197-198)
+    const int64_t step = w.ctl->step;
+    long long decided = 0, cands = 0, degs = 0;
+    for (int64_t vid = gtid; vid < p.V; vid += gstride)
+      decide_vehicle<kDecideDK < 0 ? 0 : kDecideDK>(w, (int32_t)vid, step, decided, cands, degs);
+    flush_decide_counters(w, decided, cands, degs, red);
+    grid.sync();
+  }
   if (kFusedMotion) {
     if (p.sharded) {
       // other ranks' vehicles (their decision records arrived with the
@@ -2757,10 +2777,20 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   for (int64_t s = gtid; s < w.g.M; s += gstride)
     if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
   m = block_max(m, smax);
-  if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ_acc, m);
-  if (threadIdx.x == 0) trace_max(w.ctl, 6);
-  grid.sync();
-  if (gtid == 0) finalize_step(w);
+  // the last block to finish finalizes the step (no grid barrier)
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
+    trace_max(w.ctl, 6);
+    __threadfence();
+    is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    finalize_step(w);
+    __threadfence();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2881,9 +2911,16 @@ int coop_tail_blocks(const DevWorld& w, int device) {
   int per_sm = 0, sms = 0, coop = 0;
   if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device) != cudaSuccess || !coop) return 0;
   // the variant that will be launched (colony worlds run the fused one)
-  const cudaError_t oe = w.p.algorithm == 4
-                             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<true>, kTailCoop, 0)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<false>, kTailCoop, 0);
+  cudaError_t oe;
+  if (w.p.algorithm == 4) {
+    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<true, -1>, kTailCoop, 0);
+  } else {  // the variants a reference-algorithm step may launch (with / without the fused stage B)
+    int a = 0, b = 0, c = 0;
+    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_tail_coop<false, -1>, kTailCoop, 0);
+    if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tail_coop<false, 0>, kTailCoop, 0);
+    if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_tail_coop<false, 1>, kTailCoop, 0);
+    per_sm = std::min(a, std::min(b, c));
+  }
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   // (colony worlds: slots and signals share one pass, see k_tail_coop)
@@ -3287,6 +3324,13 @@ void colony_shape(int ants, int* threads, int* vpb) {
   *vpb = t / ants;
 }
 
+// Reference algorithms run stage B inside the cooperative tail (one launch
+// per step) unless the step is split around an exchange (sharding) or the
+// device has no cooperative launch.
+static bool fuse_decide(const DevWorld& w, const StepResources& r) {
+  return w.p.algorithm != 4 && r.coop_blocks > 0 && r.part == 0 && !w.p.sharded;
+}
+
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end) {
   const int V = w.p.V, S = w.p.S, n = w.g.n;
@@ -3361,7 +3405,7 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
       else
         k_colony<0, false><<<grid, threads, 0, st>>>(w);
     }
-  } else {
+  } else if (!fuse_decide(w, r)) {
     if (w.d.kind == 1)
       k_decide<1><<<blocks_for(V, 256), 256, 0, st>>>(w);
     else
@@ -3397,7 +3441,11 @@ tail:
     at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = w.p.pdl ? 2 : 1;
-    return fused ? cudaLaunchKernelEx(&lc, k_tail_coop<true>, w) : cudaLaunchKernelEx(&lc, k_tail_coop<false>, w);
+    if (fused) return cudaLaunchKernelEx(&lc, k_tail_coop<true, -1>, w);
+    if (fuse_decide(w, r))  // stage B inside the cooperative tail: one launch per step
+      return w.d.kind == 1 ? cudaLaunchKernelEx(&lc, k_tail_coop<false, 1>, w)
+                           : cudaLaunchKernelEx(&lc, k_tail_coop<false, 0>, w);
+    return cudaLaunchKernelEx(&lc, k_tail_coop<false, -1>, w);
   }
   if (S > 0) k_signals<<<blocks_for(S, kTail), kTail, 0, st>>>(w);
   if (!fused) k_move<<<blocks_for(V, kTail), kTail, 0, st>>>(w);
@@ -3418,6 +3466,7 @@ tail:
 // Engine kernels enqueued per step by launch_step (library kernels such as
 // the CUB scan and NCCL collectives are not counted).
 int kernels_per_step(const DevWorld& w, const StepResources& r) {
+  if (fuse_decide(w, r)) return 1;  // k_tail_coop with stage B
   int k = 1;                 // stage-B walk / decide
   if (w.p.ant_queue) k += 2; // k_colony_pro + k_colony_epi around k_colony_q
   if (w.tt.rec) k += 1;      // k_tt_refresh
