@@ -648,8 +648,11 @@ static int32_t route_one(og_world* w, int algorithm, int32_t cur, int32_t dest, 
 /* Walks one ant from `start`; writes its edges to tour (if non-NULL) and
  * returns the hop count; *cost is INF64 for a failed ant.  *first_ok is set
  * when hop 0 had a candidate. */
-static int32_t ant_walk(og_world* w, int32_t vid, int32_t ant, int32_t start, int32_t dest,
-                        int64_t* cost, int32_t* tour, int* first_ok, int count) {
+/* Work counters of one planning thread (summed into w->ctr in vid order). */
+typedef struct { int64_t ant_steps, candidates, degree_sum, vehicle_routes; } og_ctr_local;
+
+static int32_t ant_walk(const og_world* w, int32_t vid, int32_t ant, int32_t start, int32_t dest,
+                        int64_t* cost, int32_t* tour, int* first_ok, og_ctr_local* count) {
   const gmaco_colony_params* cp = &w->cfg.colony;
   const int pf = w->cfg.routing.progress_filter;
   const int32_t max_hops = cp->max_hops > 0 ? cp->max_hops : w->g.n - 1;
@@ -681,7 +684,7 @@ static int32_t ant_walk(og_world* w, int32_t vid, int32_t ant, int32_t start, in
     int32_t e = pce[pick];
     x = pcn[pick];
     if (pcn != cn) { free(pcn); free(pce); }
-    if (count) { w->ctr.ant_steps++; w->ctr.candidates += nc; w->ctr.degree_sum += scanned; }
+    if (count) { count->ant_steps++; count->candidates += nc; count->degree_sum += scanned; }
     c += w->ecost[e];
     if (tour) tour[hops] = e;
     hops++;
@@ -1084,7 +1087,15 @@ static void decide(og_world* w, int32_t vid) { /* engine.cpp:175-217 */
 /* Colony stage B (north-star extension): K ants per planning vehicle, best
  * tour by (cost, ant), winner replayed to materialize its tour; vehicles at
  * a node take the winner's first hop. */
-static void colony_plan(og_world* w, int32_t vid) {
+/* Colony stage B for one vehicle: its K ants' walks, the winner's tour as
+ * the vehicle's plan.  Touches only the vehicle's own state and plan, so the
+ * vehicles of a step are planned on all host threads (colony_stage); the
+ * shared effects -- counters, deposits, the decision's take_edge -- are
+ * returned and applied in ascending vid by the caller. */
+static void colony_plan_vehicle(og_world* w, int32_t vid, og_ctr_local* ctr, int64_t* dep_amount,
+                                int32_t* decide_edge) {
+  *dep_amount = 0;
+  *decide_edge = -1;
   activate(w, vid);
   if (vid < w->vlo || vid >= w->vhi) return;
   w->dec_rec[vid] = -1;
@@ -1102,7 +1113,7 @@ static void colony_plan(og_world* w, int32_t vid) {
   for (int32_t a = 0; a < cp->ants; ++a) {
     int64_t cost;
     int ok;
-    ant_walk(w, vid, a, start, w->dest[vid], &cost, NULL, &ok, 1);
+    ant_walk(w, vid, a, start, w->dest[vid], &cost, NULL, &ok, ctr);
     if (a == 0) first_ok = ok;
     if (cost < best) { best = cost; winner = a; }
   }
@@ -1121,22 +1132,86 @@ static void colony_plan(og_world* w, int32_t vid) {
   if (pl->cap < max_hops + 1) { pl->cap = max_hops + 1; pl->a = realloc(pl->a, sizeof(int32_t) * (size_t)pl->cap); }
   int64_t cost;
   int ok;
-  pl->n = ant_walk(w, vid, winner, start, w->dest[vid], &cost, pl->a, &ok, 0);
+  pl->n = ant_walk(w, vid, winner, start, w->dest[vid], &cost, pl->a, &ok, NULL);
   w->plan_step[vid] = w->step;
   w->plan_done[vid] = pl->n > 0 && w->g.to[pl->a[pl->n - 1]] == w->dest[vid];
-  w->ctr.vehicle_routes++;
+  ctr->vehicle_routes++;
   if (w->plan_done[vid] && w->cfg.colony.deposit == GMACO_DEPOSIT_BEST_TOUR) {
     /* best-tour deposit: deposit_amount(tour length) per tour edge, summed
      * exactly per edge; applied (sum-then-clamp) in stage F */
     int64_t len = 0;
     for (int32_t i = 0; i < pl->n; ++i) len += w->g.len[pl->a[i]];
-    const int64_t amount = og_deposit_amount(len, &w->cfg.pheromone);
-    for (int32_t i = 0; i < pl->n; ++i) w->dep[pl->a[i]] += amount;
+    *dep_amount = og_deposit_amount(len, &w->cfg.pheromone);
   }
-  if (deciding) {
-    take_edge(w, vid, pl->a[0], 0);
-    w->dec_rec[vid] = pl->a[0];
+  if (deciding) *decide_edge = pl->a[0];
+}
+
+typedef struct {
+  og_world* w;
+  int64_t* dep_amount;
+  int32_t* decide_edge;
+  og_ctr_local ctr[64];
+  int32_t slots, cursor; /* threads registered; next vehicle */
+  pthread_mutex_t mu;
+} colony_job;
+
+static void* colony_worker(void* arg) {
+  colony_job* j = (colony_job*)arg;
+  pthread_mutex_lock(&j->mu);
+  og_ctr_local* ctr = &j->ctr[j->slots++];
+  pthread_mutex_unlock(&j->mu);
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    const int32_t lo = j->cursor;
+    if (j->cursor < j->w->V) j->cursor += 16;
+    pthread_mutex_unlock(&j->mu);
+    if (lo >= j->w->V) return NULL;
+    const int32_t hi = lo + 16 < j->w->V ? lo + 16 : j->w->V;
+    for (int32_t vid = lo; vid < hi; ++vid) colony_plan_vehicle(j->w, vid, ctr, &j->dep_amount[vid], &j->decide_edge[vid]);
   }
+}
+
+/* Colony stage B for the whole fleet: per-vehicle planning on all host
+ * threads, then the shared effects in ascending vid (deposits are exact
+ * integer sums, so their order is immaterial; take_edge keeps vid order). */
+static void colony_stage(og_world* w) {
+  const int32_t V = w->V;
+  colony_job j;
+  memset(&j, 0, sizeof j);
+  j.w = w;
+  j.dep_amount = calloc((size_t)(V ? V : 1), sizeof(int64_t));
+  j.decide_edge = malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+  pthread_mutex_init(&j.mu, NULL);
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  if ((int64_t)V * (w->cfg.colony.ants > 0 ? w->cfg.colony.ants : 1) < 4096) nt = 1; /* small worlds: no threads */
+  if (nt == 1) {
+    colony_worker(&j);
+  } else {
+    pthread_t th[64];
+    for (long i = 0; i < nt; ++i) pthread_create(&th[i], NULL, colony_worker, &j);
+    for (long i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+  }
+  pthread_mutex_destroy(&j.mu);
+  for (int i = 0; i < 64; ++i) {
+    w->ctr.ant_steps += j.ctr[i].ant_steps;
+    w->ctr.candidates += j.ctr[i].candidates;
+    w->ctr.degree_sum += j.ctr[i].degree_sum;
+    w->ctr.vehicle_routes += j.ctr[i].vehicle_routes;
+  }
+  for (int32_t vid = 0; vid < V; ++vid) {
+    if (j.dep_amount[vid]) {
+      const ivec* pl = &w->plan[vid];
+      for (int32_t i = 0; i < pl->n; ++i) w->dep[pl->a[i]] += j.dep_amount[vid];
+    }
+    if (j.decide_edge[vid] >= 0) {
+      take_edge(w, vid, j.decide_edge[vid], 0);
+      w->dec_rec[vid] = j.decide_edge[vid];
+    }
+  }
+  free(j.dep_amount);
+  free(j.decide_edge);
 }
 
 static void assign(og_world* w, int32_t s) { /* engine.cpp:223-239 */
@@ -1316,7 +1391,7 @@ static void step_part1(og_world* w) {
   w->active = count_active(w);
   /* B */
   if (w->cfg.algorithm == GMACO_COLONY)
-    for (int32_t vid = 0; vid < w->V; ++vid) colony_plan(w, vid);
+    colony_stage(w);
   else
     for (int32_t vid = 0; vid < w->V; ++vid) decide(w, vid);
 }

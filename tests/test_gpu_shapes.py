@@ -7,12 +7,12 @@ work counters and sampled best-of-K planned tours.
 
 * C3 exactly: 100x100 grid, 10,000 vehicles, 128 ants (one-vehicle CTAs of
   the lattice walker, multi-word move bits).
-* C5: 256x256 all-signalized grid, the rush-hour Blocks OD (bias 0.8), 64
-  ants, a 5,000-vehicle fleet (the bench's 50k fleet is sampled down so the
-  single-threaded oracle finishes; walker, grid and OD are the bench's).
-* C4: the full 1M-node / 4M-edge random-geometric graph, 64 targets,
-  max_hops 4096, 16 ants, a 2,000-vehicle fleet (per-target candidate rows,
-  BFS row order, ant-queue walker -- built at full size).
+* C5 exactly: 256x256 all-signalized grid, the rush-hour Blocks OD (bias
+  0.8), 64 ants, the bench's 50,000-vehicle fleet.
+* C4 exactly: the 1M-node / 4M-edge random-geometric graph, 64 targets,
+  max_hops 4096, 16 ants, the bench's 100,000-vehicle fleet (per-target
+  candidate rows, BFS row order, longest-band-first queue, ant-queue walker).
+  The oracle plans the vehicles of a step on all host threads.
 * alpha not in {0, 1}: tau^alpha comes from the exact glibc-pow table
   (DevWorld::taupow), so runs are bit-exact, not within-1-ulp.
 
@@ -66,25 +66,21 @@ def test_c3_exact_shape():
     del keep
 
 
-def test_c5_blocks_od_colony():
-    net, cfg, dist, keep = workloads.c5(seed=1, max_steps=10, vehicles=5000)
+def test_c5_exact_shape():
+    net, cfg, dist, keep = workloads.c5(seed=1, max_steps=10)
+    assert cfg.vehicle_count == 50_000
     assert net.node_count == 256 * 256 and cfg.od_pattern == abi.OD_BLOCKS and cfg.od_bias == 0.8
     assert cfg.colony.ants == 64
-    run_pair(net, cfg, dist, 2, 61, "C5")
+    run_pair(net, cfg, dist, 2, 499, "C5")
     del keep
 
 
-@pytest.fixture(scope="module")
-def c4_world():
-    return workloads.c4(seed=1, max_steps=10, vehicles=2000)
-
-
-def test_c4_full_graph_reduced_fleet(c4_world):
-    net, cfg, dist, keep = c4_world
-    assert net.node_count == 1_000_000 and net.edge_count >= 4_000_000
+def test_c4_exact_shape():
+    net, cfg, dist, keep = workloads.c4(seed=1, max_steps=10)
+    assert net.node_count == 1_000_000 and net.edge_count >= 4_000_000 and cfg.vehicle_count == 100_000
     assert cfg.colony.max_hops == 4096 and cfg.colony.ants == 16 and dist.target_count == 64
-    gpu, _ = run_pair(net, cfg, dist, 2, 41, "C4")
-    assert gpu.counters().ant_steps > 2000 * 16 * 100
+    gpu, _ = run_pair(net, cfg, dist, 2, 997, "C4")
+    assert gpu.counters().ant_steps > 100_000 * 16 * 500
 
 
 @pytest.mark.parametrize("alpha", [0.5, 2.0])
