@@ -268,7 +268,7 @@ def ref_algorithm_world(alg: str, config: str, seed: int = 1, max_steps: int = 5
     return net, cfg
 
 
-def reference_algorithms_block(threads: int):
+def reference_algorithms_block(threads: int, alg: str = "maco-p", config: str = "c2", fold: bool = True):
     """SURVEY 8(d)(i)/(iii) on the GPU box, same process: the paper's own
     algorithm (MACO-P, preemptive signals) on C2 end to end through the C ABI
     -- gpu_run's path: gmaco_create with the engine's device SSSP building
@@ -282,7 +282,7 @@ def reference_algorithms_block(threads: int):
     from paper_2010_14244_b200.engine import Engine
     if not O.ref_available():
         return {"unavailable": "oracle/_ref not built"}
-    net, cfg = ref_algorithm_world("maco-p", "c2")
+    net, cfg = ref_algorithm_world(alg, config)
     ours, runs, res = [], [], None
     for _ in range(4):
         torch.cuda.synchronize()
@@ -308,9 +308,11 @@ def reference_algorithms_block(threads: int):
         par.append(time.perf_counter() - t0)
         par_run_ms.append(rp[0].wall_clock_ms)
     seq_s, par_s = float(np.median(seq)), float(np.median(par))
+    R, Cc, sig, V = REF_ALG_SHAPES[config]
     block = {
-        "workload": "C2 network (32x32, signals at every intersection), 1000 vehicles, algorithm maco-p with "
-                    "preemptive signals (the reference's own path), whole run to completion",
+        "workload": f"{config.upper()} network ({R}x{Cc}, {sig} intersections signalized), {V} vehicles, algorithm "
+                    f"{alg} ({'preemptive' if alg == 'maco-p' else 'fixed'} signals; the reference's own path), "
+                    "whole run to completion",
         "identical_to_reference": O.results_identical(res, ref),
         "steps": steps, "decisions": decisions,
         "ours": {"e2e_s": ours_s, "run_s": run_s, "steps_per_sec_e2e": steps / ours_s,
@@ -323,6 +325,8 @@ def reference_algorithms_block(threads: int):
         "speedup_e2e_vs_run": seq_s / ours_s, "speedup_e2e_vs_parallel_run": par_s / ours_s,
         "speedup_run_only_vs_run": float(np.median(seq_run_ms)) / 1e3 / run_s,
     }
+    if not fold:
+        return block
     # (iii) F+G edge kernel: reference fold + evaporation on all host threads
     # over the C3 network with a step's worth of decisions, against this
     # engine's whole stage C..G tail (signals, motion, fold + evaporation) of
@@ -757,6 +761,9 @@ def run_ours(args, rank, world, local):
         line["reference_algorithms"] = reference_algorithms_block(os.cpu_count() or 1)
     if world == 1 and not args.no_cpu_baseline and headline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if world == 1 and not args.no_secondary and args.algorithm != "colony" and args.config in ("c1", "c2"):
+        line["reference_run_comparison"] = reference_algorithms_block(os.cpu_count() or 1, args.algorithm,
+                                                                      args.config, fold=False)
     if world == 1 and not args.no_cpu_baseline and args.algorithm != "colony":
         smp = RefStepSampler(args.algorithm, args.config)
         smp.iteration()

@@ -1540,6 +1540,26 @@ bool launch_direct(gmaco_engine* h) {
 }
 
 int64_t run_steps(gmaco_engine* h, int64_t steps, bool need_count = true) {
+  // reference algorithms: several steps as ONE persistent cooperative launch
+  // (k_run_coop: grid barriers between the stages and steps instead of a
+  // launch per step); it stops by itself at finished()
+  if (steps >= 2 && !h->timing && run_coop_ok(h->w, h->res)) {
+    int64_t start = 0;
+    if (need_count) {
+      if (!h->ctl_valid) refresh_ctl(h);
+      start = h->ctl_host->step;
+      if (h->ctl_host->done) return 0;
+    }
+    unbound_stop(h);
+    CK(launch_run_coop(h->w, h->res, steps, h->stream));
+    h->ctl_valid = false;
+    if (!need_count) {
+      h->pending = true;
+      return -1;
+    }
+    refresh_ctl(h);
+    return h->ctl_host->step - start;
+  }
   if (!need_count && !h->timing) {  // enqueue only: no mirror needed (steps past finished() are no-ops)
     if (steps <= 0) return -1;
     unbound_stop(h);

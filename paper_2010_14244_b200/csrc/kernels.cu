@@ -2610,12 +2610,12 @@ __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
 // grid.sync() orders E3 after E2 and F+G after E3.  Launched with the
 // cooperative attribute, which guarantees co-residency of the grid.
 // ---------------------------------------------------------------------------
-template <bool kFusedMotion, int kDecideDK>
-__global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
-  griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
-  if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
-  cg::grid_group grid = cg::this_grid();
-  if (threadIdx.x == 0) trace_min(w.ctl, 3);
+// One reference-algorithm step on the cooperative grid (stages B..G):
+// optional stage B, C, D, E1 || E2, E3 (+ the MACO fold positions), F+G.
+// kLastBlockFinalize: the last block to finish finalizes the step; else the
+// caller finalizes after a grid barrier (the persistent multi-step kernel).
+template <int kDecideDK, bool kLastBlockFinalize>
+__device__ __forceinline__ void ref_step(const DevWorld& w, cg::grid_group& grid) {
   __shared__ long long red[32];
   __shared__ int32_t smax[32];
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2631,6 +2631,124 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     flush_decide_counters(w, decided, cands, degs, red);
     grid.sync();
   }
+  // Network-wide MACO fold (fold_maco_edge, parallel.cpp:77-92): every
+  // decision's position in ascending-vid order is the exclusive prefix of
+  // dflag (set by stage B).  Block b scans the contiguous vehicle chunk
+  // [c0, c1): its count is published before the first grid barrier, its
+  // positions written before the second (F+G reads them after the third) --
+  // no extra barrier and no library scan.
+  const bool pos_scan = p.need_positions;
+  const int64_t chunk = (p.V + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = min((int64_t)p.V, (int64_t)blockIdx.x * chunk), c1 = min((int64_t)p.V, c0 + chunk);
+  if (pos_scan) {
+    long long cnt = 0;
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) cnt += w.v.dflag[i];
+    cnt = block_sum(cnt, red);
+    if (threadIdx.x == 0) w.v.bsum[blockIdx.x] = (int32_t)cnt;
+  }
+  // C, D, E1 (signals) || E2 (vehicles)
+  long long qt = 0, active = 0, unfinished = 0;
+  for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
+    if (i < p.S)
+      qt += sig_cde1(w, (int32_t)i);
+    else
+      veh_move(w, (int32_t)(i - p.S), active, unfinished);
+  }
+  qt = block_sum(qt, red);
+  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+  active = block_sum(active, red);
+  if (threadIdx.x == 0 && active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
+  unfinished = block_sum(unfinished, red);
+  if (threadIdx.x == 0 && unfinished)
+    atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
+  if (threadIdx.x == 0) trace_max(w.ctl, 4);
+  grid.sync();
+  // E3
+  for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
+  if (pos_scan) {  // positions of this block's chunk (block-uniform loop bounds)
+    long long off = 0;
+    for (int64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += w.v.bsum[b];
+    off = block_sum(off, red);
+    __shared__ long long s_off;
+    __shared__ int32_t wsum[kTailCoop / 32];
+    if (threadIdx.x == 0) s_off = off;
+    __syncthreads();
+    long long base = s_off;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
+      const int64_t i = t0 + threadIdx.x;
+      const int32_t f = i < c1 ? w.v.dflag[i] : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+      if (lane == 0) wsum[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int k = 0; k < kTailCoop / 32; ++k) {
+        before += k < wid ? wsum[k] : 0;
+        total += wsum[k];
+      }
+      if (i < c1) w.v.pos[i] = (int32_t)(base + before + __popc(bal & ((1u << lane) - 1u)));
+      base += total;
+      __syncthreads();
+    }
+  }
+  if (p.siblings_only && (p.algorithm == 2 || p.algorithm == 3)) {
+    grid.sync();
+    for (int64_t u = gtid; u < w.g.n; u += gstride) node_scoped(w, (int32_t)u);
+  }
+  if (threadIdx.x == 0) trace_max(w.ctl, 5);
+  grid.sync();
+  // F + G
+  int32_t m = 0;
+  for (int64_t s = gtid; s < w.g.M; s += gstride)
+    if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
+  m = block_max(m, smax);
+  if (kLastBlockFinalize) {  // the last block to finish finalizes the step (no grid barrier)
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+      if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
+      trace_max(w.ctl, 6);
+      __threadfence();
+      is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+      __threadfence();
+      finalize_step(w);
+      __threadfence();
+    }
+  } else if (threadIdx.x == 0 && m > 0) {
+    atomicMax(&w.ctl->max_occ_acc, m);
+  }
+}
+
+// Persistent run of up to `nsteps` reference-algorithm steps in ONE
+// cooperative launch (gmaco_run / multi-step gmaco_step, unsharded): a step
+// is stage B .. G on the whole grid, then two grid barriers around the
+// finalize; the loop ends at finished() (engine.cpp:146-152) or after nsteps.
+template <int DK>
+__global__ void __launch_bounds__(kTailCoop) k_run_coop(DevWorld w, int64_t nsteps) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t k = 0; k < nsteps && !skip_step(w.ctl); ++k) {  // ctl is read after a barrier: grid-uniform
+    ref_step<DK, false>(w, grid);
+    grid.sync();
+    if (gtid == 0) finalize_step(w);
+    grid.sync();
+  }
+}
+
+template <bool kFusedMotion, int kDecideDK>
+__global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
+  griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
+  if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
+  cg::grid_group grid = cg::this_grid();
+  if (threadIdx.x == 0) trace_min(w.ctl, 3);
+  __shared__ long long red[32];
+  __shared__ int32_t smax[32];
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const DevParams& p = w.p;
   if (kFusedMotion) {
     if (p.sharded) {
       // other ranks' vehicles (their decision records arrived with the
@@ -2705,92 +2823,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     if (gtid == 0) finalize_step(w);
     return;
   }
-  // Network-wide MACO fold (fold_maco_edge, parallel.cpp:77-92): every
-  // decision's position in ascending-vid order is the exclusive prefix of
-  // dflag (set by stage B).  Block b scans the contiguous vehicle chunk
-  // [c0, c1): its count is published before the first grid barrier, its
-  // positions written before the second (F+G reads them after the third) --
-  // no extra barrier and no library scan.
-  const bool pos_scan = p.need_positions;
-  const int64_t chunk = (p.V + gridDim.x - 1) / gridDim.x;
-  const int64_t c0 = min((int64_t)p.V, (int64_t)blockIdx.x * chunk), c1 = min((int64_t)p.V, c0 + chunk);
-  if (pos_scan) {
-    long long cnt = 0;
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) cnt += w.v.dflag[i];
-    cnt = block_sum(cnt, red);
-    if (threadIdx.x == 0) w.v.bsum[blockIdx.x] = (int32_t)cnt;
-  }
-  // C, D, E1 (signals) || E2 (vehicles)
-  long long qt = 0, active = 0, unfinished = 0;
-  for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
-    if (i < p.S)
-      qt += sig_cde1(w, (int32_t)i);
-    else
-      veh_move(w, (int32_t)(i - p.S), active, unfinished);
-  }
-  qt = block_sum(qt, red);
-  if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
-  active = block_sum(active, red);
-  if (threadIdx.x == 0 && active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
-  unfinished = block_sum(unfinished, red);
-  if (threadIdx.x == 0 && unfinished)
-    atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
-  if (threadIdx.x == 0) trace_max(w.ctl, 4);
-  grid.sync();
-  // E3
-  for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
-  if (pos_scan) {  // positions of this block's chunk (block-uniform loop bounds)
-    long long off = 0;
-    for (int64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += w.v.bsum[b];
-    off = block_sum(off, red);
-    __shared__ long long s_off;
-    __shared__ int32_t wsum[kTailCoop / 32];
-    if (threadIdx.x == 0) s_off = off;
-    __syncthreads();
-    long long base = s_off;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
-      const int64_t i = t0 + threadIdx.x;
-      const int32_t f = i < c1 ? w.v.dflag[i] : 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
-      if (lane == 0) wsum[wid] = __popc(bal);
-      __syncthreads();
-      int before = 0, total = 0;
-#pragma unroll
-      for (int k = 0; k < kTailCoop / 32; ++k) {
-        before += k < wid ? wsum[k] : 0;
-        total += wsum[k];
-      }
-      if (i < c1) w.v.pos[i] = (int32_t)(base + before + __popc(bal & ((1u << lane) - 1u)));
-      base += total;
-      __syncthreads();
-    }
-  }
-  if (p.siblings_only && (p.algorithm == 2 || p.algorithm == 3)) {
-    grid.sync();
-    for (int64_t u = gtid; u < w.g.n; u += gstride) node_scoped(w, (int32_t)u);
-  }
-  if (threadIdx.x == 0) trace_max(w.ctl, 5);
-  grid.sync();
-  // F + G
-  int32_t m = 0;
-  for (int64_t s = gtid; s < w.g.M; s += gstride)
-    if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
-  m = block_max(m, smax);
-  // the last block to finish finalizes the step (no grid barrier)
-  __shared__ bool is_last;
-  if (threadIdx.x == 0) {
-    if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
-    trace_max(w.ctl, 6);
-    __threadfence();
-    is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (is_last && threadIdx.x == 0) {
-    __threadfence();
-    finalize_step(w);
-    __threadfence();
-  }
+  ref_step<kDecideDK, true>(w, grid);
 }
 
 // ---------------------------------------------------------------------------
@@ -2915,11 +2948,13 @@ int coop_tail_blocks(const DevWorld& w, int device) {
   if (w.p.algorithm == 4) {
     oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_coop<true, -1>, kTailCoop, 0);
   } else {  // the variants a reference-algorithm step may launch (with / without the fused stage B)
-    int a = 0, b = 0, c = 0;
+    int a = 0, b = 0, c = 0, d = 0, e = 0;
     oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_tail_coop<false, -1>, kTailCoop, 0);
     if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tail_coop<false, 0>, kTailCoop, 0);
     if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_tail_coop<false, 1>, kTailCoop, 0);
-    per_sm = std::min(a, std::min(b, c));
+    if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, k_run_coop<0>, kTailCoop, 0);
+    if (oe == cudaSuccess) oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&e, k_run_coop<1>, kTailCoop, 0);
+    per_sm = std::min(std::min(a, std::min(b, c)), std::min(d, e));
   }
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
@@ -3461,6 +3496,23 @@ tail:
   }
   k_edges<<<blocks_for(w.g.M, kTail), kTail, 0, st>>>(w);
   return cudaGetLastError();
+}
+
+// Persistent multi-step run (k_run_coop) for reference algorithms.
+bool run_coop_ok(const DevWorld& w, const StepResources& r) { return fuse_decide(w, r); }
+
+cudaError_t launch_run_coop(const DevWorld& w, const StepResources& r, int64_t nsteps, cudaStream_t st) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(r.coop_blocks);
+  lc.blockDim = dim3(kTailCoop);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return w.d.kind == 1 ? cudaLaunchKernelEx(&lc, k_run_coop<1>, w, nsteps)
+                       : cudaLaunchKernelEx(&lc, k_run_coop<0>, w, nsteps);
 }
 
 // Engine kernels enqueued per step by launch_step (library kernels such as

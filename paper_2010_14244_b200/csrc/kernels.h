@@ -34,6 +34,10 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
                         cudaEvent_t walk_begin, cudaEvent_t walk_end);
 size_t scan_temp_bytes(int V);
 int kernels_per_step(const DevWorld& w, const StepResources& r);
+// Reference algorithms (unsharded, cooperative launch available): up to
+// nsteps whole steps in one persistent cooperative launch.
+bool run_coop_ok(const DevWorld& w, const StepResources& r);
+cudaError_t launch_run_coop(const DevWorld& w, const StepResources& r, int64_t nsteps, cudaStream_t st);
 cudaError_t configure_kernels();
 int coop_tail_blocks(const DevWorld& w, int device);
 int queue_blocks(const DevWorld& w, int device);
