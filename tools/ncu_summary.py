@@ -45,7 +45,8 @@ def launches(path):
             continue
         v = float(r[vi].replace(",", ""))
         v *= {"ms": 1e3, "us": 1.0, "ns": 1e-3, "usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3}.get(r[ui], 1.0)
-        agg[r[ki].split("(")[0].replace("void ", "").strip()].append(v)
+        name = r[ki].replace("(bool)", "").replace("(int)", "")
+        agg[name.split("(")[0].replace("void ", "").replace("gmaco::", "").strip()].append(v)
     tot = sum(sum(v) for v in agg.values())
     out = ["| kernel | launches | mean us | total us | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
