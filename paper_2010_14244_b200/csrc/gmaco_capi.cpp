@@ -272,6 +272,42 @@ class PinnedPool {
   }
 };
 
+// Process-wide pool of non-blocking streams per device: creating one costs
+// tens of microseconds of gmaco_create; engines created one after another
+// (the bench legs, the tests, a harness matrix) reuse them.
+class StreamPool {
+ public:
+  static cudaStream_t take(int device) {
+    {
+      std::lock_guard<std::mutex> lk(mu());
+      auto& v = free_list()[device];
+      if (!v.empty()) {
+        cudaStream_t s = v.back();
+        v.pop_back();
+        return s;
+      }
+    }
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+  }
+  static void give(int device, cudaStream_t s) {  // the caller has synchronized it
+    if (!s) return;
+    std::lock_guard<std::mutex> lk(mu());
+    free_list()[device].push_back(s);
+  }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::map<int, std::vector<cudaStream_t>>& free_list() {
+    static auto* m = new std::map<int, std::vector<cudaStream_t>>();  // process lifetime
+    return *m;
+  }
+};
+
 // Device allocations of one engine.  Direct mode (default): one cudaMalloc
 // and one synchronous copy per array.  Arena mode (build_world): arrays under
 // kArenaMax are sub-allocated (256-B aligned) from kChunk device chunks and
@@ -590,7 +626,7 @@ struct gmaco_engine {
       if (s.snap_graph) cudaGraphExecDestroy(s.snap_graph);
     }
     buf.release();  // stream-ordered frees need the stream alive
-    if (stream) cudaStreamDestroy(stream);
+    if (stream) StreamPool::give(device, stream);  // (synchronized at the top of the destructor)
     destroy_comm();
   }
   void destroy_comm();
@@ -776,7 +812,7 @@ void ensure_device(gmaco_engine* h) {
   if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
     throw std::runtime_error("no CUDA device available (the engine has no CPU path)");
   CK(cudaSetDevice(h->device));
-  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->stream = StreamPool::take(h->device);
   h->buf.stream = h->stream;
   static std::mutex mu;  // kernel attributes are per device and process: set them once
   static std::vector<char> configured;
