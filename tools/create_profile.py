@@ -17,7 +17,7 @@ config = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 for rep in range(3):
     net, cfg, dist, keep = workloads.CONFIGS[config](seed=1, max_steps=steps + 10)
-    cfg.options.flags = abi.OPT_PROFILE_CREATE if rep == 2 else 0
+    cfg.options.flags = (abi.OPT_PROFILE_CREATE if rep == 2 else 0) | int(os.environ.get("FLAGS", "0"))
     t0 = time.perf_counter()
     e = Engine(net, cfg, dist)
     t1 = time.perf_counter()
