@@ -2610,6 +2610,61 @@ __global__ void __launch_bounds__(256) k_apply_remote_move(DevWorld w) {
 // grid.sync() orders E3 after E2 and F+G after E3.  Launched with the
 // cooperative attribute, which guarantees co-residency of the grid.
 // ---------------------------------------------------------------------------
+// MACO fold positions of the vehicles [c0, c1) of this block: the exclusive
+// prefix of dflag, offset by the decisions of the blocks before it (bsum,
+// published before the last grid barrier).
+__device__ __forceinline__ void chunk_positions(const DevWorld& w, int64_t c0, int64_t c1, long long* red) {
+  long long off = 0;
+  for (int64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += w.v.bsum[b];
+  off = block_sum(off, red);
+  __shared__ long long s_off;
+  __shared__ int32_t wsum[kTailCoop / 32];
+  if (threadIdx.x == 0) s_off = off;
+  __syncthreads();
+  long long base = s_off;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
+    const int64_t i = t0 + threadIdx.x;
+    const int32_t f = i < c1 ? w.v.dflag[i] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kTailCoop / 32; ++k) {
+      before += k < wid ? wsum[k] : 0;
+      total += wsum[k];
+    }
+    if (i < c1) w.v.pos[i] = (int32_t)(base + before + __popc(bal & ((1u << lane) - 1u)));
+    base += total;
+    __syncthreads();
+  }
+}
+
+// The step's end: the running occupancy maximum, and either the last block to
+// finish finalizes the step (no grid barrier) or the caller does after one.
+template <bool kLastBlockFinalize>
+__device__ __forceinline__ void step_end(const DevWorld& w, int32_t m, int32_t* smax) {
+  m = block_max(m, smax);
+  if (kLastBlockFinalize) {
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+      if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
+      trace_max(w.ctl, 6);
+      __threadfence();
+      is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+      __threadfence();
+      finalize_step(w);
+      __threadfence();
+    }
+  } else if (threadIdx.x == 0 && m > 0) {
+    atomicMax(&w.ctl->max_occ_acc, m);
+  }
+}
+
 // One reference-algorithm step on the cooperative grid (stages B..G):
 // optional stage B, C, D, E1 || E2, E3 (+ the MACO fold positions), F+G.
 // kLastBlockFinalize: the last block to finish finalizes the step; else the
@@ -2621,6 +2676,57 @@ __device__ __forceinline__ void ref_step(const DevWorld& w, cg::grid_group& grid
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const DevParams& p = w.p;
+  if (kDecideDK >= 0 && !p.siblings_only) {
+    // Stage B fused (unsharded): TWO grid barriers per step.  Block b decides
+    // the contiguous vehicle chunk [c0, c1) and publishes its decision count;
+    // after barrier 1 it runs C, D, E1 || E2 and writes its chunk's fold
+    // positions; after barrier 2, E3 and F+G run in one pass -- for the
+    // reference algorithms F+G reads nothing E3 writes (no congestion term)
+    // and E3 nothing F+G writes.
+    const int64_t chunk = (p.V + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = min((int64_t)p.V, (int64_t)blockIdx.x * chunk), c1 = min((int64_t)p.V, c0 + chunk);
+    {
+      const int64_t step = w.ctl->step;
+      long long decided = 0, cands = 0, degs = 0;
+      for (int64_t vid = c0 + threadIdx.x; vid < c1; vid += blockDim.x)
+        decide_vehicle<kDecideDK < 0 ? 0 : kDecideDK>(w, (int32_t)vid, step, decided, cands, degs);
+      flush_decide_counters(w, decided, cands, degs, red);  // (its block reductions order the dflag writes)
+      if (p.need_positions) {
+        long long cnt = 0;
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) cnt += w.v.dflag[i];
+        cnt = block_sum(cnt, red);
+        if (threadIdx.x == 0) w.v.bsum[blockIdx.x] = (int32_t)cnt;
+      }
+    }
+    grid.sync();
+    long long qt = 0, active = 0, unfinished = 0;
+    for (int64_t i = gtid; i < (int64_t)p.S + p.V; i += gstride) {
+      if (i < p.S)
+        qt += sig_cde1(w, (int32_t)i);
+      else
+        veh_move(w, (int32_t)(i - p.S), active, unfinished);
+    }
+    qt = block_sum(qt, red);
+    if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+    active = block_sum(active, red);
+    if (threadIdx.x == 0 && active) atomicAdd((unsigned long long*)&w.ctl->n_next, (unsigned long long)active);
+    unfinished = block_sum(unfinished, red);
+    if (threadIdx.x == 0 && unfinished)
+      atomicAdd((unsigned long long*)&w.ctl->unfinished, (unsigned long long)unfinished);
+    if (p.need_positions) chunk_positions(w, c0, c1, red);
+    grid.sync();
+    int32_t m = 0;
+    const int64_t M = w.g.M;
+    for (int64_t i = gtid; i < M + p.S; i += gstride) {
+      if (i < M) {
+        if (w.g.slot_edge[i] >= 0) m = max(m, slot_fg(w, (int32_t)i));
+      } else {
+        sig_e3(w, (int32_t)(i - M));
+      }
+    }
+    step_end<kLastBlockFinalize>(w, m, smax);
+    return;
+  }
   if (kDecideDK >= 0) {
     // reference algorithms, unsharded: stage B in the same launch (one kernel
     // per step); decisions never see each other (engine.cpp:197-198)
@@ -2665,33 +2771,7 @@ __device__ __forceinline__ void ref_step(const DevWorld& w, cg::grid_group& grid
   grid.sync();
   // E3
   for (int64_t s = gtid; s < p.S; s += gstride) sig_e3(w, (int32_t)s);
-  if (pos_scan) {  // positions of this block's chunk (block-uniform loop bounds)
-    long long off = 0;
-    for (int64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += w.v.bsum[b];
-    off = block_sum(off, red);
-    __shared__ long long s_off;
-    __shared__ int32_t wsum[kTailCoop / 32];
-    if (threadIdx.x == 0) s_off = off;
-    __syncthreads();
-    long long base = s_off;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
-      const int64_t i = t0 + threadIdx.x;
-      const int32_t f = i < c1 ? w.v.dflag[i] : 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
-      if (lane == 0) wsum[wid] = __popc(bal);
-      __syncthreads();
-      int before = 0, total = 0;
-#pragma unroll
-      for (int k = 0; k < kTailCoop / 32; ++k) {
-        before += k < wid ? wsum[k] : 0;
-        total += wsum[k];
-      }
-      if (i < c1) w.v.pos[i] = (int32_t)(base + before + __popc(bal & ((1u << lane) - 1u)));
-      base += total;
-      __syncthreads();
-    }
-  }
+  if (pos_scan) chunk_positions(w, c0, c1, red);  // (block-uniform loop bounds)
   if (p.siblings_only && (p.algorithm == 2 || p.algorithm == 3)) {
     grid.sync();
     for (int64_t u = gtid; u < w.g.n; u += gstride) node_scoped(w, (int32_t)u);
@@ -2702,24 +2782,7 @@ __device__ __forceinline__ void ref_step(const DevWorld& w, cg::grid_group& grid
   int32_t m = 0;
   for (int64_t s = gtid; s < w.g.M; s += gstride)
     if (w.g.slot_edge[s] >= 0) m = max(m, slot_fg(w, (int32_t)s));
-  m = block_max(m, smax);
-  if (kLastBlockFinalize) {  // the last block to finish finalizes the step (no grid barrier)
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-      if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
-      trace_max(w.ctl, 6);
-      __threadfence();
-      is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (is_last && threadIdx.x == 0) {
-      __threadfence();
-      finalize_step(w);
-      __threadfence();
-    }
-  } else if (threadIdx.x == 0 && m > 0) {
-    atomicMax(&w.ctl->max_occ_acc, m);
-  }
+  step_end<kLastBlockFinalize>(w, m, smax);
 }
 
 // Persistent run of up to `nsteps` reference-algorithm steps in ONE
@@ -2730,10 +2793,9 @@ template <int DK>
 __global__ void __launch_bounds__(kTailCoop) k_run_coop(DevWorld w, int64_t nsteps) {
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  (void)gtid;
   for (int64_t k = 0; k < nsteps && !skip_step(w.ctl); ++k) {  // ctl is read after a barrier: grid-uniform
-    ref_step<DK, false>(w, grid);
-    grid.sync();
-    if (gtid == 0) finalize_step(w);
+    ref_step<DK, true>(w, grid);  // the step's last block finalizes it
     grid.sync();
   }
 }
