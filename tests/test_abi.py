@@ -113,6 +113,23 @@ def test_graph_validation(mut, msg):
     assert rc == abi.EVALIDATION and msg in err
 
 
+def test_engine_options_validation():
+    """gmaco_sim_config.options (implementation switches) are validated
+    before any device work: unknown bits and a negative SSSP step are status 1."""
+    net = networks.grid(3, 3)
+    cfg = abi.default_config()
+    cfg.options.flags = 1 << 20
+    rc, msg = _create(net, cfg)
+    assert rc == abi.EVALIDATION and msg == "options: unknown flag bits"
+    cfg = abi.default_config()
+    cfg.options.sssp_delta = -1.0
+    rc, msg = _create(net, cfg)
+    assert rc == abi.EVALIDATION and msg == "options: sssp_delta must be >= 0"
+    cfg = abi.default_config()
+    cfg.options.flags = abi.OPT_REDZONES | abi.OPT_NO_PDL | abi.OPT_PROFILE_CREATE
+    assert _create(net, cfg)[0] != abi.EVALIDATION  # valid switches pass validation
+
+
 def test_grid_distance_requires_lattice():
     net = networks.grid(4, 4)
     net.edge_length_mm[5] += 1  # no longer uniform
