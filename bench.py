@@ -758,10 +758,16 @@ def run_ours(args, rank, world, local):
     if world == 1 and not args.no_secondary and headline:
         line["secondary"] = secondary_c4(peak, peak_src)
         line["secondary_c3"] = secondary_c3()
+    # the CPU-baseline leg (the only leg besides --impl reference that runs
+    # the compiled reference, oracle/_ref): the reference's run() /
+    # parallel_run() beside this engine's whole-run path, and the reference
+    # colony workload for cpu_baseline
+    if world == 1 and not args.no_secondary and not args.no_cpu_baseline and headline:
         line["reference_algorithms"] = reference_algorithms_block(os.cpu_count() or 1)
     if world == 1 and not args.no_cpu_baseline and headline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
-    if world == 1 and not args.no_secondary and args.algorithm != "colony" and args.config in ("c1", "c2"):
+    if world == 1 and not args.no_secondary and not args.no_cpu_baseline and args.algorithm != "colony" \
+            and args.config in ("c1", "c2"):
         line["reference_run_comparison"] = reference_algorithms_block(os.cpu_count() or 1, args.algorithm,
                                                                       args.config, fold=False)
     if world == 1 and not args.no_cpu_baseline and args.algorithm != "colony":
