@@ -214,6 +214,17 @@ struct DevTT {
 };
 constexpr int kTTChunk = 1024;  // rows per refresh chunk
 
+// Batched gather of device arrays into (mapped pinned) host memory.
+struct PackField {
+  const void* src;
+  void* dst;  // device-visible pointer
+  size_t bytes;
+};
+struct PackDesc {
+  PackField f[24];
+  int n = 0;
+};
+
 struct DevWorld {
   DevGraph g;
   DevTT tt;
@@ -240,6 +251,10 @@ struct DevWorld {
   // glibc pow, the function routing.cpp:93 calls, so the device weights are
   // bit-identical to the reference's; nullptr otherwise
   const double* taupow;
+  // gmaco_step_snapshot of small worlds: the step's finalizing block gathers
+  // these fields after the step (device copy of the slot's descriptor), in
+  // place of a separate k_pack launch; nullptr for plain steps
+  const PackDesc* snap;
 };
 
 // pow(tau_to_double(t), alpha) (routing.cpp:91-93; tau_to_double pheromone.hpp:19)

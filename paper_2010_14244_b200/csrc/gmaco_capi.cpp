@@ -571,6 +571,12 @@ struct gmaco_engine {
     bool pd_valid = false;  // pd_cache is this slot's gather for field set pd_mask
     uint32_t pd_mask = 0;
     PackDesc pd_cache;
+    // small worlds: the gather runs in the step's finalizing tail block
+    // (DevWorld::snap) from this device copy of the descriptor
+    PackDesc* pd_dev = nullptr;
+    PackDesc pd_dev_val;
+    bool pd_dev_set = false;
+    cudaGraphExec_t tail_snap_graph = nullptr;  // one step with the in-tail gather of this slot
   } rslot[2];
   StepResources res;
   cudaStream_t stream = nullptr;
@@ -627,6 +633,7 @@ struct gmaco_engine {
       PinnedPool::give(s.buf);
       if (s.done) cudaEventDestroy(s.done);
       if (s.snap_graph) cudaGraphExecDestroy(s.snap_graph);
+      if (s.tail_snap_graph) cudaGraphExecDestroy(s.tail_snap_graph);
     }
     buf.release();  // stream-ordered frees need the stream alive
     if (stream) StreamPool::give(device, stream);  // (synchronized at the top of the destructor)
@@ -635,7 +642,7 @@ struct gmaco_engine {
   void destroy_comm();
   void reset_graphs() {
     for (auto* ge : {&graph_big, &graph_one, &tgraph_big, &tgraph_one, &graph_walk, &graph_tail, &rslot[0].snap_graph,
-                     &rslot[1].snap_graph})
+                     &rslot[1].snap_graph, &rslot[0].tail_snap_graph, &rslot[1].tail_snap_graph})
       if (*ge) {
         cudaGraphExecDestroy(*ge);
         *ge = nullptr;
@@ -1571,6 +1578,10 @@ void unbound_stop(gmaco_engine* h) {
 // more than a few dozen direct launches (the GPU runs ~25 us steps while the
 // host enqueues the next).  Longer runs then switch to the captured graphs.
 constexpr int64_t kDirectSteps = 48;
+// Snapshots up to this many bytes are gathered by the step's finalizing tail
+// block instead of a separate k_pack launch (one block writes them to mapped
+// pinned memory; larger snapshots keep the grid-wide gather kernel).
+constexpr size_t kTailSnapMax = size_t(64) << 10;
 bool launch_direct(gmaco_engine* h) {
   if (h->direct_steps >= kDirectSteps) return false;
   ++h->direct_steps;
@@ -2395,6 +2406,45 @@ int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32
   return guarded(h, [&] {
     const PackDesc pd = arm_slot(h, fields, slot);
     auto& rs = h->rslot[slot];
+    size_t snap_bytes = 0;
+    for (int i = 0; i < pd.n; ++i) snap_bytes += pd.f[i].bytes;
+    if (h->res.coop_blocks > 0 && snap_bytes <= kTailSnapMax) {
+      // small worlds: the step's finalizing tail block gathers the fields
+      // (no k_pack launch); its descriptor lives in device memory, rewritten
+      // only when the field set changes, so one graph per slot serves any set
+      if (!rs.pd_dev) rs.pd_dev = h->buf.alloc_direct<PackDesc>(1);
+      if (!rs.pd_dev_set || std::memcmp(&rs.pd_dev_val, &pd, sizeof pd) != 0) {
+        CK(cudaStreamSynchronize(h->stream));  // no enqueued gather still reads the old descriptor
+        CK(cudaMemcpy(rs.pd_dev, &pd, sizeof pd, cudaMemcpyHostToDevice));
+        rs.pd_dev_val = pd;
+        rs.pd_dev_set = true;
+      }
+      DevWorld ws = h->w;
+      ws.snap = rs.pd_dev;
+      unbound_stop(h);
+      if (!rs.tail_snap_graph && h->direct_steps < kDirectSteps) {
+        ++h->direct_steps;
+        CK(launch_step(ws, h->res, h->stream, nullptr, nullptr));
+      } else {
+        if (!rs.tail_snap_graph) {
+          StepResources r = h->res;
+          r.capturing = true;
+          cudaGraph_t graph = nullptr;
+          CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+          const cudaError_t err = launch_step(ws, r, h->stream, nullptr, nullptr);
+          const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+          CK(err);
+          CK(e2);
+          CK(cudaGraphInstantiate(&rs.tail_snap_graph, graph, 0));
+          cudaGraphDestroy(graph);
+        }
+        CK(cudaGraphLaunch(rs.tail_snap_graph, h->stream));
+      }
+      CK(cudaEventRecord(rs.done, h->stream));
+      rs.armed = true;
+      h->pending = true;
+      return;
+    }
     // the first kDirectSteps steps: a direct step launch + the gather kernel
     // (no capture cost for short runs)
     if (!rs.snap_graph && h->direct_steps < kDirectSteps) {

@@ -2465,6 +2465,26 @@ __device__ __forceinline__ void finalize_step(const DevWorld& w) {
   c->unfinished = 0;
 }
 
+// The snapshot gather by one block (the step's finalizing block; small
+// worlds only, see gmaco_step_snapshot): every requested field of the
+// post-step vehicle state into mapped pinned memory.
+__device__ __forceinline__ void block_snapshot(const PackDesc* d) {
+  const int n = d->n;
+  for (int k = 0; k < n; ++k) {
+    const PackField f = d->f[k];
+    const bool vec = ((reinterpret_cast<uintptr_t>(f.src) | reinterpret_cast<uintptr_t>(f.dst)) & 15) == 0;
+    size_t done = 0;
+    if (vec) {
+      const size_t n16 = f.bytes / 16;
+      for (size_t i = threadIdx.x; i < n16; i += blockDim.x)
+        reinterpret_cast<uint4*>(f.dst)[i] = reinterpret_cast<const uint4*>(f.src)[i];
+      done = n16 * 16;
+    }
+    for (size_t i = done + threadIdx.x; i < f.bytes; i += blockDim.x)
+      static_cast<char*>(f.dst)[i] = static_cast<const char*>(f.src)[i];
+  }
+}
+
 __device__ __forceinline__ int32_t block_max(int32_t m, int32_t* smax) {
   __syncwarp();  // reconverge first (see block_sum)
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
@@ -2515,7 +2535,10 @@ __global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
 
 // The last block to finish finalizes the step.
 __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
-  if (skip_step(w.ctl)) return;
+  if (skip_step(w.ctl)) {
+    if (blockIdx.x == 0 && w.snap) block_snapshot(w.snap);  // a no-op step still snapshots the state
+    return;
+  }
   __shared__ int32_t smax[32];
   __shared__ bool is_last;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2533,6 +2556,7 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
     finalize_step(w);
     __threadfence();
   }
+  if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
 }
 
 // ---------------------------------------------------------------------------
@@ -2660,6 +2684,7 @@ __device__ __forceinline__ void step_end(const DevWorld& w, int32_t m, int32_t* 
       finalize_step(w);
       __threadfence();
     }
+    if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
   } else if (threadIdx.x == 0 && m > 0) {
     atomicMax(&w.ctl->max_occ_acc, m);
   }
@@ -2803,7 +2828,10 @@ __global__ void __launch_bounds__(kTailCoop) k_run_coop(DevWorld w, int64_t nste
 template <bool kFusedMotion, int kDecideDK>
 __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
   griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
-  if (skip_step(w.ctl)) return;  // grid-uniform: ctl changes only in the finalize below
+  if (skip_step(w.ctl)) {  // grid-uniform: ctl changes only in the finalize below
+    if (blockIdx.x == 0 && w.snap) block_snapshot(w.snap);  // a no-op step still snapshots the state
+    return;
+  }
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) trace_min(w.ctl, 3);
   __shared__ long long red[32];
@@ -2862,6 +2890,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
         finalize_step(w);
         __threadfence();
       }
+      if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
       return;
     } else {
       for (int64_t s = gtid; s < p.S; s += gstride) {
@@ -2883,6 +2912,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     if (threadIdx.x == 0) trace_max(w.ctl, 6);
     grid.sync();
     if (gtid == 0) finalize_step(w);
+    if (blockIdx.x == 0 && w.snap) block_snapshot(w.snap);
     return;
   }
   ref_step<kDecideDK, true>(w, grid);

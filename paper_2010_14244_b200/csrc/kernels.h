@@ -65,16 +65,6 @@ cudaError_t tt_build(const DevWorld& w, int32_t T, const int32_t* place, const i
                      int64_t* base, int64_t* cstart, int4* rec, int2* sm, int2* sl, cudaStream_t st);
 cudaError_t tt_refresh(const DevWorld& w, cudaStream_t st);
 cudaError_t build_reach_bits(const int64_t* D, int32_t T, int32_t n, int64_t words, uint64_t* out, cudaStream_t st);
-// Batched gather of device arrays into (mapped pinned) host memory.
-struct PackField {
-  const void* src;
-  void* dst;  // device-visible pointer
-  size_t bytes;
-};
-struct PackDesc {
-  PackField f[24];
-  int n = 0;
-};
 cudaError_t launch_pack(const PackDesc& d, cudaStream_t st);
 // Copies `weight` into the weight half of the slot records (ant-queue walker).
 cudaError_t sync_rec_weights(const DevWorld& w, cudaStream_t st);

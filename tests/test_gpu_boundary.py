@@ -100,3 +100,26 @@ def test_destroy_with_snapshot_in_flight_then_reuse_pool():
         e.vehicles_wait(0, view)
         cpu.step(1)
         assert np.array_equal(out, cpu.vehicles()["progress_mm"]), k
+
+
+@pytest.mark.parametrize("alg", ["colony", "maco-p"])
+def test_step_snapshot_past_finished_keeps_the_final_state(alg):
+    """gmaco_step_snapshot on a small world gathers in the step's finalizing
+    tail block; a step past finished() is a no-op, and its snapshot must
+    still hold the (final) state -- on both readback slots."""
+    net = networks.grid(8, 8, signals="all")
+    if alg == "colony":
+        cfg = _colony(V=60, seed=3, steps=12, ants=16)
+    else:
+        cfg = abi.default_config(algorithm="maco-p", vehicle_count=60, seed=3, max_steps=12)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    V = cfg.vehicle_count
+    bufs = [np.zeros(V, np.int64) for _ in range(2)]
+    views = [abi.VehicleView(progress_mm=abi.ptr(b, C.c_int64)) for b in bufs]
+    for k in range(20):  # 12 real steps, then 8 no-ops
+        gpu.step_snapshot(views[k & 1], k & 1)
+        gpu.vehicles_wait(k & 1, views[k & 1])
+        cpu.step(1)
+        assert np.array_equal(bufs[k & 1], cpu.vehicles()["progress_mm"]), k
+    assert gpu.finished() and cpu.finished()
