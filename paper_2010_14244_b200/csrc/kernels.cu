@@ -3559,15 +3559,22 @@ tail:
     lc.blockDim = dim3(kTailCoop);
     lc.dynamicSmemBytes = 0;
     lc.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
     // programmatic dependent launch: the tail's CTAs are scheduled while the
     // walk drains and wait in griddepcontrol.wait for its completion + memory
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (w.p.pdl) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    // the one-pass lattice colony tail (e1_in_walk, unsharded) has no grid
+    // barrier (the last block finalizes), so it needs no cooperative launch
+    if (!(fused && w.p.e1_in_walk && !w.p.sharded)) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na++].val.cooperative = 1;
+    }
     lc.attrs = at;
-    lc.numAttrs = w.p.pdl ? 2 : 1;
+    lc.numAttrs = na;
     if (fused) return cudaLaunchKernelEx(&lc, k_tail_coop<true, -1>, w);
     if (fuse_decide(w, r))  // stage B inside the cooperative tail: one launch per step
       return w.d.kind == 1 ? cudaLaunchKernelEx(&lc, k_tail_coop<false, 1>, w)

@@ -10,8 +10,11 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-from paper_2010_14244_b200 import abi, workloads  # noqa: E402
+from paper_2010_14244_b200 import abi, engine, workloads  # noqa: E402
 from paper_2010_14244_b200.engine import Engine  # noqa: E402
+
+if os.environ.get("LIB"):  # A/B: another build of the library
+    engine.load(os.environ["LIB"])
 
 config = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
