@@ -1789,12 +1789,21 @@ __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s);
 template <bool kSmem, int kTour, bool kOneVeh = false>
 __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   griddep_launch_dependents();  // let the tail's CTAs launch early (they wait for our completion)
-  if (skip_step(w.ctl)) return;
   // Block layout: [kSigCtas signal CTAs (e1_in_walk)][prefetch CTA][walk CTAs].
   // The special CTAs come first so the block scheduler dispatches them at
   // once: placed last, they started only when the final wave of walk CTAs was
   // dispatched and held the kernel's end ~17 us past the last walk (C3).
   const int nsig = w.p.e1_in_walk ? kSigCtas : 0;
+  const int K = w.p.ants;
+  const int vpb = blockDim.x / K;
+  const int lv = threadIdx.x / K;
+  const int ant = threadIdx.x - lv * K;
+  const int32_t slot = w.p.shard_lo + ((int)blockIdx.x - nsig - 1) * vpb + lv;  // walk slot; the vehicle via the balance order
+  const bool live = (int)blockIdx.x > nsig && lv < vpb && slot < w.p.shard_hi;
+  // the walk slot's vehicle is loaded in the same memory round trip as the
+  // control block (its load does not depend on the step check below)
+  const int32_t vid = (w.v.walk_order && live) ? w.v.walk_order[slot] : slot;
+  if (skip_step(w.ctl)) return;
   if ((int)blockIdx.x == nsig) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
     return;
@@ -1820,13 +1829,6 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   __shared__ long long red5[7][32];
   // move-bit words [blockDim][bit_words] after the staged tables (kTourBits)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
-  const int K = w.p.ants;
-  const int vpb = blockDim.x / K;
-  const int lv = threadIdx.x / K;
-  const int ant = threadIdx.x - lv * K;
-  const int32_t slot = w.p.shard_lo + ((int)blockIdx.x - nsig - 1) * vpb + lv;  // walk slot; the vehicle via the balance order
-  const bool live = lv < vpb && slot < w.p.shard_hi;
-  const int32_t vid = (w.v.walk_order && live) ? w.v.walk_order[slot] : slot;
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
   const double* __restrict__ W = w.weight;
