@@ -19,3 +19,11 @@ L=paper_2010_14244_b200/_lib/libgmaco.so
 bash tools/gpu/ncu_kernel.sh $L c2 k_colony_grid 8 ${T}_c2_walk
 bash tools/gpu/ncu_kernel.sh $L c2 k_tail_coop 8 ${T}_c2_tail
 bash tools/gpu/ncu_kernel.sh $L c4 k_colony_qt 3 ${T}_c4_qt 5
+bash tools/gpu/ncu_kernel.sh $L c3 k_colony_grid 4 ${T}_c3_walk 6
+bash tools/gpu/ncu_kernel.sh $L c5 k_colony_grid 4 ${T}_c5_walk 6
+bash tools/gpu/ncu_kernel.sh $L ref:maco-p:c2 k_tail_coop 8 ${T}_macop_step
+# summaries on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back)
+for f in gpurun_out/ncu/${T}_*.ncu-rep; do
+  python tools/ncu_summary.py report $f --json ${f%.ncu-rep}.json > /dev/null 2>&1
+done
+rm -f gpurun_out/ncu/${T}_*.ncu-rep

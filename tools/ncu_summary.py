@@ -82,7 +82,7 @@ def report(path):
         s = sum(tot.values()) or 1.0
         short = name.replace("(bool)", "").replace("(int)", "").split("(")[0].replace("void ", "").replace("gmaco::", "")
         for k in kernels:
-            kk = k["kernel"].split("(")[0].replace("void ", "")
+            kk = k["kernel"].replace("(bool)", "").replace("(int)", "").split("(")[0].replace("void ", "")
             if kk.replace(" ", "") == short.replace(" ", "") and "stalls_%" not in k:
                 k["stalls_%"] = {r[6:]: round(v / s * 100, 1)
                                  for r, v in sorted(tot.items(), key=lambda kv: -kv[1])[:6]}
