@@ -338,6 +338,13 @@ int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
  * *corrupted receives the number of overwritten guards (0 = no out-of-bounds
  * write reached one); gmaco_last_error describes the first. */
 int gmaco_debug_check_redzones(gmaco_engine* h, int64_t* corrupted);
+/* Test hook of the lattice walker's roulette (LatRec in
+ * paper_2010_14244_b200/csrc/device.cuh): for each pair of candidate weights
+ * (wa first, wb second) the integer threshold thr such that the sequential
+ * roulette of routing.cpp:100-113 over {wa, wb} with u = k * 2^-53 picks the
+ * first candidate iff k < thr. */
+int gmaco_debug_roulette_threshold(gmaco_engine* h, int32_t count, const double* wa, const double* wb,
+                                   uint64_t* out);
 /* Benchmark entry point: enqueues `steps` engine steps without host
  * synchronization (one CUDA graph per step), with an L2-flushing memset of
  * flush_bytes before each step outside the timed span; returns per-step

@@ -225,6 +225,23 @@ struct PackDesc {
   int n = 0;
 };
 
+// Lattice walker record of one (node, walk quadrant): everything a hop needs
+// in one 16-B load.  On a uniform lattice a walk toward its destination has
+// at most two candidates (one vertical, one horizontal move) whose order and
+// slots are fixed by the quadrant q = 2*(rows grow) + (cols grow).  The
+// sequential roulette (routing.cpp:100-113) picks the first candidate iff
+// fl(u * (w_a + w_b)) < w_a with u = k * 2^-53 (k = the draw's top 53 bits);
+// that predicate is monotone in k, so it is exactly "k < thr" for an integer
+// threshold tabulated once per step by stage F+G (lattice_threshold).  The
+// non-finite / non-positive total case (uniform pick, "second iff u >= 1/2")
+// is thr = 2^52.  lv / lh are the congestion loads of the vertical and
+// horizontal slot: their edge costs are len * (1 + load) (slot_fg), so a
+// walk's tour cost is len * (hops + the sum of its loads).
+struct __align__(16) LatRec {
+  unsigned long long thr;
+  int32_t lv, lh;
+};
+
 struct DevWorld {
   DevGraph g;
   DevTT tt;
@@ -240,6 +257,8 @@ struct DevWorld {
   int64_t* ecost;     // [m] colony tour cost per edge for the coming step
   int32_t* ecost32;   // [M] int32 copy for the lattice walker's SMEM staging when
                       //     max len * (1 + V) < 2^31 (nullptr otherwise)
+  LatRec* lrec;       // [M] lattice walker records, index 4 * node + quadrant (nullptr
+                      //     unless the lattice walker runs)
   int32_t* occ_cur;   // [m] edge occupancy of the previous step (engine.hpp:166)
   int32_t* occ_new;   // [m] being accumulated this step
   int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)

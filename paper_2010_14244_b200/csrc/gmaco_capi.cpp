@@ -1302,6 +1302,9 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       w.ecost32 = B.upload(e32);
     }
   }
+  // lattice walker records (LatRec), written by k_lattice_rec after the seal
+  // and by stage F+G every step
+  if (lattice_walker) w.lrec = B.alloc_direct<LatRec>(M);
   w.occ_cur = B.filled<int32_t>(M, 0);
   w.occ_new = B.filled<int32_t>(M, 0);
   w.dep = B.filled<int64_t>(M, 0);
@@ -1512,6 +1515,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   if (w.p.ant_queue && h->res.queue_blocks <= 0) throw std::runtime_error("ant-queue walker: no occupancy");
   pt.mark("occupancy queries");
   B.seal();
+  CK(launch_lattice_rec(w, h->stream));
   pt.mark("arena seal (copies)");
   CK(cudaEventCreate(&h->ev_a));
   CK(cudaEventCreate(&h->ev_b));
@@ -2297,6 +2301,10 @@ int gmaco_set_pheromone(gmaco_engine* h, const int64_t* tau) {
       CK(sync_rec_weights(h->w, h->stream));
       CK(cudaStreamSynchronize(h->stream));
     }
+    if (h->w.lrec) {
+      CK(launch_lattice_rec(h->w, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
   });
 }
 
@@ -2678,6 +2686,23 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
     CK(cudaMemcpy(out_next, on, count * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_via, ov, count * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_deviated, odv, count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gmaco_debug_roulette_threshold(gmaco_engine* h, int32_t count, const double* wa, const double* wb,
+                                   uint64_t* out) {
+  NvtxRange nvtx_(__func__);
+  if (!h || count < 0 || (count > 0 && (!wa || !wb || !out))) return GMACO_EVALIDATION;
+  return guarded(h, [&] {
+    if (count == 0) return;
+    DevBuffers tmp;
+    std::vector<double> a(wa, wa + count), b(wb, wb + count);
+    const double* da = tmp.upload(a);
+    const double* db = tmp.upload(b);
+    uint64_t* dout = tmp.alloc<uint64_t>(count);
+    CK(launch_threshold_batch(count, da, db, dout, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(out, dout, (size_t)count * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -1704,7 +1704,7 @@ __global__ void __launch_bounds__(256) k_colony_csr(DevWorld w) {
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ size_t grid_staged_bytes_dev(const DevWorld& w) {
-  return (12 * (size_t)w.g.M + 15) & ~size_t(15);  // f64 weights + int32 costs (kSmem variant)
+  return 16 * (size_t)w.g.M;  // the LatRec table (kSmem variant)
 }
 // B (colony) on a validated uniform lattice (GMACO_DIST_GRID, progress filter
 // on).  The distance service is closed-form and the lattice is checked at
@@ -1831,29 +1831,23 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
-  const double* __restrict__ W = w.weight;
-  const int64_t* __restrict__ Cst = w.ecost;
-  const int32_t* Cst32 = nullptr;  // staged int32 tour costs (host-checked bound)
+  const LatRec* __restrict__ R = w.lrec;
   __shared__ __align__(8) uint64_t stage_bar;
   if (kSmem) {
-    // Stage this step's weight / tour-cost tables and the degree table in
-    // shared memory with three TMA bulk copies (cp.async.bulk) completing on
-    // one mbarrier; the other threads overlap the vehicle prologue below.
-    const uint32_t bW = 8u * (uint32_t)w.g.M, bC = 4u * (uint32_t)w.g.M;
+    // Stage this step's LatRec table in shared memory with one TMA bulk copy
+    // (cp.async.bulk) completing on an mbarrier; the other threads overlap
+    // the vehicle prologue below.
+    const uint32_t bR = 16u * (uint32_t)w.g.M;
     if (threadIdx.x == 0) {
       const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dyn_smem);
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bW + bC) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bR) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst), "l"(w.weight), "r"(bW), "r"(bar) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst + bW), "l"(w.ecost32), "r"(bC), "r"(bar) : "memory");
+                   ::"r"(dst), "l"(w.lrec), "r"(bR), "r"(bar) : "memory");
     }
-    W = reinterpret_cast<const double*>(dyn_smem);
-    Cst32 = reinterpret_cast<const int32_t*>(dyn_smem + bW);
-
+    R = reinterpret_cast<const LatRec*>(dyn_smem);
   }
   const int nw = w.p.bit_words;
   unsigned long long* const bits_w =
@@ -1909,6 +1903,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   int32_t* tour = nullptr;
   if (live) start = start_s[lv];
   if (live && start >= 0) {
+    int64_t lsum = 0;  // the walk's congestion loads (tour cost = len * (hops + lsum))
     const int32_t dest = v.dest[vid];
     const int32_t cols = w.d.cols;
     const int32_t rd = dest / cols, cd = dest - rd * cols;
@@ -1939,30 +1934,22 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     const int off_h = dc > 0 ? 2 : 1, off_v = dr > 0 ? 3 : 0;
     const int step_h = dc, step_v = dr * cols;
     const bool v_first = dr < 0;
+    const int quad = (dr > 0 ? 2 : 0) | (dc > 0 ? 1 : 0);
     int32_t x = start;
     // One hop as straight-line predicated code (no branches: the compiler can
-    // interleave the next Philox block and the two hops of a pair).
+    // interleave the next Philox block and the two hops of a pair).  The
+    // roulette (routing.cpp:100-113) over the hop's <= 2 candidates is the
+    // integer compare against the node's tabulated threshold (LatRec): the
+    // first candidate (vertical when moving up) iff the draw's top 53 bits
+    // are below it; a single candidate is taken without a draw.
     auto hop = [&](uint64_t bits) {
-      const double u = to_unit(bits);
       const bool two = (rem_h > 0) & (rem_v > 0);
-      const bool a_is_v = two ? v_first : (rem_h == 0);
-      const int oa = a_is_v ? off_v : off_h, ob = a_is_v ? off_h : off_v;
-      const int xb = 4 * x;
-      const double wa = W[xb + oa];
-      const double wr = W[xb + ob];  // in-row (a hole reads 0.0); used only when two
-      const double wb = two ? wr : 0.0;
-      const double total = __dadd_rn(wa, wb);  // + exact 0.0 for a single candidate
-      const double pt = __dmul_rn(u, total);
-      // routing.cpp:100-113: total <= 0 or non-finite picks uniformly
-      // (floor(u*2) >= 1 takes the second; u = (bits>>11)*2^-53 exactly, so
-      // u*2 >= 1 iff bit 63 is set), else the first candidate iff
-      // u*total < wa (default: the last candidate)
-      const unsigned bad = (unsigned)!((total > 0.0) & (total <= 1.7976931348623157e308));
-      const unsigned hi = (unsigned)(bits >> 63);
-      const unsigned tb = (unsigned)two & ((bad & hi) | (~bad & (unsigned)!(pt < wa)));
-      const unsigned mv = tb ? (unsigned)!a_is_v : (unsigned)a_is_v;
-      const int32_t s = xb + (mv ? off_v : off_h);
-      cost += kSmem ? (int64_t)Cst32[s] : Cst[s];
+      const LatRec r = R[4 * x + quad];
+      const bool first = (bits >> 11) < r.thr;
+      const unsigned mv = two ? (unsigned)(first == v_first) : (unsigned)(rem_h == 0);
+      lsum += mv ? r.lv : r.lh;
+      const int32_t s = 4 * x + (mv ? off_v : off_h);
+      (void)s;
       if (kTour == kTourScratch) *tp++ = s;
       if (kTour == kTourBits) {  // 64 hops per word, first hop of a word at bit 63
         mbits = (mbits << 1) | mv;
@@ -2007,6 +1994,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       walk_counters_from_bits(bits_w + threadIdx.x * nw, n, abs(rd - rx), abs(cd - cx), rx, cx, dr, dc, rows, cols,
                               idegs, n_two);
     }
+    cost = (int64_t)w.d.grid_len * ((int64_t)n + lsum);  // = the sum of the hops' len * (1 + load)
     if (capped) cost = kInf;
     hops = n;
     steps = n;
@@ -2377,11 +2365,83 @@ __device__ __forceinline__ void node_scoped(const DevWorld& w, int32_t u) {
   }
 }
 
+// The lattice walker's roulette threshold (LatRec): the least k in
+// [0, 2^53] with !(fl(fl(k * 2^-53) * (wa + wb)) < wa), i.e. the walk takes
+// the first candidate iff its draw's top 53 bits are below it.  The product
+// is monotone in k, so the boundary is exact from a quotient estimate
+// confirmed by probes, or else by bisection.  A total
+// that is not positive and finite picks uniformly (routing.cpp:100-104):
+// the second candidate iff floor(2u) >= 1, i.e. k >= 2^52.
+__device__ __forceinline__ unsigned long long lattice_threshold(double wa, double wb) {
+  const double total = __dadd_rn(wa, wb);
+  if (!((total > 0.0) & (total <= 1.7976931348623157e308))) return 1ull << 52;
+  const unsigned long long kEnd = 1ull << 53;
+  // a lattice border's hole (weight 0) on either side: never first (u *
+  // total >= 0 >= wa), or always first for a normal wa (fl(u * wa) < wa for
+  // every u <= 1 - 2^-53; not so for a subnormal one); the zero dividend
+  // would otherwise take the division's slow path
+  if (wa <= 0.0) return 0;
+  if (wb == 0.0 && wa >= 2.2250738585072014e-308) return kEnd;
+  auto first_d = [&](double kd) { return __dmul_rn(__dmul_rn(kd, 0x1.0p-53), total) < wa; };  // kd integral
+  auto first = [&](unsigned long long k) { return first_d((double)k); };
+  // estimate k0 = floor(wa / total * 2^53); the boundary is within k0 - 1
+  // .. k0 + 1 up to rounding noise, settled by four independent probes
+  const double r = __dmul_rn(__ddiv_rn(wa, total), 0x1.0p53);
+  const double kf = !(r > 0.0) ? 0.0 : (r >= 0x1.0p53 ? 0x1.0p53 : floor(r));
+  const unsigned long long k = (unsigned long long)kf;
+  const bool pmm = k < 2 || first_d(__dadd_rn(kf, -2.0));
+  const bool pm = k == 0 || first_d(__dadd_rn(kf, -1.0));
+  const bool p0 = k < kEnd && first_d(kf);
+  const bool p1 = k + 1 < kEnd && first_d(__dadd_rn(kf, 1.0));
+  if (pm && !p0) return k;
+  if (p0 && !p1) return k + 1;
+  if (k > 0 && pmm && !pm) return k - 1;
+  // otherwise bisect a window around k0 when it brackets the boundary, else
+  // all of [0, 2^53] (subnormal products round coarsely, so the boundary can
+  // lie far from the quotient): at most 53 probes
+  unsigned long long lo = k > 4 ? k - 4 : 0, hi = k + 5 < kEnd ? k + 5 : kEnd;
+  if (!((lo == 0 || first(lo - 1)) && (hi == kEnd || !first(hi)))) {
+    lo = 0;
+    hi = kEnd;
+  }
+  while (lo < hi) {
+    const unsigned long long mid = lo + ((hi - lo) >> 1);
+    if (first(mid))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// The four LatRec of node s / 4 from its four slots' next-step weights and
+// loads: lane s & 3 of the quad writes quadrant q = s & 3 (rows grow: q & 2,
+// cols grow: q & 1; slots {up, left, right, down}).  Every lane of the quad
+// calls it together (s & 3 == lane & 3: callers stride by whole warps).
+__device__ __forceinline__ void lattice_quad(const DevWorld& w, int64_t s, double wt, int32_t load) {
+  const unsigned lane = threadIdx.x & 31u, base = lane & ~3u;
+  const unsigned qm = 0xFu << base;
+  const unsigned q = (unsigned)s & 3u;
+  const bool down = q & 2u, right = q & 1u;
+  const int ov = (int)base + (down ? 3 : 0), oh = (int)base + (right ? 2 : 1);
+  const double wv = __shfl_sync(qm, wt, ov), wh = __shfl_sync(qm, wt, oh);
+  const int32_t lv = __shfl_sync(qm, load, ov), lh = __shfl_sync(qm, load, oh);
+  LatRec r;
+  // moving up, "up" is the first slot (arguments selected first: one inlined
+  // threshold chain per lane, not two divergent ones)
+  const double wa = down ? wh : wv, wb = down ? wv : wh;
+  r.thr = lattice_threshold(wa, wb);
+  r.lv = lv;
+  r.lh = lh;
+  w.lrec[s] = r;
+}
+
 // F + G for one slot: MACO fold (fold_maco_edge, parallel.cpp:77-92) or exact
 // deposit sum-then-clamp, evaporation (pheromone.cpp:61-67), colony
 // congestion term, occupancy hand-off, next step's weight / tour cost
 // (routing.cpp:90-94).  Returns the slot's occupancy (for the running max).
-__device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
+__device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s, double* wt_out = nullptr,
+                                           int32_t* load_out = nullptr) {
   const DevParams& p = w.p;
   const int alg = p.algorithm;
   const bool aco = alg == 1 || alg == 4;
@@ -2439,7 +2499,9 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s) {
       const int32_t load = occ + q;
       wt = __dmul_rn(wt, __ddiv_rn(1.0, __dadd_rn(1.0, (double)load)));
       cost = cost + cost * (int64_t)load;
+      if (load_out) *load_out = load;
     }
+    if (wt_out) *wt_out = wt;
     w.weight[s] = wt;
     if (w.rec) {  // slot record {weight, int32 cost (-1: >= 2^31, see ecost)}
       *reinterpret_cast<double*>(w.rec + s) = wt;
@@ -2535,6 +2597,37 @@ __global__ void __launch_bounds__(256) k_scoped(DevWorld w) {
   if (u < w.g.n) node_scoped(w, u);
 }
 
+// LatRec table from the current weights and tour costs (create,
+// gmaco_set_pheromone): cost = len * (1 + load) on the uniform lattice.
+__global__ void __launch_bounds__(256) k_lattice_rec(DevWorld w) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= w.g.M) return;  // (whole quads: M = 4 n)
+  const bool live = w.g.slot_edge[s] >= 0;
+  const double wt = live ? w.weight[s] : 0.0;
+  const int32_t load = live ? (int32_t)(w.ecost[s] / w.d.grid_len - 1) : 0;
+  lattice_quad(w, s, wt, load);
+}
+
+cudaError_t launch_lattice_rec(const DevWorld& w, cudaStream_t st) {
+  if (!w.lrec) return cudaSuccess;
+  k_lattice_rec<<<(unsigned)((w.g.M + 255) / 256), 256, 0, st>>>(w);
+  return cudaGetLastError();
+}
+
+// gmaco_debug_roulette_threshold: lattice_threshold over a batch.
+__global__ void k_threshold_batch(int32_t count, const double* wa, const double* wb, unsigned long long* out) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = lattice_threshold(wa[i], wb[i]);
+}
+
+cudaError_t launch_threshold_batch(int32_t count, const double* wa, const double* wb, uint64_t* out,
+                                   cudaStream_t st) {
+  if (count > 0)
+    k_threshold_batch<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, wa, wb,
+                                                                        reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
 // The last block to finish finalizes the step.
 __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   if (skip_step(w.ctl)) {
@@ -2544,7 +2637,10 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   __shared__ int32_t smax[32];
   __shared__ bool is_last;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  const int32_t occ = (s < w.g.M && w.g.slot_edge[s] >= 0) ? slot_fg(w, s) : 0;
+  double wt = 0.0;
+  int32_t load = 0;
+  const int32_t occ = (s < w.g.M && w.g.slot_edge[s] >= 0) ? slot_fg(w, s, &wt, &load) : 0;
+  if (w.lrec && s < w.g.M) lattice_quad(w, s, wt, load);  // (M = 4 n on a lattice: whole quads)
   const int32_t m = block_max(occ, smax);
   if (threadIdx.x == 0) {
     if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
@@ -2871,10 +2967,14 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       const int64_t M = w.g.M;
       int32_t m = 0;
       for (int64_t i = gtid; i < M + p.S; i += gstride) {
-        if (i < M)
-          m = max(m, slot_fg(w, (int32_t)i));
-        else
+        if (i < M) {
+          double wt = 0.0;
+          int32_t load = 0;
+          m = max(m, slot_fg(w, (int32_t)i, &wt, &load));
+          if (w.lrec) lattice_quad(w, i, wt, load);  // (M = 4 n: whole quads take this branch)
+        } else {
           sig_e3(w, (int32_t)(i - M));
+        }
       }
       const int32_t nrel = w.ctl->nrel;
       for (int64_t i = gtid; i < nrel; i += gstride) w.v.state[w.v.rel[i]] = kAtNode;
@@ -2908,7 +3008,12 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
     // deposits or occupancy and no walk reads them, so skipping the
     // validity load only shortens the dependent chain
     int32_t m = 0;
-    for (int64_t s = gtid; s < w.g.M; s += gstride) m = max(m, slot_fg(w, (int32_t)s));
+    for (int64_t s = gtid; s < w.g.M; s += gstride) {
+      double wt = 0.0;
+      int32_t load = 0;
+      m = max(m, slot_fg(w, (int32_t)s, &wt, &load));
+      if (w.lrec) lattice_quad(w, s, wt, load);
+    }
     m = block_max(m, smax);
     if (threadIdx.x == 0 && m > 0) atomicMax(&w.ctl->max_occ_acc, m);
     if (threadIdx.x == 0) trace_max(w.ctl, 6);
@@ -2988,12 +3093,10 @@ static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t -
 constexpr int kTail = 64;
 
 // Dynamic shared memory of the staged grid walker (0 = read from global):
-// weight + tour-cost tables, 16 B per slot, when they fit 96 KiB.
+// the LatRec table, 16 B per slot, when it fits 96 KiB.
 size_t grid_smem_bytes(const DevWorld& w) {
-  // staged: f64 weights + int32 tour costs (TMA bulk copies need 16-byte
-  // multiples: M is a multiple of 4 on the ELL-4 lattice)
-  const size_t bytes = 12 * (size_t)w.g.M;
-  return (!w.p.no_smem && w.ecost32 && bytes <= (96u << 10)) ? bytes : 0;
+  const size_t bytes = 16 * (size_t)w.g.M;
+  return (!w.p.no_smem && w.lrec && bytes <= (96u << 10)) ? bytes : 0;
 }
 
 // Move-bit words of a CTA (kTourBits): [threads][bit_words] u64.

@@ -33,6 +33,10 @@ cudaError_t rec_unpack(const DevWorld& w, const int32_t* recv, const int32_t* ga
 cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t st,
                         cudaEvent_t walk_begin, cudaEvent_t walk_end);
 size_t scan_temp_bytes(int V);
+// Lattice walker records (LatRec) from the current weights and tour costs.
+cudaError_t launch_lattice_rec(const DevWorld& w, cudaStream_t st);
+cudaError_t launch_threshold_batch(int32_t count, const double* wa, const double* wb, uint64_t* out,
+                                   cudaStream_t st);
 int kernels_per_step(const DevWorld& w, const StepResources& r);
 // Reference algorithms (unsharded, cooperative launch available): up to
 // nsteps whole steps in one persistent cooperative launch.

@@ -47,6 +47,7 @@ SIGNATURES = {
     "gmaco_bench_steps": (C.c_int, C.c_void_p, i32, i64, P(f64), P(f64)),
     "gmaco_debug_trace": (C.c_int, C.c_void_p, i32, P(u64)),
     "gmaco_debug_check_redzones": (C.c_int, C.c_void_p, P(i64)),
+    "gmaco_debug_roulette_threshold": (C.c_int, C.c_void_p, i32, P(C.c_double), P(C.c_double), P(u64)),
     "gmaco_set_shard": (C.c_int, C.c_void_p, i32, i32),
     "gmaco_step_split": (C.c_int, C.c_void_p, i32),
     "gmaco_shard_by_target": (C.c_int, C.c_void_p, i32, i32),
@@ -250,6 +251,16 @@ class Engine:
         """Stage timestamps (ns) of the last of `steps` steps (DevCtl::trace)."""
         out = np.zeros(12, dtype=np.uint64)
         self._check(self.L.gmaco_debug_trace(self.h, steps, abi.ptr(out, u64)))
+        return out
+
+    def roulette_threshold(self, wa: np.ndarray, wb: np.ndarray) -> np.ndarray:
+        """The lattice walker's integer roulette thresholds (LatRec.thr) of
+        candidate weight pairs (gmaco_debug_roulette_threshold)."""
+        wa = np.ascontiguousarray(wa, dtype=np.float64)
+        wb = np.ascontiguousarray(wb, dtype=np.float64)
+        out = np.zeros(len(wa), dtype=np.uint64)
+        self._check(self.L.gmaco_debug_roulette_threshold(self.h, len(wa), abi.ptr(wa, C.c_double),
+                                                          abi.ptr(wb, C.c_double), abi.ptr(out, u64)))
         return out
 
     # -- sharding (multi-GPU) -----------------------------------------------------
