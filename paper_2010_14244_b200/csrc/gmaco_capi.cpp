@@ -1257,8 +1257,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // otherwise scratch mode keeps every ant's tour (no winner
   // replay) when it fits 48 GiB of the B200's 180 GB; larger colonies replay
   // the winner instead.
+  // (V < 2^24: the walker sums a 64-hop segment's congestion loads, each
+  // <= 2V, in 32 bits)
   const bool lattice_walker = alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter &&
-                              p.ants <= 256;
+                              p.ants <= 256 && V < (1 << 24);
   // move bits: 1 bit per hop in 64-hop SMEM words per ant, when a CTA's
   // words fit 48 KB (lattice CTAs hold <= 256 ants)
   p.bit_words = (p.plan_cap + 63) / 64;

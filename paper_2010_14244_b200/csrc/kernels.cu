@@ -1942,22 +1942,16 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     // integer compare against the node's tabulated threshold (LatRec): the
     // first candidate (vertical when moving up) iff the draw's top 53 bits
     // are below it; a single candidate is taken without a draw.
-    auto hop = [&](uint64_t bits) {
+    int32_t l32 = 0;  // loads of the current (<= 64-hop) segment, flushed into lsum
+    auto hop = [&](uint64_t bits) -> unsigned {
       const bool two = (rem_h > 0) & (rem_v > 0);
-      const LatRec r = R[4 * x + quad];
-      const bool first = (bits >> 11) < r.thr;
+      // the record in one 16-B load: {thr lo, thr hi, lv, lh}
+      const uint4 r = reinterpret_cast<const uint4*>(R)[4 * x + quad];
+      const unsigned long long thr = ((unsigned long long)r.y << 32) | r.x;
+      const bool first = (bits >> 11) < thr;
       const unsigned mv = two ? (unsigned)(first == v_first) : (unsigned)(rem_h == 0);
-      lsum += mv ? r.lv : r.lh;
-      const int32_t s = 4 * x + (mv ? off_v : off_h);
-      (void)s;
-      if (kTour == kTourScratch) *tp++ = s;
-      if (kTour == kTourBits) {  // 64 hops per word, first hop of a word at bit 63
-        mbits = (mbits << 1) | mv;
-        if (++hb == 64) {
-          bits_w[threadIdx.x * nw + wj++] = mbits;
-          hb = 0;
-        }
-      }
+      l32 += (int32_t)(mv ? r.z : r.w);
+      if (kTour == kTourScratch) *tp++ = 4 * x + (mv ? off_v : off_h);
       if (kTour != kTourBits) {  // move-bit walks derive both counters after the walk
         // out-degree of x on the validated full lattice (degree_sum counter)
         idegs += (rr > 0) + (rr < rows - 1) + (cq > 0) + (cq < cols - 1);
@@ -1968,27 +1962,63 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       x += mv ? step_v : step_h;
       rem_v -= mv;
       rem_h -= mv ^ 1u;
+      return mv;
     };
+    // move bits: 64 hops per word, first hop of a word at bit 63
     if (w.p.rng == 1) {
-      for (int32_t h = 0; h < n; ++h)
-        hop(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
-                 (uint64_t)step | ((uint64_t)(uint32_t)h << 40)));
+      for (int32_t h = 0; h < n; ++h) {
+        const unsigned mv = hop(draw(w.p.seed, 5, (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)ant << 32),
+                                     (uint64_t)step | ((uint64_t)(uint32_t)h << 40)));
+        if (kTour == kTourBits) {
+          mbits = (mbits << 1) | mv;
+          if (++hb == 64) {
+            bits_w[threadIdx.x * nw + wj++] = mbits;
+            hb = 0;
+          }
+        }
+        if ((h & 63) == 63) {
+          lsum += l32;
+          l32 = 0;
+        }
+      }
     } else {
       // hop pair (2p, 2p+1) uses Philox block p; block p+1 is computed in the
-      // same basic block, so its independent chain fills the hops' latency
+      // same basic block, so its independent chain fills the hops' latency.
+      // One inner loop per 64-hop word (32 pairs): the word's bits and loads
+      // are flushed after it, not tested for every hop.
       uint4 cur = philox4_rk(make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, 0u), w.p.rk);
       const int32_t pairs = n >> 1;
-      for (int32_t p = 0; p < pairs; ++p) {
-        // next block's rounds split across the pair's two dependent hops
-        uint4 nxt = make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)p + 1u);
-        philox_rounds<0, 5>(nxt, w.p.rk);
-        hop(((uint64_t)cur.x << 32) | cur.y);
-        philox_rounds<5, 10>(nxt, w.p.rk);
-        hop(((uint64_t)cur.z << 32) | cur.w);
-        cur = nxt;
+      for (int32_t p0 = 0; p0 < pairs; p0 += 32) {
+        const int32_t pe = min(pairs, p0 + 32);
+        unsigned long long mb = 0;
+        for (int32_t p = p0; p < pe; ++p) {
+          // next block's rounds split across the pair's two dependent hops
+          uint4 nxt = make_uint4((uint32_t)step, (uint32_t)vid, (uint32_t)ant, (uint32_t)p + 1u);
+          philox_rounds<0, 5>(nxt, w.p.rk);
+          const unsigned m0 = hop(((uint64_t)cur.x << 32) | cur.y);
+          philox_rounds<5, 10>(nxt, w.p.rk);
+          const unsigned m1 = hop(((uint64_t)cur.z << 32) | cur.w);
+          mb = (mb << 2) | (m0 << 1) | m1;
+          cur = nxt;
+        }
+        lsum += l32;
+        l32 = 0;
+        if (kTour == kTourBits) {
+          if (pe - p0 == 32) {
+            bits_w[threadIdx.x * nw + wj++] = mb;
+          } else {
+            mbits = mb;
+            hb = 2 * (pe - p0);
+          }
+        }
       }
-      if (n & 1) hop(((uint64_t)cur.x << 32) | cur.y);
+      if (n & 1) {
+        const unsigned mv = hop(((uint64_t)cur.x << 32) | cur.y);
+        mbits = (mbits << 1) | mv;
+        ++hb;
+      }
     }
+    lsum += l32;
     if (kTour == kTourBits) {
       if (hb) bits_w[threadIdx.x * nw + wj] = mbits << (64 - hb);  // left-aligned
       walk_counters_from_bits(bits_w + threadIdx.x * nw, n, abs(rd - rx), abs(cd - cx), rx, cx, dr, dc, rows, cols,
@@ -3569,7 +3599,7 @@ cudaError_t launch_step(const DevWorld& w, const StepResources& r, cudaStream_t 
   const int VS = w.p.shard_hi - w.p.shard_lo;  // vehicles planned on this rank
   if (walk_begin) cudaEventRecordWithFlags(walk_begin, st, r.capturing ? cudaEventRecordExternal : 0);
   if (r.part == 2) goto tail;
-  if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256) {
+  if (w.p.algorithm == 4 && w.d.kind == 1 && w.g.ell == 4 && w.p.progress_filter && w.p.ants <= 256 && w.lrec) {
     const size_t smem = grid_smem_bytes(w);
     const int mode = w.p.grid_bits ? kTourBits : (w.p.scratch_mode ? kTourScratch : kTourReplay);
     // staged tables: pack vehicles into 256-thread CTAs; otherwise one
