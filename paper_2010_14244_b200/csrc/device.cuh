@@ -257,8 +257,11 @@ struct DevWorld {
   int64_t* ecost;     // [m] colony tour cost per edge for the coming step
   int32_t* ecost32;   // [M] int32 copy for the lattice walker's SMEM staging when
                       //     max len * (1 + V) < 2^31 (nullptr otherwise)
-  LatRec* lrec;       // [M] lattice walker records, index 4 * node + quadrant (nullptr
-                      //     unless the lattice walker runs)
+  LatRec* lrec;       // lattice walker records (nullptr unless the lattice walker runs):
+                      //   lrec_stride == 0 (staged in SMEM): [4 n], index 4 * node + quadrant;
+                      //   else four quadrant tables of lrec_stride records in diagonal-major
+                      //   order (lrec_index), so the ants of one colony, which stand on one
+                      //   diagonal at every hop, read neighbouring records
   int32_t* occ_cur;   // [m] edge occupancy of the previous step (engine.hpp:166)
   int32_t* occ_new;   // [m] being accumulated this step
   int64_t* dep;       // [m] ACO / best-tour deposit accumulator (exact int64 sums)
@@ -274,7 +277,24 @@ struct DevWorld {
   // these fields after the step (device copy of the slot's descriptor), in
   // place of a separate k_pack launch; nullptr for plain steps
   const PackDesc* snap;
+  // (appended last: the hot kernels' parameter layout stays as it was)
+  int32_t lrec_stride;  // see lrec
+  int32_t pad_;
+  uint64_t cols_magic;  // grid: ceil(2^64 / cols); x / cols = umul64hi(x, cols_magic) for 0 <= x < 2^31
 };
+
+// LatRec position of (node x, quadrant q).  Diagonal-major tables: every
+// hop of a walk in quadrant q moves to the next diagonal -- key r + c when
+// rows and cols change in the same sense (q = 0, 3), r - c + cols - 1
+// otherwise -- so within a table the index is key * rows + r and a hop adds
+// dr * rows (horizontal) or dr * (rows + 1) (vertical).
+__device__ __forceinline__ int32_t lrec_index(const DevWorld& w, int32_t x, int q) {
+  if (!w.lrec_stride) return 4 * x + q;
+  const int32_t cols = w.d.cols, rows = w.d.rows;
+  const int32_t r = (int32_t)__umul64hi((unsigned long long)x, w.cols_magic), c = x - r * cols;
+  const int32_t key = (q == 0 || q == 3) ? r + c : r - c + cols - 1;
+  return q * w.lrec_stride + key * rows + r;
+}
 
 // pow(tau_to_double(t), alpha) (routing.cpp:91-93; tau_to_double pheromone.hpp:19)
 __device__ __forceinline__ double tau_alpha(const DevWorld& w, int64_t t) {

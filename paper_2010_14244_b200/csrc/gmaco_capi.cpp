@@ -1002,6 +1002,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
     }
     w.d.rows = R;
     w.d.cols = Cc;
+    w.cols_magic = (uint64_t)((((unsigned __int128)1 << 64) + (unsigned)Cc - 1) / (unsigned)Cc);
     w.d.grid_len = g.len[0];
     dh.cols = Cc;
     dh.grid_len = g.len[0];
@@ -1258,9 +1259,10 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   // replay) when it fits 48 GiB of the B200's 180 GB; larger colonies replay
   // the winner instead.
   // (V < 2^24: the walker sums a 64-hop segment's congestion loads, each
-  // <= 2V, in 32 bits)
-  const bool lattice_walker = alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter &&
-                              p.ants <= 256 && V < (1 << 24);
+  // <= 2V, in 32 bits; its diagonal-major record tables are int32-indexed)
+  const bool lattice_walker =
+      alg == GMACO_COLONY && dd->kind == GMACO_DIST_GRID && p.progress_filter && p.ants <= 256 && V < (1 << 24) &&
+      (int64_t)4 * (dd->grid_rows + dd->grid_cols - 1) * dd->grid_rows < (int64_t)INT32_MAX;
   // move bits: 1 bit per hop in 64-hop SMEM words per ant, when a CTA's
   // words fit 48 KB (lattice CTAs hold <= 256 ants)
   p.bit_words = (p.plan_cap + 63) / 64;
@@ -1306,7 +1308,13 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   }
   // lattice walker records (LatRec), written by k_lattice_rec after the seal
   // and by stage F+G every step
-  if (lattice_walker) w.lrec = B.alloc_direct<LatRec>(M);
+  if (lattice_walker) {
+    // staged in SMEM (node-major) when it fits, else diagonal-major tables
+    const bool staged = !p.no_smem && (size_t)16 * M <= (size_t(96) << 10);
+    const int32_t R = dd->grid_rows, Cc = dd->grid_cols;
+    w.lrec_stride = staged ? 0 : (R + Cc - 1) * R;
+    w.lrec = B.alloc_direct<LatRec>(staged ? (size_t)M : (size_t)4 * w.lrec_stride);
+  }
   w.occ_cur = B.filled<int32_t>(M, 0);
   w.occ_new = B.filled<int32_t>(M, 0);
   w.dep = B.filled<int64_t>(M, 0);

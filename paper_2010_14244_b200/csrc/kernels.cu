@@ -1936,6 +1936,9 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     const bool v_first = dr < 0;
     const int quad = (dr > 0 ? 2 : 0) | (dc > 0 ? 1 : 0);
     int32_t x = start;
+    // the walk's record index and its per-hop steps (lrec_index)
+    int32_t ri = lrec_index(w, start, quad);
+    const int32_t ri_h = w.lrec_stride ? dr * rows : step_h * 4, ri_v = w.lrec_stride ? dr * (rows + 1) : step_v * 4;
     // One hop as straight-line predicated code (no branches: the compiler can
     // interleave the next Philox block and the two hops of a pair).  The
     // roulette (routing.cpp:100-113) over the hop's <= 2 candidates is the
@@ -1946,7 +1949,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     auto hop = [&](uint64_t bits) -> unsigned {
       const bool two = (rem_h > 0) & (rem_v > 0);
       // the record in one 16-B load: {thr lo, thr hi, lv, lh}
-      const uint4 r = reinterpret_cast<const uint4*>(R)[4 * x + quad];
+      const uint4 r = reinterpret_cast<const uint4*>(R)[ri];
       const unsigned long long thr = ((unsigned long long)r.y << 32) | r.x;
       const bool first = (bits >> 11) < thr;
       const unsigned mv = two ? (unsigned)(first == v_first) : (unsigned)(rem_h == 0);
@@ -1959,7 +1962,8 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
         rr += mv ? dr : 0;
         cq += mv ? 0 : dc;
       }
-      x += mv ? step_v : step_h;
+      if (kTour == kTourScratch) x += mv ? step_v : step_h;
+      ri += mv ? ri_v : ri_h;
       rem_v -= mv;
       rem_h -= mv ^ 1u;
       return mv;
@@ -2456,14 +2460,12 @@ __device__ __forceinline__ void lattice_quad(const DevWorld& w, int64_t s, doubl
   const int ov = (int)base + (down ? 3 : 0), oh = (int)base + (right ? 2 : 1);
   const double wv = __shfl_sync(qm, wt, ov), wh = __shfl_sync(qm, wt, oh);
   const int32_t lv = __shfl_sync(qm, load, ov), lh = __shfl_sync(qm, load, oh);
-  LatRec r;
   // moving up, "up" is the first slot (arguments selected first: one inlined
   // threshold chain per lane, not two divergent ones)
   const double wa = down ? wh : wv, wb = down ? wv : wh;
-  r.thr = lattice_threshold(wa, wb);
-  r.lv = lv;
-  r.lh = lh;
-  w.lrec[s] = r;
+  const unsigned long long thr = lattice_threshold(wa, wb);
+  reinterpret_cast<uint4*>(w.lrec)[lrec_index(w, (int32_t)(s >> 2), (int)q)] =
+      make_uint4((uint32_t)thr, (uint32_t)(thr >> 32), (uint32_t)lv, (uint32_t)lh);
 }
 
 // F + G for one slot: MACO fold (fold_maco_edge, parallel.cpp:77-92) or exact
@@ -3126,7 +3128,7 @@ constexpr int kTail = 64;
 // the LatRec table, 16 B per slot, when it fits 96 KiB.
 size_t grid_smem_bytes(const DevWorld& w) {
   const size_t bytes = 16 * (size_t)w.g.M;
-  return (!w.p.no_smem && w.lrec && bytes <= (96u << 10)) ? bytes : 0;
+  return (w.lrec && !w.lrec_stride && bytes <= (96u << 10)) ? bytes : 0;
 }
 
 // Move-bit words of a CTA (kTourBits): [threads][bit_words] u64.

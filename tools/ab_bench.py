@@ -40,6 +40,13 @@ e.step(warmup)
 c0 = e.counters()
 walk, step = e.bench_steps(steps, 512 << 20, "both")
 c1 = e.counters()
+e.close()
+# the step alone, as bench.py times it (two events per step: the walk -> tail
+# programmatic launch is not broken by an event in between)
+e = engine.Engine(net, cfg, dist)
+e.step(warmup)
+_, step_only = e.bench_steps(steps, 512 << 20, "step")
 print(json.dumps({"lib": lib, "config": config, "walk_ms_mean": float(walk.mean()), "walk_ms_p50": float(np.median(walk)),
                   "step_ms_mean": float(step.mean()), "step_ms_p50": float(np.median(step)),
+                  "step_only_ms_mean": float(step_only.mean()), "step_only_ms_p50": float(np.median(step_only)),
                   "ant_steps_per_step": (c1.ant_steps - c0.ant_steps) / steps}))
