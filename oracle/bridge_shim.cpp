@@ -3,6 +3,10 @@
 // same SimConfig and reports RunResult::identical_to (engine.cpp:34-40); and
 // drives the reference harness patched with the "gpu" executor
 // (harness_gpu.patch): load_scenario -> run_matrix -> write_results_csv.
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -11,6 +15,23 @@
 #include "macosim/engine.hpp"
 #include "macosim/harness.hpp"
 #include "macosim_gpu.hpp"
+
+namespace {
+// a crash inside the bridged code prints its native stack (the test log is
+// the only trace the GPU box returns)
+void bridge_segv(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "bridge: fatal signal, native stack:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvHook {
+  SegvHook() { signal(SIGSEGV, bridge_segv); }
+} segv_hook;
+}  // namespace
 
 extern "C" {
 // 1 identical, 0 different, -1 error (message via bridge_last_error)

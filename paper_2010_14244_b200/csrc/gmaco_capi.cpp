@@ -576,6 +576,10 @@ struct gmaco_engine {
     PackDesc* pd_dev = nullptr;
     PackDesc pd_dev_val;
     bool pd_dev_set = false;
+    // pinned source of the descriptor's stream-ordered upload; pd_copied
+    // marks that upload's completion (the staging is rewritten only after it)
+    PackDesc* pd_host = nullptr;
+    cudaEvent_t pd_copied = nullptr;
     cudaGraphExec_t tail_snap_graph = nullptr;  // one step with the in-tail gather of this slot
   } rslot[2];
   StepResources res;
@@ -632,6 +636,8 @@ struct gmaco_engine {
     for (auto& s : rslot) {
       PinnedPool::give(s.buf);
       if (s.done) cudaEventDestroy(s.done);
+      if (s.pd_copied) cudaEventDestroy(s.pd_copied);
+      PinnedPool::give(s.pd_host);
       if (s.snap_graph) cudaGraphExecDestroy(s.snap_graph);
       if (s.tail_snap_graph) cudaGraphExecDestroy(s.tail_snap_graph);
     }
@@ -2432,8 +2438,18 @@ int gmaco_step_snapshot(gmaco_engine* h, const gmaco_vehicle_view* fields, int32
       // only when the field set changes, so one graph per slot serves any set
       if (!rs.pd_dev) rs.pd_dev = h->buf.alloc_direct<PackDesc>(1);
       if (!rs.pd_dev_set || std::memcmp(&rs.pd_dev_val, &pd, sizeof pd) != 0) {
-        CK(cudaStreamSynchronize(h->stream));  // no enqueued gather still reads the old descriptor
-        CK(cudaMemcpy(rs.pd_dev, &pd, sizeof pd, cudaMemcpyHostToDevice));
+        // a stream-ordered upload: gathers enqueued before it still read the
+        // old descriptor, the steps after it the new one; no host sync, so a
+        // step / snapshot loop keeps the GPU fed from its first iteration
+        if (!rs.pd_host) {
+          rs.pd_host = static_cast<PackDesc*>(PinnedPool::take(sizeof(PackDesc)));
+          CK(cudaEventCreateWithFlags(&rs.pd_copied, cudaEventDisableTiming));
+        } else {
+          CK(cudaEventSynchronize(rs.pd_copied));  // the previous upload has read the staging
+        }
+        *rs.pd_host = pd;
+        CK(cudaMemcpyAsync(rs.pd_dev, rs.pd_host, sizeof pd, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaEventRecord(rs.pd_copied, h->stream));
         rs.pd_dev_val = pd;
         rs.pd_dev_set = true;
       }
