@@ -84,3 +84,38 @@ def test_threshold_edge_cases(engine):
     assert got[(0.0, 1.0)] == 0
     assert got[(0.0, 0.0)] == 1 << 52  # uniform pick
     assert thr[pairs.index((inf, 1.0))] == 1 << 52 and thr[pairs.index((1.0, nan))] == 1 << 52
+
+
+@pytest.mark.parametrize("shape", [(9, 23), (23, 9), (14, 14)])
+@pytest.mark.parametrize("flags,ants", [("no_smem", 32), ("no_smem", 64), ("no_smem_no_bits", 32)])
+def test_lattice_walker_record_layouts(shape, flags, ants):
+    """The lattice walker reading its records from global memory in the
+    diagonal-major quadrant tables (what C3/C5 run), on non-square lattices in
+    both orientations, with multi-vehicle CTAs (K=32), one-vehicle CTAs (K=64)
+    and scratch tours instead of move bits: every iteration equals the oracle
+    (vehicles, signals, pheromone, occupancy, counters, planned tours)."""
+    from oracle import oracle as O
+
+    rows, cols = shape
+    net = networks.grid(rows, cols, signals="all")
+    V = rows * cols
+    cfg = abi.colony_production(abi.default_config(algorithm="colony", controller="preemptive", vehicle_count=V,
+                                                   seed=rows * 7 + ants, max_steps=40), ants=ants)
+    cfg.options.flags = abi.OPT_NO_SMEM | (abi.OPT_NO_BITS if flags == "no_smem_no_bits" else 0)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    for it in range(4):
+        gpu.step(1)
+        cpu.step(1)
+        va, vb = gpu.vehicles(), cpu.vehicles()
+        for f in abi.VEHICLE_FIELDS:
+            assert np.array_equal(va[f], vb[f]), (it, f)
+        sa, sb = gpu.signals(), cpu.signals()
+        for f in sa:
+            assert np.array_equal(sa[f], sb[f]), (it, f)
+        assert np.array_equal(gpu.pheromone(), cpu.pheromone()), it
+        assert np.array_equal(gpu.occupancy(), cpu.occupancy()), it
+        a, b = gpu.counters(), cpu.counters()
+        assert (a.ant_steps, a.candidates, a.degree_sum) == (b.ant_steps, b.candidates, b.degree_sum), it
+        for vid in range(0, V, 5):
+            assert np.array_equal(gpu.route(vid, True), cpu.route(vid, True)), (it, vid)
