@@ -719,12 +719,15 @@ uint64_t mix64(uint64_t x) {
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
   return x ^ (x >> 31);
 }
-uint64_t draw(uint64_t seed, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
-  uint64_t h = mix64(seed);
-  h = mix64(h ^ a);
-  h = mix64(h ^ b);
-  return mix64(h ^ c);
-}
+// The reference's draw(seed, stream, b, c) = mix64(mix64(mix64(mix64(seed) ^
+// stream) ^ b) ^ c) (include/macosim/rng.hpp:28-40), with the (seed, stream)
+// prefix of the chain computed once: the per-entity loops at create draw
+// thousands of times per stream.
+struct DrawStream {
+  uint64_t h;
+  DrawStream(uint64_t seed, uint64_t a) : h(mix64(mix64(seed) ^ a)) {}
+  uint64_t operator()(uint64_t b, uint64_t c = 0) const { return mix64(mix64(h ^ b) ^ c); }
+};
 double to_unit(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
 double uniform(uint64_t bits, double lo, double hi) { return lo + to_unit(bits) * (hi - lo); }
 uint64_t below(uint64_t bits, uint64_t n) {
@@ -792,24 +795,28 @@ Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
   s.speed.resize(V);
   s.advance.resize(V);
   s.depart.assign(V, 0);
+  const DrawStream od(c.seed, 2), sp(c.seed, 3), dep(c.seed, 4);
   for (int32_t vid = 0; vid < V; ++vid) {
     const std::vector<std::pair<int32_t, int32_t>>* biased = nullptr;
     if (c.od_pattern == GMACO_OD_BLOCKS) {  // engine.cpp:88-97
-      const double r = to_unit(draw(c.seed, 2, vid, 0));
+      const double r = to_unit(od(vid, 0));
       if (r < c.od_bias) {
-        const bool forward = to_unit(draw(c.seed, 2, vid, 1)) < 0.5;
+        const bool forward = to_unit(od(vid, 1)) < 0.5;
         const auto& b = forward ? ab : ba;
         if (!b.empty()) biased = &b;
       }
     }
-    const uint64_t bits = draw(c.seed, 2, vid, 2);
+    const uint64_t bits = od(vid, 2);
     if (biased) {
       const auto& pr = (*biased)[below(bits, biased->size())];
       s.origin[vid] = pr.first;
       s.dest[vid] = pr.second;
     } else {
       const int64_t idx = (int64_t)below(bits, (uint64_t)pool);
-      const int32_t u = (int32_t)(std::upper_bound(prefix.begin(), prefix.end(), idx) - prefix.begin()) - 1;
+      // (grid: every node has n - 1 destinations)
+      const int32_t u = dh.kind == GMACO_DIST_GRID
+                            ? (int32_t)(idx / (n - 1))
+                            : (int32_t)(std::upper_bound(prefix.begin(), prefix.end(), idx) - prefix.begin()) - 1;
       int64_t r = idx - prefix[u];
       int32_t v = -1;
       if (dh.kind == GMACO_DIST_GRID) {
@@ -829,10 +836,10 @@ Spawned spawn(const gmaco_sim_config& c, const HostGraph& g, const DistHost& dh,
       s.origin[vid] = u;
       s.dest[vid] = v;
     }
-    s.speed[vid] = uniform(draw(c.seed, 3, vid), c.speed_min_mps, c.speed_max_mps);  // engine.cpp:103-105
+    s.speed[vid] = uniform(sp(vid), c.speed_min_mps, c.speed_max_mps);  // engine.cpp:103-105
     s.advance[vid] = std::llround(s.speed[vid] * c.dt_s * 1000.0);
     if (c.spawn == GMACO_UNIFORM_WINDOW)
-      s.depart[vid] = (int64_t)below(draw(c.seed, 4, vid), (uint64_t)c.spawn_window_steps);
+      s.depart[vid] = (int64_t)below(dep(vid), (uint64_t)c.spawn_window_steps);
   }
   return s;
 }
@@ -1305,10 +1312,11 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   std::vector<double> wt(M, 0.0);
   std::vector<int64_t> ecost(M, 0);
   const int64_t lo = p.tau_lo, hi = p.tau_hi;
+  const DrawStream init(c.seed, 1);
   for (int32_t s = 0; s < M; ++s) {
     const int32_t e = h->slot_edge[s];
     if (e < 0) continue;
-    const double v = uniform(draw(c.seed, 1, (uint64_t)e), c.pheromone.tau_init_lo, c.pheromone.tau_init_hi);
+    const double v = uniform(init((uint64_t)e), c.pheromone.tau_init_lo, c.pheromone.tau_init_hi);
     tau[s] = std::clamp(tau_from_double(v), lo, hi);
     const double tau_d = static_cast<double>(tau[s]) / 1e6;
     const double ta = p.alpha == 1.0 ? tau_d : (p.alpha == 0.0 ? 1.0 : std::pow(tau_d, p.alpha));
@@ -2041,8 +2049,9 @@ void read_vehicles(gmaco_engine* h, const gmaco_vehicle_view* v) {
       }
     }
     if (v->speed_mps) {  // speed is host-side setup state: recompute as spawn did
+      const DrawStream sp(h->cfg.seed, 3);
       for (size_t i = 0; i < V; ++i)
-        v->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+        v->speed_mps[i] = uniform(sp(i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
     }
   }
 }  // namespace
@@ -2561,9 +2570,11 @@ int gmaco_vehicles_wait(gmaco_engine* h, int32_t slot, const gmaco_vehicle_view*
       const int32_t* oe = reinterpret_cast<const int32_t*>(st + rs.oe_off);
       for (size_t i = 0; i < (size_t)h->w.p.V; ++i) view->on_edge[i] = oe[i] < 0 ? -1 : h->slot_edge[oe[i]];
     }
-    if (view->speed_mps)
+    if (view->speed_mps) {
+      const DrawStream sp(h->cfg.seed, 3);
       for (size_t i = 0; i < (size_t)h->w.p.V; ++i)
-        view->speed_mps[i] = uniform(draw(h->cfg.seed, 3, i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+        view->speed_mps[i] = uniform(sp(i), h->cfg.speed_min_mps, h->cfg.speed_max_mps);
+    }
     rs.armed = false;
   }, /*stream_ordered=*/true);
 }
