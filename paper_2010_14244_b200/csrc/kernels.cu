@@ -369,16 +369,24 @@ __device__ __forceinline__ void flush_counters(DevCtl* c, const Sum5& t) {
 __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_t slot, bool deviated,
                                           int32_t from) {
   const DevVehicles& v = w.v;
+  // every load ahead of the first store (the compiler may not move a load
+  // past a possibly aliasing store): one memory round trip, not one per field
+  const int64_t overshoot = v.overshoot[vid];
+  const int64_t debt = v.latency_debt[vid];
+  const int32_t ndec = v.decisions[vid];
+  const int32_t ndev = deviated ? v.deviations[vid] : 0;
+  const int32_t k = w.p.record_paths ? v.path_n[vid] : 0;
+  const int64_t plen = v.path_len_mm[vid];
+  const int64_t elen = w.g.len[slot];
   if (w.p.sharded) v.dec_rec[vid] = slot | (deviated ? GMACO_REC_DEVIATED : 0);
   v.state[vid] = kOnEdge;
   v.on_edge[vid] = slot;
-  v.progress[vid] = v.overshoot[vid];
+  v.progress[vid] = overshoot;
   v.overshoot[vid] = 0;
-  v.latency_debt[vid] += w.p.latency_us;
-  v.decisions[vid] += 1;
-  if (deviated) v.deviations[vid] += 1;
+  v.latency_debt[vid] = debt + w.p.latency_us;
+  v.decisions[vid] = ndec + 1;
+  if (deviated) v.deviations[vid] = ndev + 1;
   if (w.p.record_paths) {
-    const int32_t k = v.path_n[vid];
     if (k < w.p.path_cap) {
       v.path[(size_t)vid * w.p.path_cap + k] = slot;
       v.path_n[vid] = k + 1;
@@ -386,7 +394,7 @@ __device__ __forceinline__ void take_edge(const DevWorld& w, int32_t vid, int32_
       atomicExch(&w.ctl->error, 1);  // path buffer overflow → host error
     }
   }
-  v.path_len_mm[vid] += w.g.len[slot];
+  v.path_len_mm[vid] = plen + elen;
   if (w.p.algorithm == 2 || w.p.algorithm == 3) {  // MACO commit bookkeeping
     const int32_t key = w.p.siblings_only ? from : slot;
     v.dec_next[vid] = atomicExch(&w.dec_head[key], vid);
@@ -402,17 +410,22 @@ template <int DK>
 __device__ __forceinline__ void decide_vehicle(const DevWorld& w, int32_t vid, int64_t step, long long& decided,
                                                long long& cands, long long& degs) {
   const DevVehicles& v = w.v;
-  if (w.p.sharded) v.dec_rec[vid] = -1;
+  // the vehicle's words in one round of loads, ahead of any store
   uint8_t st = v.state[vid];
-  if (st == kPending && v.depart[vid] == step) {  // engine.cpp:177-180
+  const int64_t depart = v.depart[vid];
+  int32_t x = v.at_node[vid];
+  const int32_t origin = v.origin[vid];
+  const int32_t dest = v.dest[vid];
+  if (w.p.sharded) v.dec_rec[vid] = -1;
+  if (st == kPending && depart == step) {  // engine.cpp:177-180
     st = kAtNode;
     v.state[vid] = kAtNode;
-    v.at_node[vid] = v.origin[vid];
+    v.at_node[vid] = origin;
+    x = origin;
   }
   if (w.p.need_positions) v.dflag[vid] = 0;
   if (st != kAtNode) return;
-  const int32_t x = v.at_node[vid];
-  const Target<DK> t(w.d, v.dest[vid]);
+  const Target<DK> t(w.d, dest);
   int32_t slot = -1;
   bool dev = false;
   if (w.p.algorithm == 0) {
