@@ -35,6 +35,7 @@ if config.startswith("ref:"):  # ref:ALGORITHM:CONFIG -- a reference algorithm o
     dist, keep = net.grid_distance(), None
 else:
     net, cfg, dist, keep = workloads.CONFIGS[config](seed=1, max_steps=warmup + steps + 1, **kw)
+cfg.options.flags |= int(os.environ.get("FLAGS", "0"))  # A/B of an engine option (abi.OPT_*)
 e = engine.Engine(net, cfg, dist)
 e.step(warmup)
 c0 = e.counters()
