@@ -1479,7 +1479,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
       // distance (a walk's hop count follows it): the queue's last ants are
       // short walks instead of stragglers holding the kernel's end.  Within a
       // band, destination-major order keeps the rows of a few targets hot.
-      constexpr int kLptBands = 4;
+      constexpr int kLptBands = 8;
       std::vector<int32_t> band(V, 0);
       if (w.d.table) {
         std::vector<int32_t> rowv(V), orgv(V);
@@ -1501,7 +1501,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
         for (int32_t i = 0; i < V; ++i) {
           int b = 0;
           while (b < kLptBands - 1 && dv_[i] < cut[b]) ++b;
-          band[i] = b;  // 0: the longest quarter
+          band[i] = b;  // 0: the longest eighth
         }
       }
       std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
