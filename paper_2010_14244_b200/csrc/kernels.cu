@@ -259,6 +259,21 @@ __device__ __forceinline__ void trace_max(DevCtl* c, int i) {
   if (c->trace_on) atomicMax(&c->trace[i], gtimer());
 }
 
+// finer stage stamps (tools/stage_trace.py), compiled in with -DGMACO_TRACE_FINE
+#ifdef GMACO_TRACE_FINE
+#define TRACE_FINE(i) trace_max(w.ctl, i)
+#else
+#define TRACE_FINE(i) (void)0
+#endif
+
+// atom.add with acquire-release semantics at GPU scope (last-block detection
+// without a separate full fence)
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ bool skip_step(const DevCtl* ctl) {
   return ctl->done || ctl->step >= ctl->stop_at;
 }
@@ -557,7 +572,100 @@ __device__ __forceinline__ WalkOut ant_walk(const DevWorld& w, const Target<DK>&
 
 // E2 (motion) of one vehicle; defined with the other per-entity stage bodies.
 // Colony walks run it for each vehicle right after that vehicle's stage B.
-__device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished);
+// The words E2 reads of a vehicle on an edge and of that edge, all loaded in
+// one round (MoveWords::load) so that motion is one memory round trip.
+struct MoveWords {
+  int64_t debt, progress, advance, lat_steps, driving, len;
+  int32_t reached, bind;
+  __device__ __forceinline__ void load(const DevWorld& w, int32_t vid, int32_t slot) {
+    const DevVehicles& v = w.v;
+    debt = v.latency_debt[vid];
+    progress = v.progress[vid];
+    advance = v.advance[vid];
+    lat_steps = v.lat_steps[vid];
+    driving = v.driving[vid];
+    len = w.g.len[slot];
+    reached = w.g.col[slot];
+    bind = w.g.bind[slot];
+  }
+};
+
+// E2 (engine.cpp:221-261) for a vehicle whose state words are in registers:
+// st, depart, its edge slot and dest, and -- when st == kOnEdge -- MoveWords.
+__device__ __forceinline__ void veh_move_core(const DevWorld& w, int32_t vid, int64_t step, uint8_t st,
+                                              int64_t depart, int32_t slot, int32_t dest, const MoveWords& m,
+                                              long long& active, long long& unfinished) {
+  const DevVehicles& v = w.v;
+  if (st == kOnEdge) {
+    const int64_t prog = m.progress + m.advance;
+    const int64_t L = m.len;
+    if (m.debt >= w.p.dt_us) {
+      v.latency_debt[vid] = m.debt - w.p.dt_us;
+      v.lat_steps[vid] = m.lat_steps + 1;
+    } else {
+      v.driving[vid] = m.driving + 1;
+      if (prog < L) {
+        v.progress[vid] = prog;
+      } else {
+        if (m.reached == dest) {
+          st = kArrived;
+          v.progress[vid] = prog;
+          v.arrive[vid] = step + 1;
+          if (w.p.deposit == 0 && (w.p.algorithm == 1 || w.p.algorithm == 4)) {
+            const int32_t n = v.path_n[vid];
+            if (n > 0) {
+              const double km = __ddiv_rn((double)v.path_len_mm[vid], 1e6);
+              const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
+              const int32_t* path = v.path + (size_t)vid * w.p.path_cap;
+              for (int i = 0; i < n; ++i) atomicAdd((unsigned long long*)&w.dep[path[i]], (unsigned long long)amount);
+            }
+          }
+        } else if (m.bind >= 0) {
+          st = kQueued;
+          v.at_node[vid] = m.reached;
+          v.queued_phase[vid] = m.bind & 7;
+          v.joined[vid] = step + 1;
+          v.progress[vid] = 0;
+          v.arr_next[vid] = atomicExch(&w.s.arr_head[m.bind], vid);
+          if (w.p.e1_in_walk) atomicAdd(w.s.arr_cnt + (step & 1) * (int64_t)w.p.S * kPhases + m.bind, 1);
+        } else {
+          st = kAtNode;
+          v.at_node[vid] = m.reached;
+          v.overshoot[vid] = prog - L;
+          v.progress[vid] = 0;
+        }
+        v.state[vid] = st;
+      }
+    }
+    if (st == kOnEdge) atomicAdd(&w.occ_new[slot], 1);
+  }
+  active += st == kAtNode || st == kOnEdge || st == kQueued || st == kReleased ||
+            (st == kPending && depart == step + 1);
+  unfinished += st != kArrived && st != kRetired;
+}
+
+// E2 for a vehicle whose state words are in registers (st, depart, on_edge,
+// dest): one round of loads (the edge's words included), then the stores.
+__device__ __forceinline__ void veh_move_from(const DevWorld& w, int32_t vid, int64_t step, uint8_t st,
+                                              int64_t depart, int32_t slot, int32_t dest, long long& active,
+                                              long long& unfinished) {
+  MoveWords m{};
+  if (st == kOnEdge) m.load(w, vid, slot);
+  veh_move_core(w, vid, step, st, depart, slot, dest, m, active, unfinished);
+}
+
+// E2 for one vehicle: its state words, then the edge's and the motion words
+// (two memory round trips).
+__device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished) {
+  const DevVehicles& v = w.v;
+  const int64_t step = w.ctl->step;
+  const uint8_t st = v.state[vid];
+  const int64_t depart = v.depart[vid];
+  const int32_t slot = v.on_edge[vid];
+  const int32_t dest = v.dest[vid];
+  veh_move_from(w, vid, step, st, depart, slot, dest, active, unfinished);
+}
+
 
 // Winner epilogue: plan bookkeeping, best-tour deposit (exact int64 sums,
 // deposit_amount pheromone.cpp:73-78) and, at a node, the first hop.
@@ -1833,7 +1941,10 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       return;
     }
   }
-  if (threadIdx.x == 0) trace_min(w.ctl, 0);
+  if (threadIdx.x == 0) {
+    trace_min(w.ctl, 0);
+    TRACE_FINE(7);  // the last walk CTA's start
+  }
   constexpr int kMaxVpb = 256;
   __shared__ unsigned long long best[kMaxVpb];
   __shared__ int32_t start_s[kMaxVpb];
@@ -1866,15 +1977,21 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   unsigned long long* const bits_w =
       reinterpret_cast<unsigned long long*>(dyn_smem + (kSmem ? grid_staged_bytes_dev(w) : 0));
   long long act = 0, unf = 0;  // next step's count_active / unfinished (fused motion)
+  // a vehicle that does not walk moves (E2) after the block barrier below,
+  // beside the walks, from the words its prologue loaded
+  bool move_later = false;
+  uint8_t st = 0;
+  int64_t depart = 0;
+  int32_t on_edge = 0, dest = 0;
   if (live && ant == 0) {
     // the vehicle's words in one round of loads, ahead of any store (the
     // prologue runs beside the table staging and must not outlast it)
-    uint8_t st = v.state[vid];
-    const int64_t depart = v.depart[vid];
+    st = v.state[vid];
+    depart = v.depart[vid];
     int32_t at = v.at_node[vid];
     const int32_t origin = v.origin[vid];
-    const int32_t on_edge = v.on_edge[vid];
-    const int32_t dest = v.dest[vid];
+    on_edge = v.on_edge[vid];
+    dest = v.dest[vid];
     if (st == kPending && depart == step) {  // engine.cpp:177-180
       st = kAtNode;
       at = origin;
@@ -1898,11 +2015,13 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     start_s[lv] = start;
     deciding_s[lv] = deciding;
     if (w.p.sharded) v.dec_rec[vid] = -1;
-    if (start < 0) veh_move(w, vid, act, unf);  // E2 now: stage B leaves this vehicle untouched
+    move_later = start < 0;  // E2 below: stage B leaves this vehicle untouched
     done_s[lv] = 0;
     best[lv] = ~0ull;
   }
   __syncthreads();
+  if (threadIdx.x == 0) TRACE_FINE(10);  // vehicle prologue done
+  if (move_later) veh_move_from(w, vid, step, st, depart, on_edge, dest, act, unf);
   if (kSmem) {  // TMA tables landed (phase 0 of the staging mbarrier)
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
     asm volatile(
@@ -2041,6 +2160,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
       walk_counters_from_bits(bits_w + threadIdx.x * nw, n, abs(rd - rx), abs(cd - cx), rx, cx, dr, dc, rows, cols,
                               idegs, n_two);
     }
+    if (ant == 0) TRACE_FINE(8);  // walk loop done (all ants of a vehicle walk n hops)
     cost = (int64_t)w.d.grid_len * ((int64_t)n + lsum);  // = the sum of the hops' len * (1 + load)
     if (capped) cost = kInf;
     hops = n;
@@ -2050,11 +2170,6 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
     if (kTour == kTourBits && (K & 31) == 0) {
-      // Whole-warp colonies: a per-vehicle named barrier (id 1+lv, K
-      // threads), then warp 0 of the vehicle runs the epilogue in parallel —
-      // lane i rebuilds hops i and i+32 directly from the winner's move bits
-      // (node after i hops = start + step_v*popc(first i bits) + step_h*rest)
-      // and issues their deposits; lane 0 does the bookkeeping and motion.
       if (kOneVeh)
         asm volatile("bar.sync 1, %0;" ::"r"(K) : "memory");
       else
@@ -2092,9 +2207,10 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
             const unsigned mv0 = (unsigned)(wb[0] >> 63) & 1u;
             take_edge(w, vid, 4 * start + (mv0 ? off_v : off_h), false, start);
           }
+          veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
           routes = 1;
           decided = deciding;
-          veh_move(w, vid, act, unf);  // E2 right after this vehicle's stage B
+          TRACE_FINE(9);  // vehicle epilogue done
         }
       }
     } else {
@@ -2272,66 +2388,6 @@ __device__ __forceinline__ long long sig_cde1(const DevWorld& w, int32_t s) {
 // engine.cpp:341-346; per-edge sum-then-clamp equals sequential clamping for
 // amounts >= 0), queue arrival push, occupancy histogram (engine.cpp:316-322)
 // and the next step's count_active / unfinished contributions.
-__device__ __forceinline__ void veh_move(const DevWorld& w, int32_t vid, long long& active, long long& unfinished) {
-  const DevVehicles& v = w.v;
-  const int64_t step = w.ctl->step;
-  // the vehicle's words, then its edge's, each in one round of loads ahead
-  // of any store (the compiler may not move a load past an aliasing store)
-  uint8_t st = v.state[vid];
-  const int64_t depart = v.depart[vid];
-  if (st == kOnEdge) {
-    const int64_t debt = v.latency_debt[vid];
-    const int64_t prog = v.progress[vid] + v.advance[vid];
-    const int32_t slot = v.on_edge[vid];
-    const int32_t dest = v.dest[vid];
-    const int64_t L = w.g.len[slot];
-    const int32_t reached = w.g.col[slot];
-    const int32_t bind = w.g.bind[slot];
-    if (debt >= w.p.dt_us) {
-      v.latency_debt[vid] = debt - w.p.dt_us;
-      v.lat_steps[vid] += 1;
-    } else {
-      v.driving[vid] += 1;
-      if (prog < L) {
-        v.progress[vid] = prog;
-      } else {
-        if (reached == dest) {
-          st = kArrived;
-          v.progress[vid] = prog;
-          v.arrive[vid] = step + 1;
-          if (w.p.deposit == 0 && (w.p.algorithm == 1 || w.p.algorithm == 4)) {
-            const int32_t n = v.path_n[vid];
-            if (n > 0) {
-              const double km = __ddiv_rn((double)v.path_len_mm[vid], 1e6);
-              const int64_t amount = llround(__dmul_rn(__ddiv_rn(w.p.deposit_q, km), 1e6));
-              const int32_t* path = v.path + (size_t)vid * w.p.path_cap;
-              for (int i = 0; i < n; ++i) atomicAdd((unsigned long long*)&w.dep[path[i]], (unsigned long long)amount);
-            }
-          }
-        } else if (bind >= 0) {
-          st = kQueued;
-          v.at_node[vid] = reached;
-          v.queued_phase[vid] = bind & 7;
-          v.joined[vid] = step + 1;
-          v.progress[vid] = 0;
-          v.arr_next[vid] = atomicExch(&w.s.arr_head[bind], vid);
-          if (w.p.e1_in_walk) atomicAdd(w.s.arr_cnt + (step & 1) * (int64_t)w.p.S * kPhases + bind, 1);
-        } else {
-          st = kAtNode;
-          v.at_node[vid] = reached;
-          v.overshoot[vid] = prog - L;
-          v.progress[vid] = 0;
-        }
-        v.state[vid] = st;
-      }
-    }
-    if (st == kOnEdge) atomicAdd(&w.occ_new[slot], 1);
-  }
-  active += st == kAtNode || st == kOnEdge || st == kQueued || st == kReleased ||
-            (st == kPending && depart == step + 1);
-  unfinished += st != kArrived && st != kRetired;
-}
-
 // E3 for one signal: enqueue commit in ascending vid (engine.cpp:297-301) and
 // timers (engine.cpp:303-314).  This step's arrivals all share joined =
 // step+1, larger than every queued key, so FIFO order = old queue then the
@@ -3017,8 +3073,10 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
           int32_t load = 0;
           m = max(m, slot_fg(w, (int32_t)i, &wt, &load));
           if (w.lrec) lattice_quad(w, i, wt, load);  // (M = 4 n: whole quads take this branch)
+          TRACE_FINE(4);
         } else {
           sig_e3(w, (int32_t)(i - M));
+          TRACE_FINE(5);
         }
       }
       const int32_t nrel = w.ctl->nrel;
@@ -3028,14 +3086,15 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       if (threadIdx.x == 0) {
         if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
         trace_max(w.ctl, 6);
-        __threadfence();
-        is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+        // release: the block's stores (ordered before thread 0 by block_max's
+        // barrier) and its atomicMax; acquire: the last block sees every
+        // block's, and its threads see them after the barrier below
+        is_last = atom_add_acq_rel(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
       }
       __syncthreads();
       if (is_last && threadIdx.x == 0) {
-        __threadfence();
-        finalize_step(w);
-        __threadfence();
+        finalize_step(w);  // the kernel's completion publishes it
+        TRACE_FINE(11);
       }
       if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
       return;
