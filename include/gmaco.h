@@ -330,9 +330,9 @@ int gmaco_next_node(gmaco_engine* h, int32_t algorithm, int32_t count, const int
 int gmaco_last_timing(gmaco_engine* h, double* walk_ms, double* step_ms, int64_t* walk_launches);
 int gmaco_set_timing(gmaco_engine* h, int32_t enabled);
 /* Profiling hook: runs `steps` steps and returns the last one's stage
- * timestamps (ns, %globaltimer, 12 slots; see DevCtl::trace in
+ * timestamps (ns, %globaltimer, 16 slots; see DevCtl::trace in
  * paper_2010_14244_b200/csrc/device.cuh). */
-int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12);
+int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out16);
 /* Memory check of a world created with GMACO_OPT_REDZONES: settles the
  * stream and verifies every guard band around the engine's device arrays.
  * *corrupted receives the number of overwritten guards (0 = no out-of-bounds

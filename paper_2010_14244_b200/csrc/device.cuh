@@ -132,9 +132,9 @@ struct DevCtl {
   alignas(128) int32_t max_occ_acc;  // atomicMax target of stage F+G
   // stage trace of the current step (%globaltimer ns; written when trace_on
   // is set): [0] walk start (min), [1] walk staging done (max), [2] walk end
-  // (max), [3] tail start (min), [4]/[7]-[11] probes, [5] signals done,
+  // (max), [3] tail start (min), [4]/[7]-[15] probes, [5] signals done,
   // [6] F+G done
-  alignas(128) unsigned long long trace[12];
+  alignas(128) unsigned long long trace[16];
 };
 
 struct DevVehicles {

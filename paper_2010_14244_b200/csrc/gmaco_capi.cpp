@@ -2850,21 +2850,21 @@ int gmaco_bench_steps(gmaco_engine* h, int32_t steps, int64_t flush_bytes, doubl
 
 // Profiling hook: stage timestamps (%globaltimer ns) of the next `steps`
 // steps' LAST step; see DevCtl::trace.  Not part of the reference surface.
-int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out12) {
+int gmaco_debug_trace(gmaco_engine* h, int32_t steps, uint64_t* out16) {
   if (h) h->ctl_valid = false;
-  if (!h || !out12) return GMACO_EVALIDATION;
+  if (!h || !out16) return GMACO_EVALIDATION;
   return guarded(h, [&] {
     for (int32_t i = 0; i < steps; ++i) {
       DevCtl t;
       CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
       t.trace_on = 1;
-      for (int k = 0; k < 12; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
+      for (int k = 0; k < 16; ++k) t.trace[k] = (k == 0 || k == 3) ? ~0ull : 0ull;
       h2d(h, h->ctl, &t, sizeof t);
       run_steps(h, 1);
     }
     DevCtl t;
     CK(cudaMemcpy(&t, h->ctl, sizeof t, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < 12; ++k) out12[k] = t.trace[k];
+    for (int k = 0; k < 16; ++k) out16[k] = t.trace[k];
     t.trace_on = 0;
     h2d(h, h->ctl, &t, sizeof t);
   });

@@ -1927,6 +1927,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   if (skip_step(w.ctl)) return;
   if ((int)blockIdx.x == nsig) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
+    if (threadIdx.x == 0) TRACE_FINE(11);  // prefetch CTA done
     return;
   }
   if (w.p.e1_in_walk) {  // stages C, D, E1, concurrent with B
@@ -1938,6 +1939,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
         qt += sig_cde1<true>(w, s);
       qt = block_sum(qt, redq);
       if (threadIdx.x == 0 && qt) atomicAdd((unsigned long long*)&w.ctl->qtotal, (unsigned long long)qt);
+      if (threadIdx.x == 0) TRACE_FINE(15);  // signal CTA done
       return;
     }
   }
@@ -2170,10 +2172,12 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
     const uint64_t cc = cost >= (int64_t)kCostCap ? kCostCap : (uint64_t)cost;
     atomicMin(&best[lv], (cc << 10) | (uint64_t)ant);
     if (kTour == kTourBits && (K & 31) == 0) {
+      if (ant == 32) TRACE_FINE(12);  // the vehicle's second warp's walk done
       if (kOneVeh)
         asm volatile("bar.sync 1, %0;" ::"r"(K) : "memory");
       else
         asm volatile("bar.sync %0, %1;" ::"r"(1 + lv), "r"(K) : "memory");
+      if (ant == 0) TRACE_FINE(13);  // past the vehicle's barrier
       if (ant < 32) {
         const int winner = (int)(best[lv] & 1023u);
         const unsigned long long* wb = bits_w + (size_t)(lv * K + winner) * nw;
@@ -2199,6 +2203,7 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
           before += __popcll(word);
         }
         if (ant == 0) {
+          TRACE_FINE(14);  // tour rebuilt, deposits issued
           const bool deciding = deciding_s[lv];
           v.plan_n[vid] = hops;
           v.plan_step[vid] = step;
@@ -2442,6 +2447,50 @@ __device__ __forceinline__ void sig_e3(const DevWorld& w, int32_t s) {
     S.head_wait[k0 + ph] = len[ph] == 0 ? 0.0 : __dmul_rn((double)(now - joined[ph]), w.p.dt_s);
   S.el_steps[s] = e;
   S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
+}
+
+// E3 for one queue k = s * kPhases + ph: the per-queue body of sig_e3, for
+// the one-pass colony tail (one thread per queue, so a signal's queues with
+// arrivals no longer chain their round trips one after another).  A kept
+// head's joined step is loaded beside the arrival chain: appends do not move
+// a non-empty queue's head, and a queue that was empty gets an arrival head,
+// whose joined step is now (veh_move_core).
+__device__ __forceinline__ void queue_e3(const DevWorld& w, int32_t k) {
+  const DevSignals& S = w.s;
+  const int64_t now = w.ctl->step + 1;
+  const int32_t s = k / kPhases;
+  const bool first = k == s * kPhases;  // the signal's phase-0 queue also advances its clock
+  const int32_t chain = S.arr_head[k];
+  const int32_t len0 = S.qlen[k], head0 = S.qhead[k], tail0 = S.qtail[k];
+  const int64_t e = first ? S.el_steps[s] + 1 : 0;
+  const int64_t jh = len0 ? w.v.joined[head0] : now;
+  int32_t n = len0;
+  if (chain >= 0) {
+    S.arr_head[k] = -1;
+    int32_t hd = head0, tail = tail0, last = -1;
+    for (;;) {  // append chain members in ascending vid (selection; chains are short)
+      int32_t best = INT32_MAX;
+      for (int32_t c = chain; c >= 0; c = w.v.arr_next[c])
+        if (c > last && c < best) best = c;
+      if (best == INT32_MAX) break;
+      w.v.qnext[best] = -1;
+      if (tail < 0)
+        hd = best;
+      else
+        w.v.qnext[tail] = best;
+      tail = best;
+      ++n;
+      last = best;
+    }
+    S.qhead[k] = hd;
+    S.qtail[k] = tail;
+    S.qlen[k] = n;
+  }
+  S.head_wait[k] = n == 0 ? 0.0 : __dmul_rn((double)(now - jh), w.p.dt_s);
+  if (first) {
+    S.el_steps[s] = e;
+    S.el_s[s] = __dmul_rn((double)e, w.p.dt_s);
+  }
 }
 
 // F (scoped MACO) for one decision node: replay the step's decisions at that
@@ -3063,22 +3112,24 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       // E3 || F+G in one pass (F+G's queue loads come from qlen_e1 + the
       // arrival counters), the kReleased fix-up, and the last block to finish
       // finalizes the step: no grid-wide barrier at all
-      // one index space (slots, then signals) so that no thread chains a
-      // signal's E3 after a slot's F+G when the grid covers both
+      // one index space (slots, then queues: E3 per queue) so that no thread
+      // chains a queue's E3 after a slot's F+G when the grid covers both
       const int64_t M = w.g.M;
       int32_t m = 0;
-      for (int64_t i = gtid; i < M + p.S; i += gstride) {
+      for (int64_t i = gtid; i < M + (int64_t)p.S * kPhases; i += gstride) {
         if (i < M) {
           double wt = 0.0;
           int32_t load = 0;
           m = max(m, slot_fg(w, (int32_t)i, &wt, &load));
           if (w.lrec) lattice_quad(w, i, wt, load);  // (M = 4 n: whole quads take this branch)
-          TRACE_FINE(4);
         } else {
-          sig_e3(w, (int32_t)(i - M));
-          TRACE_FINE(5);
+          queue_e3(w, (int32_t)(i - M));
         }
       }
+#ifdef GMACO_TRACE_FINE
+      __syncwarp();  // one stamp per warp: [4] slot warps done, [5] queue warps done
+      if ((threadIdx.x & 31) == 0 && gtid < M + (int64_t)p.S * kPhases) TRACE_FINE(gtid < M ? 4 : 5);
+#endif
       const int32_t nrel = w.ctl->nrel;
       for (int64_t i = gtid; i < nrel; i += gstride) w.v.state[w.v.rel[i]] = kAtNode;
       m = block_max(m, smax);
@@ -3094,7 +3145,6 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
       __syncthreads();
       if (is_last && threadIdx.x == 0) {
         finalize_step(w);  // the kernel's completion publishes it
-        TRACE_FINE(11);
       }
       if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
       return;
@@ -3260,7 +3310,7 @@ int coop_tail_blocks(const DevWorld& w, int device) {
   if (oe != cudaSuccess || per_sm < 1) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
   // (colony worlds: slots and signals share one pass, see k_tail_coop)
-  const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M + (w.p.algorithm == 4 ? w.p.S : 0));
+  const int64_t work = std::max<int64_t>((int64_t)w.p.S + w.p.V, w.g.M + (w.p.algorithm == 4 ? (int64_t)w.p.S * kPhases : 0));
   const int64_t want = (work + kTailCoop - 1) / kTailCoop;
   return (int)std::min<int64_t>(want, (int64_t)per_sm * sms);
 }

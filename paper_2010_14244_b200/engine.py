@@ -249,7 +249,7 @@ class Engine:
 
     def debug_trace(self, steps: int = 1) -> np.ndarray:
         """Stage timestamps (ns) of the last of `steps` steps (DevCtl::trace)."""
-        out = np.zeros(12, dtype=np.uint64)
+        out = np.zeros(16, dtype=np.uint64)
         self._check(self.L.gmaco_debug_trace(self.h, steps, abi.ptr(out, u64)))
         return out
 

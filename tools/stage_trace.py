@@ -36,5 +36,7 @@ for V in (10, 1000):
             t = raw.astype(np.int64)
             rel = (t - t[0]) / 1e3
             print(f"{os.environ.get('TAG', '')} V={V} {mode:7s} walk: last CTA start {rel[7]:.2f} prologue "
-                  f"{rel[10]:.2f} staged {rel[1]:.2f} loop end {rel[8]:.2f} epilogue end {rel[9]:.2f} end {rel[2]:.2f} | "
-                  f"tail start {rel[3]:.2f} slots {rel[4]:.2f} signals {rel[5]:.2f} FG {rel[6]:.2f} finalized {rel[11]:.2f} (us)")
+                  f"{rel[10]:.2f} staged {rel[1]:.2f} loop end {rel[8]:.2f} (warp 1 {rel[12]:.2f}) barrier "
+                  f"{rel[13]:.2f} rebuilt {rel[14]:.2f} epilogue end {rel[9]:.2f} end {rel[2]:.2f} signal CTAs "
+                  f"{rel[15]:.2f} prefetch CTA {rel[11]:.2f} | tail start {rel[3]:.2f} slots {rel[4]:.2f} "
+                  f"signals {rel[5]:.2f} FG {rel[6]:.2f} (us)")
