@@ -34,9 +34,10 @@ for V in (10, 1000):
                 torch.cuda.synchronize()
             raw = e.debug_trace(1)
             t = raw.astype(np.int64)
-            rel = (t - t[0]) / 1e3
-            print(f"{os.environ.get('TAG', '')} V={V} {mode:7s} walk: last CTA start {rel[7]:.2f} prologue "
-                  f"{rel[10]:.2f} staged {rel[1]:.2f} loop end {rel[8]:.2f} (warp 1 {rel[12]:.2f}) barrier "
-                  f"{rel[13]:.2f} rebuilt {rel[14]:.2f} epilogue end {rel[9]:.2f} end {rel[2]:.2f} signal CTAs "
-                  f"{rel[15]:.2f} prefetch CTA {rel[11]:.2f} | tail start {rel[3]:.2f} slots {rel[4]:.2f} "
-                  f"signals {rel[5]:.2f} FG {rel[6]:.2f} (us)")
+            # fine stamps (-DGMACO_TRACE_FINE builds) are 0 in the product build
+            rel = [(x - t[0]) / 1e3 if x else None for x in t]
+            names = [(7, "last CTA start"), (10, "prologue"), (1, "staged"), (8, "loop end"), (12, "warp 1"),
+                     (13, "barrier"), (14, "rebuilt"), (9, "epilogue end"), (2, "end"), (15, "signal CTAs"),
+                     (11, "prefetch CTA"), (3, "| tail start"), (4, "slots"), (5, "signals"), (6, "FG")]
+            cols = " ".join(f"{n} {rel[i]:.2f}" for i, n in names if rel[i] is not None)
+            print(f"{os.environ.get('TAG', '')} V={V} {mode:7s} walk: {cols} (us)")
