@@ -712,6 +712,23 @@ def run_ours(args, rank, world, local):
     note = ("latency-bound: one colony iteration is a ~15 us dependent walk over L2/SMEM-resident state "
             "(~1 MB), see DESIGN.md §7" if args.config in ("c1", "c2") else
             "throughput-bound gather walk, see DESIGN.md §7")
+    if args.algorithm == "colony" and args.config in ("c3", "c5"):
+        note = ("frac is of the SURVEY 8(d) byte model, which counts every table read a walk makes; the lattice "
+                "walker serves them from L1/L2 (real DRAM traffic per launch: 'traffic'), so frac > 1 is on-chip "
+                "reuse, not HBM above its peak. The kernel's real limiter is in 'limiter' (ncu): issue and the "
+                "dependent L1/L2 round trip per hop, see DESIGN.md §7")
+    limiter = None
+    try:  # the walk kernel's ncu limiter (committed capture of the same workload)
+        cap = {"c2": "c2_walk", "c3": "c3_walk", "c5": "c5_walk", "c4": "c4_qt"}[args.config]
+        with open(os.path.join(ROOT, "profiles", f"r02_ncu_{cap}.json")) as f:
+            rep = json.load(f)
+        rep = rep[0] if isinstance(rep, list) else rep
+        limiter = {"source": f"profiles/r02_ncu_{cap}.json", "issue_active_pct": float(rep["issue_active_%"].split()[0]),
+                   "l1_lsu_wavefronts_pct": float(rep["l1_lsu_wavefronts_%"].split()[0]),
+                   "top_stalls_pct": dict(list(rep["stalls_%"].items())[:3]),
+                   "dram_gbps": (traffic / walk_avg_s / 1e9) if (traffic and walk_avg_s > 0) else None}
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
     line = {
         "metric": "ant-steps/sec",
         "value": tot_steps / t_dev,
@@ -741,6 +758,7 @@ def run_ours(args, rank, world, local):
                      "algorithmic_bytes_per_launch": alg_bytes / launches,
                      "algorithmic_bytes_model": "SURVEY 8(d): 8 + 4d + 4d(table dist) + 12c + 4(tour) per ant-step",
                      "avg_launch_us": walk_avg_s * 1e6,
+                     "limiter": limiter if args.algorithm == "colony" else None,
                      "note": note},
         "e2e": {"value": tot_e2e / e2e_dt, "unit": "ant-steps/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
