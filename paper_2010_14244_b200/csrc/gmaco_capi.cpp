@@ -441,10 +441,25 @@ struct DevBuffers {
   T* upload_one(const T& v) {
     return upload(std::vector<T>{v});
   }
+  // Starts the copies of every arena chunk's not-yet-sent range (stream-
+  // ordered, no wait): the DMA overlaps the host work that fills the next
+  // ranges.  A shadow range is written only when it is carved (upload /
+  // filled), so a range once sent is never written on the host again.
+  void flush_async() {
+    for (auto& ch : chunks)
+      if (ch.used > ch.sent) {
+        CK(cudaMemcpyAsync(ch.dev + ch.sent, ch.shadow + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice,
+                           stream));
+        ch.sent = ch.used;
+        pending = true;
+      }
+  }
+  bool pending = false;  // copies started by flush_async, not yet waited for
   // Sends every arena chunk's not-yet-sent range to the device (one copy per
   // chunk); ranges already sent are device-authoritative from then on.
   void flush() {
-    bool any = false;
+    bool any = pending;
+    pending = false;
     for (auto& ch : chunks)
       if (ch.used > ch.sent) {
         CK(cudaMemcpyAsync(ch.dev + ch.sent, ch.shadow + ch.sent, ch.used - ch.sent, cudaMemcpyHostToDevice,
@@ -1188,6 +1203,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   w.g.slot_edge = B.upload(h->slot_edge);
   w.g.slot_from = B.upload(slot_from);
   w.g.eta_beta = B.upload(eta);
+  B.flush_async();  // the graph's arrays travel while the host builds the rest
 
   pt.mark("graph slots + upload");
   // ---- params ----------------------------------------------------------------
@@ -1375,6 +1391,7 @@ void build_world(gmaco_engine* h, const gmaco_graph_desc* gd, const gmaco_distan
   ds.arr_head = B.filled<int32_t>((size_t)S * kPhases, -1);
   ds.head_wait = B.filled<double>((size_t)S * kPhases, 0.0);
   ds.rem = B.filled<double>((size_t)S * kPhases, 0.0);
+  B.flush_async();
 
   pt.mark("params, tables, pheromone, signals");
   // ---- vehicles ------------------------------------------------------------
