@@ -1924,7 +1924,33 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   // the walk slot's vehicle is loaded in the same memory round trip as the
   // control block (its load does not depend on the step check below)
   const int32_t vid = (w.v.walk_order && live) ? w.v.walk_order[slot] : slot;
-  if (skip_step(w.ctl)) return;
+  // Stage this step's LatRec table in shared memory with one TMA bulk copy
+  // (cp.async.bulk) completing on an mbarrier, issued first thing: it does
+  // not wait for the step check's round trip, and the prologue below
+  // overlaps it.  (The table is the previous tail's output, complete at
+  // launch: this kernel is not a programmatic dependent.)
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  __shared__ __align__(8) uint64_t stage_bar;
+  const bool stages = kSmem && (int)blockIdx.x > nsig;
+  if (stages && threadIdx.x == 0) {
+    const uint32_t bR = 16u * (uint32_t)w.g.M;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dyn_smem);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bR) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(w.lrec), "r"(bR), "r"(bar) : "memory");
+  }
+  if (skip_step(w.ctl)) {
+    if (stages && threadIdx.x == 0) {  // the copy lands before the CTA's shared memory is released
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+      asm volatile(
+          "{\n .reg .pred p;\n WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAITS_%=;\n}" ::"r"(bar)
+          : "memory");
+    }
+    return;
+  }
   if ((int)blockIdx.x == nsig) {  // dedicated prefetch block: stages C..G's state into L2
     if (w.p.prefetch) prefetch_tail_state(w);
     if (threadIdx.x == 0) TRACE_FINE(11);  // prefetch CTA done
@@ -1954,27 +1980,9 @@ __global__ void __launch_bounds__(256, 2) k_colony_grid(DevWorld w) {
   __shared__ uint8_t deciding_s[kMaxVpb];
   __shared__ long long red5[7][32];
   // move-bit words [blockDim][bit_words] after the staged tables (kTourBits)
-  extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int64_t step = w.ctl->step;
   const DevVehicles& v = w.v;
-  const LatRec* __restrict__ R = w.lrec;
-  __shared__ __align__(8) uint64_t stage_bar;
-  if (kSmem) {
-    // Stage this step's LatRec table in shared memory with one TMA bulk copy
-    // (cp.async.bulk) completing on an mbarrier; the other threads overlap
-    // the vehicle prologue below.
-    const uint32_t bR = 16u * (uint32_t)w.g.M;
-    if (threadIdx.x == 0) {
-      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dyn_smem);
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bR) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst), "l"(w.lrec), "r"(bR), "r"(bar) : "memory");
-    }
-    R = reinterpret_cast<const LatRec*>(dyn_smem);
-  }
+  const LatRec* __restrict__ R = kSmem ? reinterpret_cast<const LatRec*>(dyn_smem) : w.lrec;
   const int nw = w.p.bit_words;
   unsigned long long* const bits_w =
       reinterpret_cast<unsigned long long*>(dyn_smem + (kSmem ? grid_staged_bytes_dev(w) : 0));
