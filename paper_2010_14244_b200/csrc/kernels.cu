@@ -2598,8 +2598,26 @@ __device__ __forceinline__ void lattice_quad(const DevWorld& w, int64_t s, doubl
 // deposit sum-then-clamp, evaporation (pheromone.cpp:61-67), colony
 // congestion term, occupancy hand-off, next step's weight / tour cost
 // (routing.cpp:90-94).  Returns the slot's occupancy (for the running max).
+// A slot's words that no step changes (the graph's) and the step parity,
+// loaded by a programmatic-dependent tail before it waits for the walk:
+// the slot's F+G is then one memory round trip after the wait, not two.
+struct SlotStatic {
+  double eta;
+  int64_t len;
+  int32_t bind;
+  int32_t par;
+  __device__ __forceinline__ void load(const DevWorld& w, int32_t s) {
+    const int alg = w.p.algorithm;
+    const bool aco = alg == 1 || alg == 4;
+    eta = aco ? w.g.eta_beta[s] : 0.0;
+    len = aco ? w.g.len[s] : 0;
+    bind = (alg == 4 && w.p.congestion) ? w.g.bind[s] : -1;
+    par = (int32_t)(w.ctl->step & 1);  // (finalize of the previous step wrote it)
+  }
+};
+
 __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s, double* wt_out = nullptr,
-                                           int32_t* load_out = nullptr) {
+                                           int32_t* load_out = nullptr, const SlotStatic* pre = nullptr) {
   const DevParams& p = w.p;
   const int alg = p.algorithm;
   const bool aco = alg == 1 || alg == 4;
@@ -2609,10 +2627,10 @@ __device__ __forceinline__ int32_t slot_fg(const DevWorld& w, int32_t s, double*
   int64_t t = w.tau[s];
   const int32_t occ = w.occ_new[s];
   const int64_t d = aco ? w.dep[s] : 0;
-  const double eta = aco ? w.g.eta_beta[s] : 0.0;
-  const int64_t len = aco ? w.g.len[s] : 0;
-  const int32_t b = (alg == 4 && p.congestion) ? w.g.bind[s] : -1;
-  const int64_t par = (b >= 0 && p.e1_in_walk) ? (w.ctl->step & 1) : 0;
+  const double eta = pre ? pre->eta : (aco ? w.g.eta_beta[s] : 0.0);
+  const int64_t len = pre ? pre->len : (aco ? w.g.len[s] : 0);
+  const int32_t b = pre ? pre->bind : ((alg == 4 && p.congestion) ? w.g.bind[s] : -1);
+  const int64_t par = (b >= 0 && p.e1_in_walk) ? (pre ? pre->par : (w.ctl->step & 1)) : 0;
   int32_t q = 0;  // the queue's length after E3
   if (b >= 0)
     q = p.e1_in_walk ? w.s.qlen_e1[b] + w.s.arr_cnt[par * (int64_t)p.S * kPhases + b] : w.s.qlen[b];
@@ -3083,6 +3101,12 @@ __global__ void __launch_bounds__(kTailCoop) k_run_coop(DevWorld w, int64_t nste
 
 template <bool kFusedMotion, int kDecideDK>
 __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
+  // the first slot's static words, loaded while the walk still runs (PDL
+  // early launch); nothing the walk writes is read before the wait below
+  SlotStatic pre{};
+  const int64_t gtid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool have_pre = kFusedMotion && w.p.e1_in_walk && gtid0 < w.g.M;
+  if (have_pre) pre.load(w, (int32_t)gtid0);
   griddep_wait();  // PDL: the preceding kernel (walk) completed and its writes are visible
   if (skip_step(w.ctl)) {  // grid-uniform: ctl changes only in the finalize below
     if (blockIdx.x == 0 && w.snap) block_snapshot(w.snap);  // a no-op step still snapshots the state
@@ -3128,7 +3152,7 @@ __global__ void __launch_bounds__(kTailCoop) k_tail_coop(DevWorld w) {
         if (i < M) {
           double wt = 0.0;
           int32_t load = 0;
-          m = max(m, slot_fg(w, (int32_t)i, &wt, &load));
+          m = max(m, slot_fg(w, (int32_t)i, &wt, &load, (have_pre && i == gtid) ? &pre : nullptr));
           if (w.lrec) lattice_quad(w, i, wt, load);  // (M = 4 n: whole quads take this branch)
         } else {
           queue_e3(w, (int32_t)(i - M));
