@@ -185,6 +185,28 @@ def test_colony_production_stepwise(ants):
     assert O.results_identical(gpu.run(), cpu.run())
 
 
+def test_colony_dense_queues_stepwise():
+    """Congested lattice colony (800 vehicles on a 5x5 all-signalized grid):
+    many arrivals join one queue in one step, so the tail's per-queue E3
+    (one thread per signal queue) appends long arrival chains in ascending
+    vid (commit_enqueue, engine.cpp:297-301).  Every step's full state is
+    compared with the oracle, and the run must have produced such chains."""
+    net = networks.grid(5, 5, signals="all")
+    cfg = abi.colony_production(_cfg("colony", 800, 21, max_steps=80, controller=abi.PREEMPTIVE), ants=32)
+    gpu = Engine(net, cfg, net.grid_distance())
+    cpu = O.PortWorld(net, cfg, net.grid_distance())
+    prev = gpu.signals()["queue_len"].astype(np.int64)
+    most = 0
+    for _ in range(40):
+        assert gpu.step(1) == cpu.step(1)
+        _same_snapshot(gpu, cpu, f"dense colony step {cpu.current_step()}")
+        cur = gpu.signals()["queue_len"].astype(np.int64)
+        most = max(most, int((cur - prev).max()))
+        prev = cur
+    assert most >= 3, f"no queue took 3 or more arrivals in one step (max {most})"
+    assert O.results_identical(gpu.run(), cpu.run())
+
+
 def test_colony_no_filter_tabu():
     """Progress filter off: tabu tenure + hop cap (cycles possible)."""
     net = networks.grid(8, 8)
