@@ -2820,16 +2820,10 @@ __global__ void __launch_bounds__(256) k_edges(DevWorld w) {
   const int32_t m = block_max(occ, smax);
   if (threadIdx.x == 0) {
     if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
-    __threadfence();
-    const unsigned prev = atomicAdd(&w.ctl->blocks_done, 1u);
-    is_last = prev == gridDim.x - 1;
+    is_last = atom_add_acq_rel(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {
-    __threadfence();
-    finalize_step(w);
-    __threadfence();
-  }
+  if (is_last && threadIdx.x == 0) finalize_step(w);  // the kernel's completion publishes it
   if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
 }
 
@@ -2949,15 +2943,11 @@ __device__ __forceinline__ void step_end(const DevWorld& w, int32_t m, int32_t* 
     if (threadIdx.x == 0) {
       if (m > 0) atomicMax(&w.ctl->max_occ_acc, m);
       trace_max(w.ctl, 6);
-      __threadfence();
-      is_last = atomicAdd(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
+      // release the block's stores, acquire every block's (see k_tail_coop)
+      is_last = atom_add_acq_rel(&w.ctl->blocks_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (is_last && threadIdx.x == 0) {
-      __threadfence();
-      finalize_step(w);
-      __threadfence();
-    }
+    if (is_last && threadIdx.x == 0) finalize_step(w);  // the kernel's completion publishes it
     if (is_last && w.snap) block_snapshot(w.snap);  // (is_last is block-uniform)
   } else if (threadIdx.x == 0 && m > 0) {
     atomicMax(&w.ctl->max_occ_acc, m);
